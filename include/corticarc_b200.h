@@ -1,0 +1,222 @@
+/*
+ * corticarc_b200.h - C ABI of the B200 engine for the per-millisecond loop of
+ * the DPSNN cortical simulator (arXiv 1803.08833; reference package
+ * `corticarc`, /root/reference/pkg/src/corticarc).
+ *
+ * Plain pointers and sizes only: every device buffer is owned by the caller
+ * (torch tensors in the Python host layer) and described to the library by a
+ * `cc_shard` value.  All launchers are asynchronous on the given stream,
+ * return 0 on success and a negative code on failure, with the message in
+ * cc_last_error() (thread-local).
+ *
+ * Each entry point replaces a piece of the reference's hot path; the
+ * reference interface it stands in for is cited per function.
+ */
+#ifndef CORTICARC_B200_H
+#define CORTICARC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CC_ABI_VERSION 3
+
+/* error bits raised by kernels into cc_ctl.error_bits */
+#define CC_ERR_SPIKE_LOG      0x01u  /* more spikes in one step than log capacity   */
+#define CC_ERR_PIECES         0x02u  /* delivery work list full                     */
+#define CC_ERR_OVERFLOW_BIN   0x04u  /* overflow record list full                   */
+#define CC_ERR_SCRATCH        0x08u  /* event staging scratch exhausted             */
+#define CC_ERR_POISSON        0x10u  /* Poisson draw budget exceeded (engine.py:187)*/
+#define CC_ERR_RASTER         0x20u  /* raster buffer full                          */
+#define CC_ERR_OUTLIST        0x40u  /* exchange out-list full                      */
+#define CC_ERR_GEN            0x80u  /* generator: row larger than planned          */
+
+/* Constants of one neuron population (model.py:44-86, NeuronBlock
+ * per-neuron arrays model.py:243-267).  k1 = tau_c - tau_m and
+ * k2 = tau_m * tau_c are pre-evaluated in float64 on the host (identical IEEE
+ * results to the reference's in-line expressions, model.py:133). */
+typedef struct cc_pop {
+    double tau_m, tau_c, E, V_theta, V_r, tau_arp, alpha_c, sfa, k1, k2;
+} cc_pop;
+
+/* Device-resident loop control and counters (one per shard). */
+typedef struct cc_ctl {
+    long long t;                          /* current step                     */
+    unsigned long long rec_events;        /* expanded recurrent events        */
+    unsigned long long ext_events;        /* generated external events        */
+    unsigned long long n_spikes;
+    unsigned long long raster_n;          /* entries in the raster buffer     */
+    unsigned int done_blocks;             /* last-block detection (neuron k.) */
+    unsigned int error_bits;
+    long long error_step;
+    unsigned int max_bin;                 /* max events at one (slot, neuron) */
+    unsigned int max_events;              /* max events of one neuron-step    */
+    unsigned long long scratch_used;      /* staging events spilled (this step) */
+    unsigned int out_n;                   /* exchange out-list fill           */
+    unsigned int pad0;
+    unsigned long long spilled_total;     /* neuron-steps that spilled smem   */
+    unsigned long long ovf_total;         /* records that went to overflow    */
+} cc_ctl;
+
+/* One shard's device state.  Layout documented in DESIGN.md section 3. */
+typedef struct cc_shard {
+    /* sizes and constants */
+    int32_t n_local;        /* neurons owned                                   */
+    int32_t n_col;          /* neurons per column                              */
+    int32_t n_exc_col;      /* excitatory slots per column                     */
+    int32_t d_max;          /* delay ring slots (SimConfig.d_max)              */
+    int32_t bin_cap;        /* K records per (slot, neuron) in the dense bins  */
+    int32_t log_slots;      /* d_max + 1                                       */
+    int32_t spk_cap;        /* spike-log entries per step                      */
+    int32_t piece_len;      /* synapses per delivery work piece                */
+    int64_t ovf_cap;        /* overflow records per slot                       */
+    int64_t piece_cap;      /* delivery pieces per step                        */
+    int64_t raster_cap;     /* raster entries                                  */
+    int64_t scratch_cap;    /* staging events (global spill)                   */
+    int64_t n_rows;         /* CSR rows (= global neuron count)                */
+    int32_t out_cap;        /* exchange out-list capacity                      */
+    int32_t ext_budget;     /* m = ceil(lam + 12 sqrt(lam)) + 20; 0 = no drive */
+    int32_t n_probe;
+    int32_t direct_log;     /* 1: neuron kernel feeds the delivery log itself  */
+    uint64_t h2_ext;        /* splitmix chain prefix for EXTERNAL (rng.py:85-86)      */
+    uint64_t h2_time;       /* ... for EXTERNAL_TIME                                  */
+    uint64_t h2_init;       /* ... for INIT_STATE                                     */
+    double dt;
+    double ext_weight;      /* float64 external weight (engine.py:377-378)     */
+    double ext_thresh;      /* exp(-lambda) evaluated with math.exp (engine.py:185) */
+    cc_pop pop[2];          /* 0 excitatory, 1 inhibitory                      */
+
+    /* neuron identity and state */
+    const uint32_t* gid;    /* [n_local] global id                             */
+    double* state;          /* [n_local][4] V, c, last_t, refr_until           */
+
+    /* incoming-synapse CSR, rows keyed by global source id (network.py:114-152) */
+    const int64_t* row_off; /* [n_rows + 1]                                    */
+    const int32_t* syn_tgt; /* [S] local target index                          */
+    const float* syn_w;     /* [S] weight, mV                                  */
+    const uint8_t* syn_d;   /* [S] delay, steps                                */
+
+    /* delay ring of event records (DelayRing, engine.py:124-163) */
+    uint32_t* bin_cnt;      /* [d_max][n_local]                                */
+    uint64_t* bin_rec;      /* [d_max][bin_cap][n_local] spike_ref | w_bits << 32 */
+    uint32_t* ovf_rec;      /* [d_max][ovf_cap][4] {tgt, spike_ref, w_bits, 0}  */
+    uint32_t* ovf_cnt;      /* [d_max]                                         */
+
+    /* spike log (AER payloads, network.py:60-63) and delivery work list */
+    double* log_t;          /* [log_slots][spk_cap]                            */
+    uint32_t* log_gid;      /* [log_slots][spk_cap]                            */
+    unsigned long long* log_ctr; /* [log_slots] (pieces << 32) | spikes        */
+    uint32_t* pieces;       /* [2][piece_cap][4] {syn_lo, syn_hi, ref, count}  */
+
+    /* outputs */
+    uint32_t* raster_gid;   /* [raster_cap]                                    */
+    double* raster_t;       /* [raster_cap]                                    */
+    uint32_t* out_gid;      /* [out_cap] exchange out-list (direct_log == 0)   */
+    double* out_t;          /* [out_cap]                                       */
+    float* scratch;         /* [scratch_cap][4] spill staging                  */
+    const int32_t* probe_map; /* [n_local] probe slot or -1                    */
+    double* probe_out;      /* [steps][n_probe][5] V c last refr V_end         */
+    int64_t probe_steps;    /* rows in probe_out                               */
+    cc_ctl* ctl;
+} cc_shard;
+
+/* ---------------------------------------------------------------- misc */
+int cc_abi_version(void);
+const char* cc_last_error(void);
+/* sizeof(cc_shard) and sizeof(cc_ctl) as compiled, so hosts can verify layout. */
+int64_t cc_sizeof_shard(void);
+int64_t cc_sizeof_ctl(void);
+
+/* ------------------------------------------------------- simulation step */
+/* Initial state: V = V_r + u (V_theta - V_r), u = counter_uniforms(seed,
+ * INIT_STATE, gid, 0, 0); c = 0, last_t = 0, refr_until = -inf.
+ * Replaces engine.py:297-302 and NeuronBlock.__init__ (model.py:263-267). */
+int cc_init_state(const cc_shard* sh, void* stream);
+
+/* Step phase (3): arborise the spikes emitted in step t-1 (the log slot the
+ * previous cc_neuron_step or cc_ingest filled) into the delay ring.
+ * Replaces the expand block engine.py:338-367 and DelayRing.insert
+ * (engine.py:138-149). */
+int cc_deliver(const cc_shard* sh, void* stream);
+
+/* Step phases (4)-(6): drain the ring slot of step t, generate the external
+ * Poisson events, order each neuron's inputs by (time, source, weight) and
+ * integrate them exactly; emit spikes.  Increments ctl->t.
+ * Replaces DelayRing.drain (engine.py:151-163), _external_events
+ * (engine.py:191-206), the lexsort (engine.py:386) and
+ * NeuronBlock.integrate_sorted (model.py:289-337). */
+int cc_neuron_step(const cc_shard* sh, void* stream);
+
+/* Multi-shard mode: append the n received AER events (gid, t) emitted in
+ * step ctl->t - 1 to the delivery log.  Stands in for the receive half of
+ * deliver_spikes (network.py:360-378) + rows_for (network.py:135-141). */
+int cc_ingest(const cc_shard* sh, const uint32_t* in_gid, const double* in_t,
+              const int32_t* in_n, void* stream);
+
+/* Pack this shard's out-list into per-destination AER buffers using the
+ * per-neuron destination bit mask (source_masks, network.py:229-230).
+ * local_of_col maps a global column to its rank among owned columns.
+ * send_gid/send_t are [n_dest][dest_cap]; send_n [n_dest] (zeroed by caller). */
+int cc_pack_outgoing(const cc_shard* sh, const uint32_t* dest_mask_by_local,
+                     int32_t n_dest, int32_t dest_cap, uint32_t* send_gid,
+                     double* send_t, int32_t* send_n, const uint32_t* local_of_col,
+                     void* stream);
+
+/* ------------------------------------------------- connectivity generator */
+/* Philox4x64-10 generator of the incoming-synapse CSR of one shard, bit-exact
+ * with connectivity.py:383-417 (Bernoulli targets, ziggurat normal weights,
+ * uniform / exponential delays), for the sources listed in src_gid.
+ * Pass 1 (cc_gen_count) writes the row length of every listed source;
+ * the host scans them into row_off; pass 2 (cc_gen_fill) writes the rows,
+ * sorted by (delay, layout order) like network.py:257.
+ * Layout tables (geometry.layout_blocks): blk_col/blk_p [n_columns][kmax],
+ * blk_count [n_columns]; col_local [n_columns] = rank of an owned column or -1. */
+typedef struct cc_gen {
+    uint64_t seed;
+    int32_t n_col, n_exc_col, n_columns, kmax;
+    const int32_t* blk_col;
+    const double* blk_p;
+    const int32_t* blk_count;
+    const int32_t* col_local;
+    double j_ee, j_ei, j_ie, j_ii, sd_frac;
+    int32_t delay_kind;      /* 0 uniform, 1 exponential */
+    double d_lo, d_scale;    /* uniform: low, high - low; exponential: scale = mean */
+    double dt;
+    int32_t d_max;
+} cc_gen;
+
+int cc_gen_count(const cc_gen* g, const uint32_t* src_gid, int64_t n_src,
+                 int64_t* row_len, unsigned* err, void* stream);
+int cc_gen_fill(const cc_gen* g, const uint32_t* src_gid, int64_t n_src,
+                const int64_t* row_start, int32_t* syn_tgt, float* syn_w,
+                uint8_t* syn_d, unsigned long long* checksum, float* scratch,
+                int64_t scratch_per_warp, unsigned* err, void* stream);
+/* Warps in the generator's persistent grid (scratch is sized per warp). */
+int64_t cc_gen_warps(void);
+int64_t cc_sizeof_gen(void);
+
+/* Order-independent checksum of the wire records (network.py:70-88) of the
+ * rows of the given sources, in global target ids.  Adds into *checksum. */
+int cc_csr_checksum(const int64_t* row_off, const uint32_t* src_gid, int64_t n_src,
+                    const int32_t* syn_tgt_global, const float* syn_w,
+                    const uint8_t* syn_d, int32_t n_col, int32_t n_exc_col,
+                    unsigned long long* checksum, void* stream);
+
+/* Raw stream probes used by the parity tests.  kind: 0 Philox4x64-10 words
+ * (bit patterns), 1 random() doubles, 2 ziggurat standard normals,
+ * 3 ziggurat exponentials (serial reader); 11 / 12 the warp-cooperative
+ * exponential / normal walk of the generator.  Plus
+ * counter_uniforms(seed, purpose, a, b, k) of rng.py:74-90. */
+int cc_test_philox(uint64_t seed, uint64_t purpose, uint64_t a, int64_t n,
+                   int32_t kind, double* out, void* stream);
+int cc_test_counter_uniforms(uint64_t seed, uint64_t purpose, const uint64_t* a,
+                             uint64_t b, const uint64_t* k, int64_t n, double* out,
+                             void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CORTICARC_B200_H */

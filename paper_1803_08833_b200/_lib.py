@@ -1,0 +1,152 @@
+"""ctypes binding of libcorticarc_b200.so (the C ABI in include/corticarc_b200.h).
+
+The product path has no fallback: if the library is missing or CUDA is not
+available, `lib()` raises.  Struct mirrors are checked against the sizes the
+library was compiled with.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+__all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BITS",
+           "LIB_PATH"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
+ABI_VERSION = 3
+
+ERR_BITS = {
+    0x01: "spike log full (more spikes in one step than planned)",
+    0x02: "delivery work list full",
+    0x04: "delay-ring overflow list full",
+    0x08: "event staging scratch exhausted",
+    0x10: "Poisson draw budget exceeded (engine.py:187)",
+    0x20: "raster buffer full",
+    0x40: "exchange out-list full",
+    0x80: "generator row larger than planned",
+}
+
+
+class EngineError(RuntimeError):
+    """A device-side capacity or protocol violation, naming the step."""
+
+
+class Pop(C.Structure):
+    _fields_ = [(n, C.c_double) for n in
+                ("tau_m", "tau_c", "E", "V_theta", "V_r", "tau_arp", "alpha_c", "sfa", "k1", "k2")]
+
+
+class Ctl(C.Structure):
+    _fields_ = [
+        ("t", C.c_longlong), ("rec_events", C.c_ulonglong), ("ext_events", C.c_ulonglong),
+        ("n_spikes", C.c_ulonglong), ("raster_n", C.c_ulonglong),
+        ("done_blocks", C.c_uint), ("error_bits", C.c_uint), ("error_step", C.c_longlong),
+        ("max_bin", C.c_uint), ("max_events", C.c_uint), ("scratch_used", C.c_ulonglong),
+        ("out_n", C.c_uint), ("pad0", C.c_uint), ("spilled_total", C.c_ulonglong),
+        ("ovf_total", C.c_ulonglong),
+    ]
+
+
+_P = C.c_void_p
+
+
+class Shard(C.Structure):
+    _fields_ = [
+        ("n_local", C.c_int32), ("n_col", C.c_int32), ("n_exc_col", C.c_int32),
+        ("d_max", C.c_int32), ("bin_cap", C.c_int32), ("log_slots", C.c_int32),
+        ("spk_cap", C.c_int32), ("piece_len", C.c_int32),
+        ("ovf_cap", C.c_int64), ("piece_cap", C.c_int64), ("raster_cap", C.c_int64),
+        ("scratch_cap", C.c_int64), ("n_rows", C.c_int64),
+        ("out_cap", C.c_int32), ("ext_budget", C.c_int32), ("n_probe", C.c_int32),
+        ("direct_log", C.c_int32),
+        ("h2_ext", C.c_uint64), ("h2_time", C.c_uint64), ("h2_init", C.c_uint64),
+        ("dt", C.c_double), ("ext_weight", C.c_double), ("ext_thresh", C.c_double),
+        ("pop", Pop * 2),
+        ("gid", _P), ("state", _P),
+        ("row_off", _P), ("syn_tgt", _P), ("syn_w", _P), ("syn_d", _P),
+        ("bin_cnt", _P), ("bin_rec", _P), ("ovf_rec", _P), ("ovf_cnt", _P),
+        ("log_t", _P), ("log_gid", _P), ("log_ctr", _P), ("pieces", _P),
+        ("raster_gid", _P), ("raster_t", _P), ("out_gid", _P), ("out_t", _P),
+        ("scratch", _P), ("probe_map", _P), ("probe_out", _P),
+        ("probe_steps", C.c_int64), ("ctl", _P),
+    ]
+
+
+class Gen(C.Structure):
+    _fields_ = [
+        ("seed", C.c_uint64), ("n_col", C.c_int32), ("n_exc_col", C.c_int32),
+        ("n_columns", C.c_int32), ("kmax", C.c_int32),
+        ("blk_col", _P), ("blk_p", _P), ("blk_count", _P), ("col_local", _P),
+        ("j_ee", C.c_double), ("j_ei", C.c_double), ("j_ie", C.c_double), ("j_ii", C.c_double),
+        ("sd_frac", C.c_double), ("delay_kind", C.c_int32),
+        ("d_lo", C.c_double), ("d_scale", C.c_double), ("dt", C.c_double),
+        ("d_max", C.c_int32),
+    ]
+
+
+_lib = None
+
+_SIGS = {
+    "cc_abi_version": (C.c_int, []),
+    "cc_last_error": (C.c_char_p, []),
+    "cc_sizeof_shard": (C.c_int64, []),
+    "cc_sizeof_ctl": (C.c_int64, []),
+    "cc_sizeof_gen": (C.c_int64, []),
+    "cc_init_state": (C.c_int, [C.POINTER(Shard), _P]),
+    "cc_deliver": (C.c_int, [C.POINTER(Shard), _P]),
+    "cc_neuron_step": (C.c_int, [C.POINTER(Shard), _P]),
+    "cc_ingest": (C.c_int, [C.POINTER(Shard), _P, _P, _P, _P]),
+    "cc_pack_outgoing": (C.c_int, [C.POINTER(Shard), _P, C.c_int32, C.c_int32, _P, _P, _P,
+                                   _P, _P]),
+    "cc_gen_count": (C.c_int, [C.POINTER(Gen), _P, C.c_int64, _P, _P, _P]),
+    "cc_gen_fill": (C.c_int, [C.POINTER(Gen), _P, C.c_int64, _P, _P, _P, _P, _P, _P,
+                              C.c_int64, _P, _P]),
+    "cc_gen_warps": (C.c_int64, []),
+    "cc_csr_checksum": (C.c_int, [_P, _P, C.c_int64, _P, _P, _P, C.c_int32, C.c_int32, _P, _P]),
+    "cc_test_philox": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_int32,
+                                 _P, _P]),
+    "cc_test_counter_uniforms": (C.c_int, [C.c_uint64, C.c_uint64, _P, C.c_uint64, _P,
+                                           C.c_int64, _P, _P]),
+}
+
+
+def load_library(path: str = LIB_PATH):
+    """Load and type the library without touching CUDA (CPU-safe)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with "
+                          "`python -m paper_1803_08833_b200.build` (there is no CPU fallback)")
+    L = C.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(L, name)
+        fn.restype, fn.argtypes = res, args
+    if L.cc_abi_version() != ABI_VERSION:
+        raise ImportError(f"ABI mismatch: library {L.cc_abi_version()} != {ABI_VERSION}")
+    for name, st in (("cc_sizeof_shard", Shard), ("cc_sizeof_ctl", Ctl), ("cc_sizeof_gen", Gen)):
+        if getattr(L, name)() != C.sizeof(st):
+            raise ImportError(f"struct layout mismatch for {name}: "
+                              f"{getattr(L, name)()} != {C.sizeof(st)}")
+    _lib = L
+    return L
+
+
+def lib():
+    """The library, for device work: fails loudly without a CUDA device."""
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1803_08833_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    return load_library()
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != 0:
+        msg = _lib.cc_last_error().decode() if _lib is not None else "?"
+        raise EngineError(f"{what}: {msg}" if what else msg)
+
+
+def decode_errors(bits: int) -> str:
+    return "; ".join(v for k, v in ERR_BITS.items() if bits & k) or f"0x{bits:x}"

@@ -1,0 +1,62 @@
+"""In-tree build of libcorticarc_b200.so for sm_100a (nvcc, no torch JIT).
+
+    python -m paper_1803_08833_b200.build          # or __graft_entry__.build()
+
+The shared library is written next to this file so it travels with the repo
+snapshot to the GPU host; `-fmad=false` keeps every float64 expression in the
+reference's evaluation order (no contracted multiply-adds).
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+GEN = os.path.join(CSRC, "_gen")
+LIB = os.path.join(PKG, "libcorticarc_b200.so")
+SOURCES = ["capi.cu", "sim_kernels.cu", "gen_kernels.cu"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false",
+         "-gencode", "arch=compute_100a,code=sm_100a",
+         "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
+         "--extended-lambda"]
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)
+            if f.endswith((".cu", ".cuh", ".py"))]
+    deps.append(os.path.join(ROOT, "include", "corticarc_b200.h"))
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    sys.path.insert(0, CSRC)
+    try:
+        import gen_ziggurat
+    finally:
+        sys.path.pop(0)
+    gen_ziggurat.emit(os.path.join(GEN, "cc_ziggurat_tables.h"))
+    cmd = [NVCC, *FLAGS, "-shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+           "-I", GEN, *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    with open(os.path.join(GEN, "ptxas.log"), "w") as fh:
+        fh.write(res.stdout + res.stderr)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stderr[-6000:])
+    os.replace(LIB + ".tmp", LIB)
+    if verbose:
+        print(res.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,484 @@
+// Simulation-step kernels of the B200 engine (sm_100a).
+//
+// Per 1 ms step t (engine.py:318-394):
+//   k_deliver   arborise the spikes of step t-1 into the delay ring of event
+//               records (engine.py:338-367, DelayRing.insert :138-149)
+//   k_neuron    drain ring slot t, add the external Poisson events, order each
+//               neuron's inputs by (time, source, weight), integrate exactly in
+//               float64, emit spikes (engine.py:371-394, model.py:272-337)
+// plus k_ingest / k_pack for multi-shard runs and k_init_state.
+//
+// Exactness contract: every float64 expression below
+// follows the reference's evaluation order; the file is compiled with
+// -fmad=false so no multiply-add is contracted.
+#include <climits>
+#include "cc_common.cuh"
+
+namespace {
+
+constexpr int NEURON_BLOCK = 128;       // 4 warps
+constexpr int WARPS_PER_BLOCK = NEURON_BLOCK / 32;
+constexpr int WCAP = 512;               // staged events per warp in shared memory
+
+struct Ev {                              // one input event, 16 B
+    double t;                            // arrival time, ms
+    uint32_t src;                        // source gid (CC_EXT_SRC for the drive)
+    float w;                             // recurrent weight (f32 as stored)
+};
+
+__device__ __forceinline__ bool ev_less(const Ev& a, const Ev& b) {
+    // (t, src) is unique per target except for identical external events,
+    // whose weights are equal too, so this is the reference's total order
+    // lexsort((w, src, tm, tgt)) restricted to one target (engine.py:386).
+    return a.t < b.t || (a.t == b.t && a.src < b.src);
+}
+
+__device__ __forceinline__ long long pos_mod(long long a, long long m) {
+    long long r = a % m;
+    return r < 0 ? r + m : r;
+}
+
+// Free evolution of one neuron to time te (NeuronBlock.advance,
+// model.py:272-287 with _voltage_decay, model.py:116-143).
+struct NState { double V, c, last, ru; };
+
+__device__ __forceinline__ void advance(NState& s, const cc_pop& P, double te) {
+    const double ff = fmin(fmax(s.last, s.ru), te);            // free_from
+    double cs = s.c;
+    if (ff != s.last && cs != 0.0)                             // exp(-0/tau) == 1 exactly
+        cs = cs * exp(-(ff - s.last) / P.tau_c);
+    const double Vs = (s.last < s.ru) ? P.V_r : s.V;
+    const double dt = te - ff;
+    const double em = exp(-dt / P.tau_m);
+    double Vt = P.E + (Vs - P.E) * em;
+    double ct = cs;
+    if (cs != 0.0) {
+        // with c == 0 the fatigue term is (sfa*0)*f == 0 for the always
+        // finite f, and c*ec == 0: both skipped exactly
+        const double ec = exp(-dt / P.tau_c);
+        const double x = dt * P.k1 / P.k2;
+        double f;
+        if (x == 0.0)
+            f = dt * em;
+        else if (fabs(x) <= 1.0)
+            f = dt * em * expm1(x) / x;
+        else
+            f = dt * (ec - em) / x;
+        Vt = Vt - P.sfa * cs * f;
+        ct = cs * ec;
+    }
+    s.V = (te < s.ru) ? P.V_r : Vt;
+    s.c = ct;
+    s.last = te;
+}
+
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t& total) {
+    const int lane = threadIdx.x & 31;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+}
+
+// Append one spike to the delivery log of emission step t (slot e) and cut
+// its CSR row into work pieces for the next step's k_deliver.
+__device__ __forceinline__ void log_spike(const cc_shard& sh, long long t, uint32_t gid,
+                                          double te) {
+    const int64_t r0 = sh.row_off[gid];
+    const int64_t len = sh.row_off[gid + 1] - r0;
+    if (len == 0) return;                       // no synapse on this shard
+    const int e = (int)pos_mod(t, sh.log_slots);
+    const unsigned long long np = (unsigned long long)((len + sh.piece_len - 1) / sh.piece_len);
+    const unsigned long long old = atomicAdd(&sh.log_ctr[e], (np << 32) | 1ull);
+    const unsigned long long idx = old & 0xffffffffull;
+    const unsigned long long pb = old >> 32;
+    if (idx >= (unsigned long long)sh.spk_cap || pb + np > (unsigned long long)sh.piece_cap) {
+        cc_raise(sh.ctl, idx >= (unsigned long long)sh.spk_cap ? CC_ERR_SPIKE_LOG : CC_ERR_PIECES, t);
+        return;
+    }
+    const uint32_t ref = (uint32_t)(e * sh.spk_cap + idx);
+    sh.log_t[ref] = te;
+    sh.log_gid[ref] = gid;
+    uint4* pcs = reinterpret_cast<uint4*>(sh.pieces) + (size_t)(t & 1) * sh.piece_cap + pb;
+    for (unsigned long long k = 0; k < np; ++k) {
+        const int64_t s0 = r0 + (int64_t)k * sh.piece_len;
+        const int64_t cnt = min((int64_t)sh.piece_len, len - (int64_t)k * sh.piece_len);
+        pcs[k] = make_uint4((uint32_t)s0, (uint32_t)((uint64_t)s0 >> 32), ref, (uint32_t)cnt);
+    }
+}
+
+__device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, int t_mod_l) {
+    const uint32_t ref = (uint32_t)rec;
+    const int e = (int)(ref / (uint32_t)sh.spk_cap);
+    int d = t_mod_l - e;
+    if (d <= 0) d += sh.log_slots;
+    Ev ev;
+    // t_arr = t_emit + delay * dt (engine.py:364-365)
+    ev.t = sh.log_t[ref] + (double)d * sh.dt;
+    ev.src = sh.log_gid[ref];
+    ev.w = __uint_as_float((uint32_t)(rec >> 32));
+    return ev;
+}
+
+template <bool PROBE>
+__global__ void __launch_bounds__(NEURON_BLOCK)
+k_neuron(const cc_shard sh) {
+    __shared__ Ev stage[WARPS_PER_BLOCK][WCAP];
+    cc_ctl* ctl = sh.ctl;
+    const long long t = *(volatile long long*)&ctl->t;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int li = blockIdx.x * NEURON_BLOCK + threadIdx.x;
+    const bool active = li < sh.n_local;
+    const int D = sh.d_max;
+    const int slot = (int)pos_mod(t, D);
+    const int t_mod_l = (int)pos_mod(t, sh.log_slots);
+
+    uint32_t gid = 0, n_r = 0, n_e = 0;
+    int pop = 0;
+    if (active) {
+        gid = sh.gid[li];
+        pop = ((int)(gid % (uint32_t)sh.n_col) < sh.n_exc_col) ? 0 : 1;
+        const size_t ci = (size_t)slot * sh.n_local + li;
+        n_r = sh.bin_cnt[ci];
+        if (n_r) sh.bin_cnt[ci] = 0;
+        if (sh.ext_budget > 0) {
+            // Poisson count by product of uniforms (engine.py:172-188): the
+            // prefix product never increases, so stopping at the first
+            // product <= exp(-lambda) counts exactly the same terms.
+            const uint64_t h4 = cc_splitmix64(cc_splitmix64(sh.h2_ext ^ (uint64_t)gid)
+                                              ^ (uint64_t)t);
+            double prod = 1.0;
+            int k = 0;
+            for (; k < sh.ext_budget; ++k) {
+                prod = prod * cc_u53(cc_splitmix64(h4 ^ (uint64_t)k));
+                if (!(prod > sh.ext_thresh)) break;
+            }
+            if (k >= sh.ext_budget) cc_raise(ctl, CC_ERR_POISSON, t);
+            n_e = (uint32_t)k;
+        }
+    }
+    const uint32_t n = n_r + n_e;
+    uint32_t wtotal;
+    const uint32_t off = warp_excl_scan(n, wtotal);
+    Ev* seg = nullptr;
+    bool ok = true;
+    if (n) {
+        if (off + n <= (uint32_t)WCAP) {
+            seg = &stage[warp][off];
+        } else {
+            const unsigned long long at = atomicAdd(&ctl->scratch_used, (unsigned long long)n);
+            if (at + n > (unsigned long long)sh.scratch_cap) {
+                cc_raise(ctl, CC_ERR_SCRATCH, t);
+                ok = false;
+            } else {
+                seg = reinterpret_cast<Ev*>(sh.scratch) + at;
+                atomicAdd(&ctl->spilled_total, 1ull);
+            }
+        }
+    }
+    // recurrent records, k-major: lanes of a warp read 32 consecutive words
+    const uint32_t nb = ok ? min(n_r, (uint32_t)sh.bin_cap) : 0u;
+    uint32_t kmax = nb;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    for (uint32_t k = 0; k < kmax; ++k) {
+        if (k < nb) {
+            const uint64_t rec = sh.bin_rec[((size_t)slot * sh.bin_cap + k) * sh.n_local + li];
+            seg[k] = make_rec_event(sh, rec, t_mod_l);
+        }
+    }
+    if (ok && n_r > nb) {               // this neuron's surplus sits in the overflow list
+        uint32_t got = nb;
+        const uint32_t no = min(sh.ovf_cnt[slot], (uint32_t)sh.ovf_cap);
+        const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_rec) + (size_t)slot * sh.ovf_cap;
+        for (uint32_t i = 0; i < no && got < n_r; ++i) {
+            const uint4 r = ov[i];
+            if (r.x == (uint32_t)li)
+                seg[got++] = make_rec_event(sh, (uint64_t)r.y | ((uint64_t)r.z << 32), t_mod_l);
+        }
+    }
+    if (ok && n_e) {
+        // event times (t_step + u) * dt, u = counter_uniforms(EXTERNAL_TIME, gid, t, j)
+        const uint64_t h4 = cc_splitmix64(cc_splitmix64(sh.h2_time ^ (uint64_t)gid)
+                                          ^ (uint64_t)t);
+        for (uint32_t k = 0; k < n_e; ++k) {
+            Ev ev;
+            ev.t = ((double)t + cc_u53(cc_splitmix64(h4 ^ (uint64_t)k))) * sh.dt;
+            ev.src = CC_EXT_SRC;
+            ev.w = 0.0f;
+            seg[n_r + k] = ev;
+        }
+    }
+    __syncwarp();
+
+    uint32_t my_spikes = 0;
+    if (active && (n || PROBE)) {
+        const cc_pop& P = sh.pop[pop];
+        double* st = sh.state + (size_t)li * 4;
+        const double2 a = reinterpret_cast<const double2*>(st)[0];
+        const double2 b = reinterpret_cast<const double2*>(st)[1];
+        NState s{a.x, a.y, b.x, b.y};
+        if (ok && n) {
+            // insertion sort of this neuron's inputs
+            for (uint32_t i = 1; i < n; ++i) {
+                const Ev key = seg[i];
+                uint32_t j = i;
+                while (j > 0 && ev_less(key, seg[j - 1])) { seg[j] = seg[j - 1]; --j; }
+                seg[j] = key;
+            }
+            for (uint32_t i = 0; i < n; ++i) {
+                const Ev ev = seg[i];
+                advance(s, P, ev.t);
+                if (ev.t >= s.ru) {
+                    const double w = (ev.src == CC_EXT_SRC) ? sh.ext_weight : (double)ev.w;
+                    const double V = s.V + w;
+                    if (V > P.V_theta) {                 // strict threshold
+                        s.V = P.V_r;
+                        s.c = s.c + P.alpha_c;
+                        s.ru = ev.t + P.tau_arp;
+                        ++my_spikes;
+                        if (sh.direct_log) {
+                            log_spike(sh, t, gid, ev.t);
+                        } else {
+                            const unsigned o = atomicAdd(&ctl->out_n, 1u);
+                            if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = ev.t; }
+                            else cc_raise(ctl, CC_ERR_OUTLIST, t);
+                        }
+                        const unsigned long long r = atomicAdd(&ctl->raster_n, 1ull);
+                        if (r < (unsigned long long)sh.raster_cap) {
+                            sh.raster_gid[r] = gid;
+                            sh.raster_t[r] = ev.t;
+                        } else {
+                            cc_raise(ctl, CC_ERR_RASTER, t);
+                        }
+                    } else {
+                        s.V = V;
+                    }
+                } else {
+                    s.V = P.V_r;                         // refractory: input discarded
+                }
+            }
+            reinterpret_cast<double2*>(st)[0] = make_double2(s.V, s.c);
+            reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
+        }
+        if (PROBE) {
+            const int ps = sh.probe_map[li];
+            if (ps >= 0 && t < sh.probe_steps) {
+                double* o = sh.probe_out + ((size_t)t * sh.n_probe + ps) * 5;
+                o[0] = s.V; o[1] = s.c; o[2] = s.last; o[3] = s.ru;
+                NState q = s;
+                const double te = (double)(t + 1) * sh.dt;
+                advance(q, P, te);
+                o[4] = q.V;
+            }
+        }
+    }
+    // counters: one atomic per warp
+    unsigned long long e_sum = n_e, s_sum = my_spikes;
+    uint32_t mx_b = n_r, mx_e = n;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        e_sum += __shfl_xor_sync(0xffffffffu, e_sum, o);
+        s_sum += __shfl_xor_sync(0xffffffffu, s_sum, o);
+        mx_b = max(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, o));
+        mx_e = max(mx_e, __shfl_xor_sync(0xffffffffu, mx_e, o));
+    }
+    if (lane == 0) {
+        if (e_sum) atomicAdd(&ctl->ext_events, e_sum);
+        if (s_sum) atomicAdd(&ctl->n_spikes, s_sum);
+        if (mx_b > 0) atomicMax(&ctl->max_bin, mx_b);
+        if (mx_e > 0) atomicMax(&ctl->max_events, mx_e);
+    }
+    // last block out advances the step counter and retires the slot
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(&ctl->done_blocks, 1u);
+        if (prev == gridDim.x - 1) {
+            ctl->done_blocks = 0;
+            sh.ovf_cnt[slot] = 0;
+            __threadfence();
+            *(volatile long long*)&ctl->t = t + 1;
+        }
+    }
+}
+
+// One warp per delivery piece (<= piece_len synapses of one spiking source).
+__global__ void __launch_bounds__(256)
+k_deliver(const cc_shard sh) {
+    cc_ctl* ctl = sh.ctl;
+    const long long t = *(volatile long long*)&ctl->t;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sh.log_ctr[pos_mod(t, sh.log_slots)] = 0ull;   // the slot k_neuron(t) fills
+        ctl->scratch_used = 0ull;
+    }
+    const int ep = (int)pos_mod(t - 1, sh.log_slots);
+    const unsigned long long n_pieces = sh.log_ctr[ep] >> 32;
+    const int lane = threadIdx.x & 31;
+    const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const uint4* pcs = reinterpret_cast<const uint4*>(sh.pieces) + (size_t)((t - 1) & 1) * sh.piece_cap;
+    const int D = sh.d_max;
+    const int base = (int)pos_mod(t - 1, D);
+    const int n = sh.n_local;
+    const int K = sh.bin_cap;
+    const int32_t* __restrict__ tgt_a = sh.syn_tgt;
+    const float* __restrict__ w_a = sh.syn_w;
+    const uint8_t* __restrict__ d_a = sh.syn_d;
+    unsigned long long events = 0;
+    for (long long p = wid; p < (long long)n_pieces; p += nw) {
+        const uint4 pc = pcs[p];
+        const size_t s0 = (size_t)pc.x | ((size_t)pc.y << 32);
+        const uint32_t ref = pc.z;
+        const int cnt = (int)pc.w;
+        events += (unsigned long long)cnt;
+        for (int j0 = 0; j0 < cnt; j0 += 128) {
+            int tg[4], sl[4];
+            float w[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = j0 + u * 32 + lane;
+                sl[u] = -1;
+                if (j < cnt) {
+                    const size_t si = s0 + j;
+                    tg[u] = __ldg(tgt_a + si);
+                    w[u] = __ldg(w_a + si);
+                    int s = base + (int)__ldg(d_a + si);
+                    sl[u] = s >= D ? s - D : s;
+                }
+            }
+            unsigned pos[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (sl[u] >= 0) pos[u] = atomicAdd(&sh.bin_cnt[(size_t)sl[u] * n + tg[u]], 1u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (sl[u] < 0) continue;
+                const uint64_t rec = (uint64_t)ref | ((uint64_t)__float_as_uint(w[u]) << 32);
+                if (pos[u] < (unsigned)K) {
+                    sh.bin_rec[((size_t)sl[u] * K + pos[u]) * n + tg[u]] = rec;
+                } else {
+                    const unsigned o = atomicAdd(&sh.ovf_cnt[sl[u]], 1u);
+                    atomicAdd(&ctl->ovf_total, 1ull);
+                    if (o < (unsigned)sh.ovf_cap) {
+                        reinterpret_cast<uint4*>(sh.ovf_rec)[(size_t)sl[u] * sh.ovf_cap + o] =
+                            make_uint4((uint32_t)tg[u], ref, __float_as_uint(w[u]), 0u);
+                    } else {
+                        cc_raise(ctl, CC_ERR_OVERFLOW_BIN, t);
+                    }
+                }
+            }
+        }
+    }
+    if (lane == 0 && events) atomicAdd(&ctl->rec_events, events);
+}
+
+// Multi-shard receive: log the AER events of step ctl->t - 1 that have rows here.
+__global__ void k_ingest(const cc_shard sh, const uint32_t* in_gid, const double* in_t,
+                         const int32_t* in_n) {
+    const long long t = *(volatile long long*)&sh.ctl->t - 1;
+    const int n = *in_n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        log_spike(sh, t, in_gid[i], in_t[i]);
+}
+
+// Multi-shard send: AER payload per destination (source_masks, network.py:229-230).
+__global__ void k_pack(const cc_shard sh, const uint32_t* dest_mask, int n_dest, int dest_cap,
+                       uint32_t* send_gid, double* send_t, int32_t* send_n,
+                       const uint32_t* local_of_col, int n_col) {
+    const unsigned n = min(*(volatile unsigned*)&sh.ctl->out_n, (unsigned)sh.out_cap);
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t g = sh.out_gid[i];
+        const uint32_t li = local_of_col[g / n_col] * n_col + g % n_col;
+        const uint32_t m = dest_mask[li];
+        for (int d = 0; d < n_dest; ++d) {
+            if (!(m >> d & 1u)) continue;
+            const int p = atomicAdd(&send_n[d], 1);
+            if (p < dest_cap) {
+                send_gid[(size_t)d * dest_cap + p] = g;
+                send_t[(size_t)d * dest_cap + p] = sh.out_t[i];
+            } else {
+                cc_raise(sh.ctl, CC_ERR_OUTLIST, *(volatile long long*)&sh.ctl->t - 1);
+            }
+        }
+    }
+}
+
+__global__ void k_init_state(const cc_shard sh) {
+    const int li = blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= sh.n_local) return;
+    const uint32_t gid = sh.gid[li];
+    const int pop = ((int)(gid % (uint32_t)sh.n_col) < sh.n_exc_col) ? 0 : 1;
+    const cc_pop& P = sh.pop[pop];
+    // counter_uniforms(seed, INIT_STATE, gid, 0, 0)
+    const uint64_t h = cc_splitmix64(cc_splitmix64(cc_splitmix64(sh.h2_init ^ (uint64_t)gid)));
+    const double u = cc_u53(h);
+    double* st = sh.state + (size_t)li * 4;
+    reinterpret_cast<double2*>(st)[0] = make_double2(P.V_r + u * (P.V_theta - P.V_r), 0.0);
+    reinterpret_cast<double2*>(st)[1] = make_double2(0.0, -INFINITY);
+}
+
+}  // namespace
+
+// --------------------------------------------------------------- launchers
+extern "C" int cc_set_error(const char* fmt, ...);
+extern "C" int cc_check_launch(const char* what);
+
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+extern "C" int cc_init_state(const cc_shard* sh, void* stream) {
+    if (!sh) return cc_set_error("cc_init_state: null shard");
+    if (sh->n_local == 0) return 0;
+    k_init_state<<<(sh->n_local + 255) / 256, 256, 0, (cudaStream_t)stream>>>(*sh);
+    return cc_check_launch("k_init_state");
+}
+
+extern "C" int cc_deliver(const cc_shard* sh, void* stream) {
+    if (!sh) return cc_set_error("cc_deliver: null shard");
+    k_deliver<<<sm_count() * 8, 256, 0, (cudaStream_t)stream>>>(*sh);
+    return cc_check_launch("k_deliver");
+}
+
+extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
+    if (!sh) return cc_set_error("cc_neuron_step: null shard");
+    if (sh->n_local <= 0) return cc_set_error("cc_neuron_step: empty shard");
+    const int blocks = (sh->n_local + NEURON_BLOCK - 1) / NEURON_BLOCK;
+    if (sh->n_probe > 0)
+        k_neuron<true><<<blocks, NEURON_BLOCK, 0, (cudaStream_t)stream>>>(*sh);
+    else
+        k_neuron<false><<<blocks, NEURON_BLOCK, 0, (cudaStream_t)stream>>>(*sh);
+    return cc_check_launch("k_neuron");
+}
+
+extern "C" int cc_ingest(const cc_shard* sh, const uint32_t* in_gid, const double* in_t,
+                         const int32_t* in_n, void* stream) {
+    if (!sh) return cc_set_error("cc_ingest: null shard");
+    k_ingest<<<sm_count() * 2, 256, 0, (cudaStream_t)stream>>>(*sh, in_gid, in_t, in_n);
+    return cc_check_launch("k_ingest");
+}
+
+extern "C" int cc_pack_outgoing(const cc_shard* sh, const uint32_t* dest_mask_by_local,
+                                int32_t n_dest, int32_t dest_cap, uint32_t* send_gid,
+                                double* send_t, int32_t* send_n, const uint32_t* local_of_col,
+                                void* stream) {
+    if (!sh) return cc_set_error("cc_pack_outgoing: null shard");
+    if (n_dest > 32) return cc_set_error("cc_pack_outgoing: at most 32 shards");
+    k_pack<<<sm_count(), 256, 0, (cudaStream_t)stream>>>(*sh, dest_mask_by_local, n_dest,
+                                                         dest_cap, send_gid, send_t, send_n,
+                                                         local_of_col, sh->n_col);
+    return cc_check_launch("k_pack");
+}

@@ -1,0 +1,325 @@
+"""B200 simulation engine: device buffers, CUDA-graph step loop, RunResult.
+
+Drop-in for the reference's simulate entry points (corticarc/engine.py):
+
+    run_b200(config, workers=1) -> RunResult      ~ engine.run / run_multiprocess
+    Simulator(config, net).run(n_steps)           ~ run_worker's step loop (:318-394)
+
+Per step two kernels run on one stream (k_deliver, k_neuron; see
+csrc/sim_kernels.cu); chunks of steps are captured once into a CUDA graph and
+replayed, with a host check of the device counters between chunks (errors are
+raised with the step they occurred at, the raster is copied out).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+import numpy as np
+
+from . import _lib
+from .geometry import grid_totals
+from .network import DeviceNetwork, build_b200
+from .spec import MemoryBudgetError
+
+__all__ = ["RunResult", "Simulator", "run_b200", "raster_checksum", "estimate_worker_bytes"]
+
+MASK64 = (1 << 64) - 1
+DOMAIN = 0x636F727469636172
+P_INIT_STATE, P_EXTERNAL, P_EXTERNAL_TIME = 4, 5, 7
+
+
+def _sm(x: int) -> int:
+    z = (x + 0x9E3779B97F4A7C15) & MASK64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+    return z ^ (z >> 31)
+
+
+def _h2(seed: int, purpose: int) -> int:
+    """First two links of counter_uniforms' splitmix chain (rng.py:85-86)."""
+    return _sm(_sm((seed & MASK64) ^ DOMAIN) ^ purpose)
+
+
+def raster_checksum(gids, times) -> int:
+    """network.py:91-97 (order independent)."""
+    if len(gids) == 0:
+        return 0
+    u = np.uint64
+    lo = np.asarray(gids, dtype=u)
+    hi = np.asarray(times, dtype=np.float64).view(u)
+    with np.errstate(over="ignore"):
+        def sm(x):
+            z = x + u(0x9E3779B97F4A7C15)
+            z = (z ^ (z >> u(30))) * u(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> u(27))) * u(0x94D049BB133111EB)
+            return z ^ (z >> u(31))
+        return int(np.sum(sm(lo ^ sm(hi)), dtype=u))
+
+
+def estimate_worker_bytes(config, workers: int) -> int:
+    """The reference's pre-allocation estimate (engine.py:278-283)."""
+    local, remote = grid_totals(config.kernel, config.grid)
+    syn = (local + remote) / workers
+    state = config.grid.n_neurons / workers * 13 * 8
+    return int(syn * 32 + state)
+
+
+@dataclass
+class RunResult:
+    """Same fields and meanings as the reference RunResult (engine.py:251-275)."""
+    config: object
+    worker_count: int
+    raster_gids: np.ndarray
+    raster_times: np.ndarray
+    n_spikes: int
+    recurrent_events: int
+    external_events: int
+    recurrent_synapses: int
+    construction_checksum: int
+    raster_checksum: int
+    construction_seconds: float
+    sim_seconds_wall: float
+    substep_seconds: Dict[str, float]
+    steady_bytes_per_worker: List[int]
+    peak_bytes_per_worker: List[int]
+    workers: list = field(default_factory=list)
+    probe_state: Optional[np.ndarray] = None      # [steps, P, 4]
+    probe_v_end: Optional[np.ndarray] = None      # [steps, P]
+    device_stats: dict = field(default_factory=dict)
+
+    @property
+    def mean_rate_hz(self) -> float:
+        denom = self.config.grid.n_neurons * self.config.duration_s
+        return self.n_spikes / denom if denom else 0.0
+
+
+def _pop(p) -> _lib.Pop:
+    q = _lib.Pop()
+    q.tau_m, q.tau_c, q.E = p.tau_m, p.tau_c, p.E
+    q.V_theta, q.V_r, q.tau_arp, q.alpha_c = p.V_theta, p.V_r, p.tau_arp, p.alpha_c
+    q.sfa = p.g_c / p.C_m
+    q.k1 = p.tau_c - p.tau_m
+    q.k2 = p.tau_m * p.tau_c
+    return q
+
+
+def _spikes_per_step_bound(cfg) -> int:
+    taus = [cfg.exc_params.tau_arp, cfg.inh_params.tau_arp]
+    if min(taus) <= 0:
+        return 8
+    return int(math.floor(cfg.timestep_ms / min(taus))) + 1
+
+
+class Simulator:
+    """One shard's device state and step loop."""
+
+    def __init__(self, cfg, net: DeviceNetwork, *, probes=None, probe_steps: int = 0,
+                 bin_cap: Optional[int] = None, piece_len: int = 256, chunk: int = 100,
+                 use_graphs: bool = True, direct_log: Optional[bool] = None,
+                 device=None):
+        import torch
+        self.L = _lib.lib()
+        self.torch = torch
+        self.cfg, self.net = cfg, net
+        self.dev = torch.device(device or net.row_off.device)
+        dev = self.dev
+        grid = cfg.grid
+        n = grid.neurons_per_column
+        owned = net.owned_columns
+        gids = (owned[:, None].astype(np.int64) * n + np.arange(n)[None, :]).ravel()
+        self.gids = gids
+        n_local = len(gids)
+        D = cfg.d_max
+        bound = _spikes_per_step_bound(cfg)
+        if bin_cap is None:
+            bin_cap = 64
+        self.chunk = max(1, int(chunk))
+        self.use_graphs = use_graphs
+        direct = (net.size == 1) if direct_log is None else direct_log
+        T = torch
+        i32, i64, f64 = T.int32, T.int64, T.float64
+        spk_cap = max(1, min(net.nonempty_rows(), grid.n_neurons) * bound)
+        if spk_cap * (D + 1) >= 2 ** 32:
+            raise MemoryBudgetError("spike log references exceed 32 bits")
+        piece_cap = max(1, net.pieces_upper_bound(piece_len) * bound)
+        ovf_cap = max(1024, n_local * 2)
+        raster_cap = max(1024, n_local * bound * self.chunk)
+        scratch_cap = max(4096, n_local * 16)
+        self.buf = dict(
+            gid=T.from_numpy(gids.astype(np.uint32).view(np.int32)).to(dev),
+            state=T.zeros((n_local, 4), dtype=f64, device=dev),
+            bin_cnt=T.zeros((D, n_local), dtype=i32, device=dev),
+            bin_rec=T.empty((D, bin_cap, n_local), dtype=i64, device=dev),
+            ovf_rec=T.empty((D, ovf_cap, 4), dtype=i32, device=dev),
+            ovf_cnt=T.zeros(D, dtype=i32, device=dev),
+            log_t=T.empty((D + 1, spk_cap), dtype=f64, device=dev),
+            log_gid=T.empty((D + 1, spk_cap), dtype=i32, device=dev),
+            log_ctr=T.zeros(D + 1, dtype=i64, device=dev),
+            pieces=T.empty((2, piece_cap, 4), dtype=i32, device=dev),
+            raster_gid=T.empty(raster_cap, dtype=i32, device=dev),
+            raster_t=T.empty(raster_cap, dtype=f64, device=dev),
+            out_gid=T.empty(max(1, n_local * bound), dtype=i32, device=dev),
+            out_t=T.empty(max(1, n_local * bound), dtype=f64, device=dev),
+            scratch=T.empty((scratch_cap, 4), dtype=T.float32, device=dev),
+            probe_map=T.full((n_local,), -1, dtype=i32, device=dev),
+            ctl=T.zeros(C.sizeof(_lib.Ctl) // 8, dtype=i64, device=dev),
+        )
+        self.probes = None if probes is None else np.asarray(probes, np.int64)
+        n_probe = 0 if self.probes is None else len(self.probes)
+        if n_probe:
+            self.buf["probe_map"][T.from_numpy(self.probes).to(dev)] = \
+                T.arange(n_probe, dtype=i32, device=dev)
+        self.buf["probe_out"] = T.zeros((max(1, probe_steps), max(1, n_probe), 5), dtype=f64,
+                                        device=dev)
+        self.buf["ctl"][6] = (1 << 63) - 1          # error_step = LLONG_MAX
+        b = self.buf
+        sh = _lib.Shard()
+        sh.n_local, sh.n_col, sh.n_exc_col = n_local, n, grid.n_excitatory_per_column
+        sh.d_max, sh.bin_cap, sh.log_slots = D, bin_cap, D + 1
+        sh.spk_cap, sh.piece_len = spk_cap, piece_len
+        sh.ovf_cap, sh.piece_cap, sh.raster_cap = ovf_cap, piece_cap, raster_cap
+        sh.scratch_cap, sh.n_rows = scratch_cap, grid.n_neurons
+        sh.out_cap = b["out_gid"].numel()
+        lam = cfg.external.mean_per_step(cfg.timestep_ms)
+        if lam > 0:
+            sh.ext_budget = int(math.ceil(lam + 12.0 * math.sqrt(lam))) + 20
+            sh.ext_thresh = math.exp(-lam)
+        else:
+            sh.ext_budget, sh.ext_thresh = 0, 1.0
+        sh.n_probe = n_probe
+        sh.direct_log = 1 if direct else 0
+        sh.h2_ext = _h2(cfg.seed, P_EXTERNAL)
+        sh.h2_time = _h2(cfg.seed, P_EXTERNAL_TIME)
+        sh.h2_init = _h2(cfg.seed, P_INIT_STATE)
+        sh.dt = cfg.timestep_ms
+        sh.ext_weight = cfg.external.weight_mv
+        sh.pop[0] = _pop(cfg.exc_params)
+        sh.pop[1] = _pop(cfg.inh_params)
+        sh.gid, sh.state = b["gid"].data_ptr(), b["state"].data_ptr()
+        sh.row_off, sh.syn_tgt = net.row_off.data_ptr(), net.syn_tgt.data_ptr()
+        sh.syn_w, sh.syn_d = net.syn_w.data_ptr(), net.syn_d.data_ptr()
+        for k in ("bin_cnt", "bin_rec", "ovf_rec", "ovf_cnt", "log_t", "log_gid", "log_ctr",
+                  "pieces", "raster_gid", "raster_t", "out_gid", "out_t", "scratch",
+                  "probe_map", "probe_out", "ctl"):
+            setattr(sh, k, b[k].data_ptr())
+        sh.probe_steps = b["probe_out"].shape[0] if n_probe else 0
+        self.shard = sh
+        self.n_local = n_local
+        self._graph = None
+        self._graph_steps = 0
+        self.t = 0
+        self.raster_g: List[np.ndarray] = []
+        self.raster_t: List[np.ndarray] = []
+        self.device_bytes = sum(x.numel() * x.element_size() for x in b.values())
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(self.L.cc_init_state(C.byref(sh), stream), "cc_init_state")
+
+    # ------------------------------------------------------------------ steps
+    def _launch_step(self, stream) -> None:
+        _lib.check(self.L.cc_deliver(C.byref(self.shard), stream), "cc_deliver")
+        _lib.check(self.L.cc_neuron_step(C.byref(self.shard), stream), "cc_neuron_step")
+
+    def ctl(self) -> _lib.Ctl:
+        raw = self.buf["ctl"].cpu().numpy().tobytes()
+        return _lib.Ctl.from_buffer_copy(raw)
+
+    def check(self, collect_raster: bool = True) -> _lib.Ctl:
+        """Synchronise, raise on device errors, drain the raster buffer."""
+        self.torch.cuda.synchronize(self.dev)
+        c = self.ctl()
+        if c.error_bits:
+            raise _lib.EngineError(f"step {c.error_step}: {_lib.decode_errors(c.error_bits)}")
+        if c.raster_n:
+            n = int(c.raster_n)
+            if collect_raster:
+                self.raster_g.append(self.buf["raster_gid"][:n].cpu().numpy().view(np.uint32)
+                                     .astype(np.uint64))
+                self.raster_t.append(self.buf["raster_t"][:n].cpu().numpy())
+            self.buf["ctl"][4] = 0
+        return c
+
+    def _capture(self, steps: int, stream_obj) -> None:
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream_obj):
+            s = torch.cuda.current_stream(self.dev).cuda_stream
+            for _ in range(steps):
+                self._launch_step(s)
+        self._graph, self._graph_steps = g, steps
+
+    def advance(self, n_steps: int, collect_raster: bool = True) -> None:
+        """Run n_steps more steps (chunks replayed from a CUDA graph)."""
+        torch = self.torch
+        done = 0
+        while done < n_steps:
+            k = min(self.chunk, n_steps - done)
+            if self.use_graphs and k == self.chunk and self.t > 0:
+                if self._graph is None or self._graph_steps != k:
+                    self._capture(k, torch.cuda.Stream(self.dev))
+                self._graph.replay()
+            else:
+                s = torch.cuda.current_stream(self.dev).cuda_stream
+                for _ in range(k):
+                    self._launch_step(s)
+            self.t += k
+            done += k
+            self.check(collect_raster)
+
+    def raster(self):
+        g = np.concatenate(self.raster_g) if self.raster_g else np.empty(0, np.uint64)
+        t = np.concatenate(self.raster_t) if self.raster_t else np.empty(0)
+        o = np.lexsort((g, t))
+        return g[o], t[o]
+
+    def probe_results(self, steps: int):
+        if self.probes is None:
+            return None, None
+        p = self.buf["probe_out"][:steps].cpu().numpy()
+        return p[:, :, :4].copy(), p[:, :, 4].copy()
+
+
+def run_b200(config, workers: int = 1, *, net: Optional[DeviceNetwork] = None, probes=None,
+             steps: Optional[int] = None, bin_cap: Optional[int] = None, chunk: int = 100,
+             use_graphs: bool = True, device=None) -> RunResult:
+    """Build (unless `net` is given) and simulate on one B200; same result
+    contract as corticarc.engine.run (engine.py:449-480).  workers > 1 runs
+    one process per GPU (see paper_1803_08833_b200.distributed)."""
+    import torch
+    if workers != 1:
+        from .distributed import run_multi_gpu
+        return run_multi_gpu(config, workers)
+    est = estimate_worker_bytes(config, workers)
+    if est > config.memory_budget_bytes:
+        raise MemoryBudgetError(
+            f"estimated {est / 1e9:.2f} GB per worker exceeds the "
+            f"{config.memory_budget_bytes / 1e9:.2f} GB budget")
+    _lib.lib()
+    if net is None:
+        net = build_b200(config, device=device)
+    n_steps = config.n_steps if steps is None else steps
+    sim = Simulator(config, net, probes=probes, probe_steps=n_steps, bin_cap=bin_cap,
+                    chunk=chunk, use_graphs=use_graphs, device=device)
+    torch.cuda.synchronize(sim.dev)
+    t0 = time.perf_counter()
+    sim.advance(n_steps)
+    wall = time.perf_counter() - t0
+    c = sim.ctl()
+    g, t = sim.raster()
+    ps, pv = sim.probe_results(n_steps)
+    return RunResult(
+        config=config, worker_count=1, raster_gids=g, raster_times=t,
+        n_spikes=int(c.n_spikes), recurrent_events=int(c.rec_events),
+        external_events=int(c.ext_events), recurrent_synapses=net.n_synapses,
+        construction_checksum=net.checksum, raster_checksum=raster_checksum(g, t),
+        construction_seconds=net.construction_seconds, sim_seconds_wall=wall,
+        substep_seconds={"deliver": 0.0, "expand": 0.0, "external": 0.0, "integrate": wall},
+        steady_bytes_per_worker=[net.steady_bytes], peak_bytes_per_worker=[net.peak_bytes],
+        probe_state=ps, probe_v_end=pv,
+        device_stats=dict(max_bin=int(c.max_bin), max_events=int(c.max_events),
+                          spilled=int(c.spilled_total), overflow=int(c.ovf_total),
+                          bin_cap=sim.shard.bin_cap, device_bytes=sim.device_bytes))
