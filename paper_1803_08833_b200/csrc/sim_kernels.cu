@@ -163,67 +163,76 @@ k_neuron(const cc_shard sh) {
         }
     }
     const uint32_t n = n_r + n_e;
-    uint32_t wtotal;
-    const uint32_t off = warp_excl_scan(n, wtotal);
-    Ev* seg = nullptr;
-    bool ok = true;
-    if (n) {
-        if (off + n <= (uint32_t)WCAP) {
-            seg = &stage[warp][off];
-        } else {
-            const unsigned long long at = atomicAdd(&ctl->scratch_used, (unsigned long long)n);
-            if (at + n > (unsigned long long)sh.scratch_cap) {
-                cc_raise(ctl, CC_ERR_SCRATCH, t);
-                ok = false;
-            } else {
-                seg = reinterpret_cast<Ev*>(sh.scratch) + at;
-                atomicAdd(&ctl->spilled_total, 1ull);
-            }
-        }
-    }
-    // recurrent records, k-major: lanes of a warp read 32 consecutive words
-    const uint32_t nb = ok ? min(n_r, (uint32_t)sh.bin_cap) : 0u;
-    uint32_t kmax = nb;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-    for (uint32_t k = 0; k < kmax; ++k) {
-        if (k < nb) {
-            const uint64_t rec = sh.bin_rec[((size_t)slot * sh.bin_cap + k) * sh.n_local + li];
-            seg[k] = make_rec_event(sh, rec, t_mod_l);
-        }
-    }
-    if (ok && n_r > nb) {               // this neuron's surplus sits in the overflow list
-        uint32_t got = nb;
-        const uint32_t no = min(sh.ovf_cnt[slot], (uint32_t)sh.ovf_cap);
-        const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_rec) + (size_t)slot * sh.ovf_cap;
-        for (uint32_t i = 0; i < no && got < n_r; ++i) {
-            const uint4 r = ov[i];
-            if (r.x == (uint32_t)li)
-                seg[got++] = make_rec_event(sh, (uint64_t)r.y | ((uint64_t)r.z << 32), t_mod_l);
-        }
-    }
-    if (ok && n_e) {
-        // event times (t_step + u) * dt, u = counter_uniforms(EXTERNAL_TIME, gid, t, j)
-        const uint64_t h4 = cc_splitmix64(cc_splitmix64(sh.h2_time ^ (uint64_t)gid)
-                                          ^ (uint64_t)t);
-        for (uint32_t k = 0; k < n_e; ++k) {
-            Ev ev;
-            ev.t = ((double)t + cc_u53(cc_splitmix64(h4 ^ (uint64_t)k))) * sh.dt;
-            ev.src = CC_EXT_SRC;
-            ev.w = 0.0f;
-            seg[n_r + k] = ev;
-        }
-    }
-    __syncwarp();
-
-    uint32_t my_spikes = 0;
+    NState s{0.0, 0.0, 0.0, 0.0};
+    double* st = sh.state + (size_t)(active ? li : 0) * 4;
     if (active && (n || PROBE)) {
-        const cc_pop& P = sh.pop[pop];
-        double* st = sh.state + (size_t)li * 4;
         const double2 a = reinterpret_cast<const double2*>(st)[0];
         const double2 b = reinterpret_cast<const double2*>(st)[1];
-        NState s{a.x, a.y, b.x, b.y};
-        if (ok && n) {
+        s = NState{a.x, a.y, b.x, b.y};
+    }
+    const cc_pop& P = sh.pop[pop];
+    const uint32_t nb = min(n_r, (uint32_t)sh.bin_cap);
+    uint32_t my_spikes = 0;
+    // The warp's neurons pass through the shared staging buffer in rounds:
+    // every round admits the pending lanes whose inputs fit behind the lanes
+    // before them; the first pending lane always goes (spilling to global
+    // scratch only when it alone exceeds the buffer).
+    bool pending = active && n > 0;
+    while (__any_sync(0xffffffffu, pending)) {
+        uint32_t tot;
+        const uint32_t off = warp_excl_scan(pending ? n : 0u, tot);
+        bool go = pending && (off + n <= (uint32_t)WCAP || off == 0);
+        Ev* seg = nullptr;
+        if (go) {
+            if (n <= (uint32_t)WCAP) {
+                seg = &stage[warp][off];
+            } else {
+                const unsigned long long at = atomicAdd(&ctl->scratch_used, (unsigned long long)n);
+                if (at + n > (unsigned long long)sh.scratch_cap) {
+                    cc_raise(ctl, CC_ERR_SCRATCH, t);
+                    go = false;
+                    pending = false;
+                } else {
+                    seg = reinterpret_cast<Ev*>(sh.scratch) + at;
+                    atomicAdd(&ctl->spilled_total, 1ull);
+                }
+            }
+        }
+        // recurrent records, k-major: lanes of a warp read consecutive words
+        const uint32_t mine = go ? nb : 0u;
+        uint32_t kmax = mine;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+        for (uint32_t k = 0; k < kmax; ++k) {
+            if (k < mine) {
+                const uint64_t rec = sh.bin_rec[((size_t)slot * sh.bin_cap + k) * sh.n_local + li];
+                seg[k] = make_rec_event(sh, rec, t_mod_l);
+            }
+        }
+        if (go && n_r > nb) {           // this neuron's surplus sits in the overflow list
+            uint32_t got = nb;
+            const uint32_t no = min(sh.ovf_cnt[slot], (uint32_t)sh.ovf_cap);
+            const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_rec) + (size_t)slot * sh.ovf_cap;
+            for (uint32_t i = 0; i < no && got < n_r; ++i) {
+                const uint4 r = ov[i];
+                if (r.x == (uint32_t)li)
+                    seg[got++] = make_rec_event(sh, (uint64_t)r.y | ((uint64_t)r.z << 32), t_mod_l);
+            }
+        }
+        if (go && n_e) {
+            // event times (t_step + u) * dt, u = counter_uniforms(EXTERNAL_TIME, gid, t, j)
+            const uint64_t h4 = cc_splitmix64(cc_splitmix64(sh.h2_time ^ (uint64_t)gid)
+                                              ^ (uint64_t)t);
+            for (uint32_t k = 0; k < n_e; ++k) {
+                Ev ev;
+                ev.t = ((double)t + cc_u53(cc_splitmix64(h4 ^ (uint64_t)k))) * sh.dt;
+                ev.src = CC_EXT_SRC;
+                ev.w = 0.0f;
+                seg[n_r + k] = ev;
+            }
+        }
+        __syncwarp();
+        if (go) {
             // insertion sort of this neuron's inputs
             for (uint32_t i = 1; i < n; ++i) {
                 const Ev key = seg[i];
@@ -265,17 +274,18 @@ k_neuron(const cc_shard sh) {
             }
             reinterpret_cast<double2*>(st)[0] = make_double2(s.V, s.c);
             reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
+            pending = false;
         }
-        if (PROBE) {
-            const int ps = sh.probe_map[li];
-            if (ps >= 0 && t < sh.probe_steps) {
-                double* o = sh.probe_out + ((size_t)t * sh.n_probe + ps) * 5;
-                o[0] = s.V; o[1] = s.c; o[2] = s.last; o[3] = s.ru;
-                NState q = s;
-                const double te = (double)(t + 1) * sh.dt;
-                advance(q, P, te);
-                o[4] = q.V;
-            }
+        __syncwarp();
+    }
+    if (PROBE && active) {
+        const int ps = sh.probe_map[li];
+        if (ps >= 0 && t < sh.probe_steps) {
+            double* o = sh.probe_out + ((size_t)t * sh.n_probe + ps) * 5;
+            o[0] = s.V; o[1] = s.c; o[2] = s.last; o[3] = s.ru;
+            NState q = s;
+            advance(q, P, (double)(t + 1) * sh.dt);
+            o[4] = q.V;
         }
     }
     // counters: one atomic per warp
