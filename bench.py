@@ -1,0 +1,317 @@
+"""Benchmark: synaptic events/s of the per-millisecond DPSNN loop on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A "step" is one simulated 1 ms step of the whole network (k_deliver + k_neuron
+for every shard).  Workload (N=1): BASELINE config 1 - 8x8 grid of
+1240-neuron columns (79,360 LIF+SFA neurons, ~95 M synapses), Gaussian
+lateral decay, calibrated operating point (presets.py).  Connectivity and
+drive are generated on the device from the seed (bit-exact with the
+reference's streams); timing excludes construction like the reference's
+normalized cost (metrics.py:114-123).
+
+value      = (recurrent + external events in K timed steps) / device time of
+             the K steps (CUDA events around CUDA-graph replays, one sync).
+e2e        = same metric through the public API run_b200(config) wall clock
+             (host loop, per-chunk counter checks and raster device->host copies).
+roofline   = k_deliver against measured HBM bandwidth, 17 B per recurrent
+             event; per-kernel times from event-record nodes
+             in an instrumented graph replay of the same workload.
+cpu_baseline / --impl reference = the CPU oracle (numpy port of the
+             reference loop) on the same connectivity, 1 core, bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_EVENT = 17          # 9 B CSR record + 8 B deposit
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8 and parts[0].replace(".", "").isdigit():
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def workload(args):
+    from paper_1803_08833_b200.presets import baseline_config
+    cfg = baseline_config(args.config, "calibrated", kernel=args.kernel,
+                          duration_s=(args.warmup + args.steps) / 1000.0, seed=args.seed,
+                          drive_hz=args.drive)
+    return cfg
+
+
+def oracle_net(net):
+    """DeviceNetwork -> the oracle's ShardNet (host copy of the same CSR)."""
+    from oracle import corticarc_oracle as O
+    row_off, tgt, w, d = net.host_csr()
+    ln = np.diff(row_off)
+    src = np.flatnonzero(ln).astype(np.uint64)
+    offs = np.concatenate([row_off[src.astype(np.int64)], [row_off[-1]]]).astype(np.int64)
+    return O.ShardNet(src, offs, tgt.astype(np.uint32), d.astype(np.uint16), w, net.checksum,
+                      net.n_synapses)
+
+
+def cpu_oracle_sample(cfg, net, budget_s: float, max_steps: int):
+    """Time the numpy oracle (1 core) on the same connectivity from t=0."""
+    from oracle import corticarc_oracle as O
+    onet = oracle_net(net)
+    sim = O.ShardSim(cfg, onet)
+    t0 = time.perf_counter()
+    steps = 0
+    while steps < max_steps and time.perf_counter() - t0 < budget_s:
+        inc = [sim.outgoing()] if len(sim.prev_idx) else []
+        sim.step(steps, inc)
+        steps += 1
+    wall = time.perf_counter() - t0
+    ev = sim.rec + sim.ext
+    return dict(value=ev / wall if wall > 0 else 0.0, unit="events/s", cores=1, kind="port",
+                sample=f"oracle/corticarc_oracle.py ShardSim, config {cfg.grid.nx}x{cfg.grid.ny}, "
+                       f"steps 0..{steps - 1} from t=0 ({ev} events, {wall:.1f} s, 1 thread)",
+                steps=steps, events=int(ev), wall_s=wall)
+
+
+def run_reference_arm(args):
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1803_08833_b200.network import build_b200
+    cfg = workload(args)
+    net = build_b200(cfg) if torch.cuda.is_available() else None
+    if net is None:
+        print(json.dumps({"impl": "reference", "unavailable": "no CUDA device to build the "
+                          "shared connectivity"}))
+        return
+    budget = float(os.environ.get("CC_REF_BUDGET_S", "150"))
+    # warmup steps are part of the sample's transient; the oracle is timed over
+    # all steps it completes within the budget
+    cb = cpu_oracle_sample(cfg, net, budget, args.warmup + args.steps)
+    steps = cb["steps"]
+    ms = cb["wall_s"] * 1000.0 / max(1, steps)
+    line = {
+        "metric": "synaptic events/s (recurrent + external)", "value": cb["value"],
+        "unit": "events/s", "n_gpus": args.gpus, "steps": steps, "warmup": 0,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, same connectivity)",
+        "config": config_block(cfg, net, args), "impl": "reference",
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": "events/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def config_block(cfg, net, args):
+    return {"workload": f"BASELINE config {args.config}: {cfg.grid.nx}x{cfg.grid.ny} columns x "
+                        f"{cfg.grid.neurons_per_column} LIF+SFA neurons, {cfg.kernel.kind} "
+                        f"lateral decay, calibrated drive",
+            "grid": f"{cfg.grid.nx}x{cfg.grid.ny}", "neurons": cfg.grid.n_neurons,
+            "synapses": int(net.n_synapses) if net is not None else None,
+            "kernel": cfg.kernel.kind, "drive_hz": cfg.external.rate_per_synapse_hz,
+            "j_inh_mv": cfg.genspec.j_inh_exc, "dt_ms": cfg.timestep_ms, "seed": cfg.seed,
+            "l2": "no flush between steps: per-step working set is scattered over the "
+                  f"{9 * net.n_synapses / 1e9:.2f} GB CSR + delay ring (> 126 MB L2)",
+            "parallelism": f"column blocks over {args.gpus} GPU(s)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--kernel", default=None)
+    ap.add_argument("--drive", type=float, default=None)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--chunk", type=int, default=100)
+    ap.add_argument("--bin-cap", type=int, default=None)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--instrument-steps", type=int, default=200)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_1803_08833_b200.distributed import bench_distributed
+        return bench_distributed(args, workload(args))
+    return bench_single(args)
+
+
+def bench_single(args):
+    import torch
+    from paper_1803_08833_b200 import _lib
+    from paper_1803_08833_b200.engine import Simulator, run_b200
+    from paper_1803_08833_b200.network import build_b200
+    L = _lib.lib()
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    cfg = workload(args)
+    net = build_b200(cfg)
+    K, W, CH = args.steps, args.warmup, min(args.chunk, args.steps)
+    sim = Simulator(cfg, net, chunk=CH, raster_steps=K + CH, bin_cap=args.bin_cap)
+    sim.advance(W)                                         # warm-up (eager + graphs)
+    c0 = sim.check()
+    g_main = sim.capture(CH)
+    rem = K % CH
+    g_rem = sim.capture(rem) if rem else None
+    stream = torch.cuda.current_stream(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = Clocks(0)
+    time.sleep(0.3)
+    torch.cuda.synchronize(dev)
+    ev0.record(stream)
+    for _ in range(K // CH):
+        g_main.replay()
+    if g_rem is not None:
+        g_rem.replay()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    sim.t += K
+    c1 = sim.check(collect_raster=False)
+    events = (c1.rec_events + c1.ext_events) - (c0.rec_events + c0.ext_events)
+    rec = c1.rec_events - c0.rec_events
+    spikes = c1.n_spikes - c0.n_spikes
+    value = events / (ms / 1e3)
+
+    # instrumented replay: per-kernel durations from event-record nodes
+    NI = min(args.instrument_steps, 1000)
+    timer = C.c_void_p()
+    _lib.check(L.cc_timer_create(3 * NI, C.byref(timer)))
+    g_t = sim.capture(NI, timer=timer)
+    c2 = sim.check(collect_raster=False)
+    g_t.replay()
+    torch.cuda.synchronize(dev)
+    sim.t += NI
+    c3 = sim.check(collect_raster=False)
+    t_del = [L.cc_timer_elapsed_ms(timer, 3 * i, 3 * i + 1) for i in range(NI)]
+    t_neu = [L.cc_timer_elapsed_ms(timer, 3 * i + 1, 3 * i + 2) for i in range(NI)]
+    L.cc_timer_destroy(timer)
+    rec_i = c3.rec_events - c2.rec_events
+    del_ms, neu_ms = float(np.sum(t_del)), float(np.sum(t_neu))
+    hbm, peak_src = peaks()
+    achieved = rec_i * BYTES_PER_EVENT / (del_ms / 1e3) / 1e9 if del_ms > 0 else 0.0
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("k_deliver", {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    kernels = {
+        "k_deliver": {"avg_us": 1e3 * del_ms / NI, "share": del_ms / (del_ms + neu_ms),
+                      "bytes_per_launch": rec_i * BYTES_PER_EVENT / NI},
+        "k_neuron": {"avg_us": 1e3 * neu_ms / NI, "share": neu_ms / (del_ms + neu_ms),
+                     "neuron_events_per_launch": (c3.rec_events + c3.ext_events
+                                                  - c2.rec_events - c2.ext_events) / NI},
+        "instrumented_steps": NI,
+        "instrumented_ms_per_step": (del_ms + neu_ms) / NI,
+    }
+    line = {
+        "metric": "synaptic events/s (recurrent + external)",
+        "value": value, "unit": "events/s", "n_gpus": 1, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: seeded counter-based RNG (connectivity, Poisson drive), "
+                "bit-exact with the reference streams",
+        "config": config_block(cfg, net, args),
+        "wall_s_per_sim_s": (ms / 1e3) / (K * cfg.timestep_ms / 1e3),
+        "recurrent_events_per_s": rec / (ms / 1e3),
+        "mean_rate_hz": spikes / (cfg.grid.n_neurons * K * cfg.timestep_ms / 1e3),
+        "roofline": {"bound": "hbm", "kernel": "k_deliver", "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                     "peak_source": peak_src,
+                     "bytes_per_event": BYTES_PER_EVENT},
+        "step_roofline": {"achieved": rec / (ms / 1e3) * BYTES_PER_EVENT / 1e9, "peak": hbm,
+                          "unit": "GB/s",
+                          "frac": rec / (ms / 1e3) * BYTES_PER_EVENT / 1e9 / hbm,
+                          "definition": "recurrent events/s x 17 B over the whole step "
+                                        "(BASELINE.md roofline formula)"},
+        "kernels": kernels,
+        "gpu_launches": 2 * K,
+        "clocks": clk,
+        "construction_s": net.construction_seconds,
+        "bytes_per_synapse_steady": net.steady_bytes / max(1, net.n_synapses),
+        "device_stats": {"max_bin": int(c1.max_bin), "max_events": int(c1.max_events),
+                         "overflow_records": int(c1.ovf_total),
+                         "spilled_neuron_steps": int(c1.spilled_total),
+                         "bin_cap": sim.shard.bin_cap},
+    }
+    del sim, g_main, g_rem, g_t
+    torch.cuda.empty_cache()
+    if not args.no_e2e:
+        res = run_b200(cfg, 1, net=net)
+        ev = res.recurrent_events + res.external_events
+        line["e2e"] = {"value": ev / res.sim_seconds_wall, "unit": "events/s",
+                       "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": (12 * res.n_spikes + 128 * math.ceil(
+                           cfg.n_steps / 100)) / cfg.n_steps,
+                       "api": "paper_1803_08833_b200.run_b200(config, 1) sim_seconds_wall",
+                       "steps": cfg.n_steps}
+    if not args.no_cpu:
+        cb = cpu_oracle_sample(cfg, net, float(os.environ.get("CC_CPU_BUDGET_S", "20")), 10 ** 9)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

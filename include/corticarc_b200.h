@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 3
+#define CC_ABI_VERSION 4
 
 /* error bits raised by kernels into cc_ctl.error_bits */
 #define CC_ERR_SPIKE_LOG      0x01u  /* more spikes in one step than log capacity   */
@@ -129,6 +129,13 @@ const char* cc_last_error(void);
 /* sizeof(cc_shard) and sizeof(cc_ctl) as compiled, so hosts can verify layout. */
 int64_t cc_sizeof_shard(void);
 int64_t cc_sizeof_ctl(void);
+
+/* CUDA-event timers usable inside captured CUDA graphs (records use
+ * cudaEventRecordExternal): per-kernel durations of graph replays. */
+int cc_timer_create(int32_t n, void** handle);
+int cc_timer_record(void* handle, int32_t i, void* stream);
+float cc_timer_elapsed_ms(void* handle, int32_t i, int32_t j);
+int cc_timer_destroy(void* handle);
 
 /* ------------------------------------------------------- simulation step */
 /* Initial state: V = V_r + u (V_theta - V_r), u = counter_uniforms(seed,

@@ -14,7 +14,7 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BIT
            "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 ERR_BITS = {
     0x01: "spike log full (more spikes in one step than planned)",
@@ -93,6 +93,10 @@ _SIGS = {
     "cc_sizeof_shard": (C.c_int64, []),
     "cc_sizeof_ctl": (C.c_int64, []),
     "cc_sizeof_gen": (C.c_int64, []),
+    "cc_timer_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
+    "cc_timer_record": (C.c_int, [C.c_void_p, C.c_int32, _P]),
+    "cc_timer_elapsed_ms": (C.c_float, [C.c_void_p, C.c_int32, C.c_int32]),
+    "cc_timer_destroy": (C.c_int, [C.c_void_p]),
     "cc_init_state": (C.c_int, [C.POINTER(Shard), _P]),
     "cc_deliver": (C.c_int, [C.POINTER(Shard), _P]),
     "cc_neuron_step": (C.c_int, [C.POINTER(Shard), _P]),

@@ -121,7 +121,7 @@ class Simulator:
     def __init__(self, cfg, net: DeviceNetwork, *, probes=None, probe_steps: int = 0,
                  bin_cap: Optional[int] = None, piece_len: int = 256, chunk: int = 100,
                  use_graphs: bool = True, direct_log: Optional[bool] = None,
-                 device=None):
+                 raster_steps: Optional[int] = None, device=None):
         import torch
         self.L = _lib.lib()
         self.torch = torch
@@ -148,7 +148,7 @@ class Simulator:
             raise MemoryBudgetError("spike log references exceed 32 bits")
         piece_cap = max(1, net.pieces_upper_bound(piece_len) * bound)
         ovf_cap = max(1024, n_local * 2)
-        raster_cap = max(1024, n_local * bound * self.chunk)
+        raster_cap = max(1024, n_local * bound * max(self.chunk, raster_steps or 0))
         scratch_cap = max(4096, n_local * 16)
         self.buf = dict(
             gid=T.from_numpy(gids.astype(np.uint32).view(np.int32)).to(dev),
@@ -251,6 +251,25 @@ class Simulator:
             for _ in range(steps):
                 self._launch_step(s)
         self._graph, self._graph_steps = g, steps
+
+    def capture(self, steps: int, timer=None, timer_base: int = 0):
+        """A CUDA graph of `steps` steps; with a timer (cc_timer_create handle)
+        event-record nodes bracket every kernel: events timer_base + 3*i,
+        +1, +2 around k_deliver / k_neuron of step i."""
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=torch.cuda.Stream(self.dev)):
+            s = torch.cuda.current_stream(self.dev).cuda_stream
+            for i in range(steps):
+                if timer is not None:
+                    _lib.check(self.L.cc_timer_record(timer, timer_base + 3 * i, s))
+                _lib.check(self.L.cc_deliver(C.byref(self.shard), s), "cc_deliver")
+                if timer is not None:
+                    _lib.check(self.L.cc_timer_record(timer, timer_base + 3 * i + 1, s))
+                _lib.check(self.L.cc_neuron_step(C.byref(self.shard), s), "cc_neuron_step")
+                if timer is not None:
+                    _lib.check(self.L.cc_timer_record(timer, timer_base + 3 * i + 2, s))
+        return g
 
     def advance(self, n_steps: int, collect_raster: bool = True) -> None:
         """Run n_steps more steps (chunks replayed from a CUDA graph)."""
