@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 4
+#define CC_ABI_VERSION 5
 
 /* error bits raised by kernels into cc_ctl.error_bits */
 #define CC_ERR_SPIKE_LOG      0x01u  /* more spikes in one step than log capacity   */
@@ -59,6 +59,8 @@ typedef struct cc_ctl {
     unsigned int pad0;
     unsigned long long spilled_total;     /* neuron-steps that spilled smem   */
     unsigned long long ovf_total;         /* records that went to overflow    */
+    unsigned int done_deliver;            /* last-block detection (deliver k.) */
+    unsigned int ovf_grouped;             /* records grouped for this step    */
 } cc_ctl;
 
 /* One shard's device state.  Layout documented in DESIGN.md section 3. */
@@ -104,6 +106,9 @@ typedef struct cc_shard {
     uint64_t* bin_rec;      /* [d_max][bin_cap][n_local] spike_ref | w_bits << 32 */
     uint32_t* ovf_rec;      /* [d_max][ovf_cap][4] {tgt, spike_ref, w_bits, 0}  */
     uint32_t* ovf_cnt;      /* [d_max]                                         */
+    uint32_t* ovf_sorted;   /* [ovf_cap][4] overflow of the current slot, grouped by target */
+    int32_t* ovf_off;       /* [n_local] start of a neuron's group in ovf_sorted */
+    int32_t* ovf_fill;      /* [n_local] grouping cursors (all zero between steps) */
 
     /* spike log (AER payloads, network.py:60-63) and delivery work list */
     double* log_t;          /* [log_slots][spk_cap]                            */
@@ -116,7 +121,7 @@ typedef struct cc_shard {
     double* raster_t;       /* [raster_cap]                                    */
     uint32_t* out_gid;      /* [out_cap] exchange out-list (direct_log == 0)   */
     double* out_t;          /* [out_cap]                                       */
-    float* scratch;         /* [scratch_cap][4] spill staging                  */
+    float* scratch;         /* [scratch_cap][12] spill staging (48 B per event) */
     const int32_t* probe_map; /* [n_local] probe slot or -1                    */
     double* probe_out;      /* [steps][n_probe][5] V c last refr V_end         */
     int64_t probe_steps;    /* rows in probe_out                               */

@@ -14,7 +14,7 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BIT
            "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 ERR_BITS = {
     0x01: "spike log full (more spikes in one step than planned)",
@@ -44,7 +44,7 @@ class Ctl(C.Structure):
         ("done_blocks", C.c_uint), ("error_bits", C.c_uint), ("error_step", C.c_longlong),
         ("max_bin", C.c_uint), ("max_events", C.c_uint), ("scratch_used", C.c_ulonglong),
         ("out_n", C.c_uint), ("pad0", C.c_uint), ("spilled_total", C.c_ulonglong),
-        ("ovf_total", C.c_ulonglong),
+        ("ovf_total", C.c_ulonglong), ("done_deliver", C.c_uint), ("ovf_grouped", C.c_uint),
     ]
 
 
@@ -66,6 +66,7 @@ class Shard(C.Structure):
         ("gid", _P), ("state", _P),
         ("row_off", _P), ("syn_tgt", _P), ("syn_w", _P), ("syn_d", _P),
         ("bin_cnt", _P), ("bin_rec", _P), ("ovf_rec", _P), ("ovf_cnt", _P),
+        ("ovf_sorted", _P), ("ovf_off", _P), ("ovf_fill", _P),
         ("log_t", _P), ("log_gid", _P), ("log_ctr", _P), ("pieces", _P),
         ("raster_gid", _P), ("raster_t", _P), ("out_gid", _P), ("out_t", _P),
         ("scratch", _P), ("probe_map", _P), ("probe_out", _P),

@@ -18,7 +18,6 @@ namespace {
 
 constexpr int NEURON_BLOCK = 128;       // 4 warps
 constexpr int WARPS_PER_BLOCK = NEURON_BLOCK / 32;
-constexpr int WCAP = 512;               // staged events per warp in shared memory
 
 struct Ev {                              // one input event, 16 B
     double t;                            // arrival time, ms
@@ -31,6 +30,21 @@ __device__ __forceinline__ bool ev_less(const Ev& a, const Ev& b) {
     // whose weights are equal too, so this is the reference's total order
     // lexsort((w, src, tm, tgt)) restricted to one target (engine.py:386).
     return a.t < b.t || (a.t == b.t && a.src < b.src);
+}
+
+// Shell sort (Ciura gaps) degenerating to insertion sort for short inputs.
+__device__ __forceinline__ void sort_events(Ev* seg, uint32_t n) {
+    const uint32_t gaps[8] = {701u, 301u, 132u, 57u, 23u, 10u, 4u, 1u};
+    for (int gi = (n > 32 ? 0 : 7); gi < 8; ++gi) {
+        const uint32_t g = gaps[gi];
+        if (g >= n) continue;
+        for (uint32_t i = g; i < n; ++i) {
+            const Ev key = seg[i];
+            uint32_t j = i;
+            while (j >= g && ev_less(key, seg[j - g])) { seg[j] = seg[j - g]; j -= g; }
+            seg[j] = key;
+        }
+    }
 }
 
 __device__ __forceinline__ long long pos_mod(long long a, long long m) {
@@ -124,19 +138,94 @@ __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, i
     return ev;
 }
 
+// ------------------------------------------------------------------ k_neuron
+// A warp owns 32 consecutive neurons.  Their inputs pass through a per-warp
+// shared-memory buffer in rounds (all of a round's work is spread over the 32
+// lanes, so one bursty neuron does not serialise its warp):
+//   1 gather   recurrent records, flattened in k-major order (coalesced)
+//   2 drive    external Poisson events (per lane)
+//   3 sort     rank sort of every neuron's segment by (t, src), flattened
+//   4 factors  em = exp(-dt/tau_m), ec, f (model.py:116-143) for every event,
+//              flattened, assuming refractory window and fatigue as at step
+//              start (exactly the values the serial update would compute)
+//   5 update   per lane, in event order: the cheap affine update, jump,
+//              threshold, reset; after a spike the remaining factors of that
+//              neuron are recomputed in line.
+struct WarpLayout {
+    int wcap, kcap;
+    __host__ __device__ size_t bytes() const {
+        size_t b = (size_t)wcap * (8 * 4 + 4 + 4 + 2);
+        b = (b + 15) & ~(size_t)15;
+        b += (size_t)(kcap + 1) * 4 + (size_t)kcap * 4 + 33 * 4 + 32 * (8 + 8 + 4);
+        return (b + 15) & ~(size_t)15;
+    }
+};
+
+struct WarpBuf {
+    double* t; double* em; double* ec; double* f;
+    uint32_t* src; float* w; uint16_t* perm;
+    uint32_t* lvl_off; uint32_t* lvl_mask; int* seg;
+    double* o_last; double* o_ru; uint32_t* o_flag;
+};
+
+__device__ __forceinline__ WarpBuf carve(char* base, int wcap, int kcap) {
+    WarpBuf b;
+    char* p = base;
+    b.t = (double*)p; p += wcap * 8;
+    b.em = (double*)p; p += wcap * 8;
+    b.ec = (double*)p; p += wcap * 8;
+    b.f = (double*)p; p += wcap * 8;
+    b.src = (uint32_t*)p; p += wcap * 4;
+    b.w = (float*)p; p += wcap * 4;
+    b.perm = (uint16_t*)p; p += wcap * 2;
+    p = (char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+    b.lvl_off = (uint32_t*)p; p += (kcap + 1) * 4;
+    b.lvl_mask = (uint32_t*)p; p += kcap * 4;
+    b.seg = (int*)p; p += 33 * 4;
+    p = (char*)(((uintptr_t)p + 7) & ~(uintptr_t)7);
+    b.o_last = (double*)p; p += 32 * 8;
+    b.o_ru = (double*)p; p += 32 * 8;
+    b.o_flag = (uint32_t*)p;
+    return b;
+}
+
+// decay factors of one event (the dt-dependent part of _voltage_decay)
+__device__ __forceinline__ void decay_factors(const cc_pop& P, double dt, bool with_c,
+                                              double& em, double& ec, double& f) {
+    em = exp(-dt / P.tau_m);
+    ec = 1.0;
+    f = 0.0;
+    if (with_c) {
+        ec = exp(-dt / P.tau_c);
+        const double x = dt * P.k1 / P.k2;
+        if (x == 0.0)
+            f = dt * em;
+        else if (fabs(x) <= 1.0)
+            f = dt * em * expm1(x) / x;
+        else
+            f = dt * (ec - em) / x;
+    }
+}
+
+constexpr int NEURON_WCAP = 320;
+
 template <bool PROBE>
 __global__ void __launch_bounds__(NEURON_BLOCK)
 k_neuron(const cc_shard sh) {
-    __shared__ Ev stage[WARPS_PER_BLOCK][WCAP];
+    extern __shared__ __align__(16) char nsm[];
     cc_ctl* ctl = sh.ctl;
     const long long t = *(volatile long long*)&ctl->t;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int li = blockIdx.x * NEURON_BLOCK + threadIdx.x;
+    const WarpLayout lay{NEURON_WCAP, sh.bin_cap};
+    WarpBuf B = carve(nsm + warp * lay.bytes(), NEURON_WCAP, sh.bin_cap);
+    const int li0 = blockIdx.x * NEURON_BLOCK + warp * 32;
+    const int li = li0 + lane;
     const bool active = li < sh.n_local;
     const int D = sh.d_max;
     const int slot = (int)pos_mod(t, D);
     const int t_mod_l = (int)pos_mod(t, sh.log_slots);
+    const uint32_t K = (uint32_t)sh.bin_cap;
 
     uint32_t gid = 0, n_r = 0, n_e = 0;
     int pop = 0;
@@ -163,6 +252,7 @@ k_neuron(const cc_shard sh) {
         }
     }
     const uint32_t n = n_r + n_e;
+    const uint32_t nb = min(n_r, K);
     NState s{0.0, 0.0, 0.0, 0.0};
     double* st = sh.state + (size_t)(active ? li : 0) * 4;
     if (active && (n || PROBE)) {
@@ -171,97 +261,203 @@ k_neuron(const cc_shard sh) {
         s = NState{a.x, a.y, b.x, b.y};
     }
     const cc_pop& P = sh.pop[pop];
-    const uint32_t nb = min(n_r, (uint32_t)sh.bin_cap);
+    B.o_last[lane] = s.last;
+    B.o_ru[lane] = s.ru;
+    B.o_flag[lane] = (uint32_t)pop | (s.c != 0.0 ? 2u : 0u);
     uint32_t my_spikes = 0;
-    // The warp's neurons pass through the shared staging buffer in rounds:
-    // every round admits the pending lanes whose inputs fit behind the lanes
-    // before them; the first pending lane always goes (spilling to global
-    // scratch only when it alone exceeds the buffer).
     bool pending = active && n > 0;
     while (__any_sync(0xffffffffu, pending)) {
+        // ---- admission: lanes whose inputs fit behind the earlier ones
         uint32_t tot;
         const uint32_t off = warp_excl_scan(pending ? n : 0u, tot);
-        bool go = pending && (off + n <= (uint32_t)WCAP || off == 0);
-        Ev* seg = nullptr;
-        if (go) {
-            if (n <= (uint32_t)WCAP) {
-                seg = &stage[warp][off];
-            } else {
-                const unsigned long long at = atomicAdd(&ctl->scratch_used, (unsigned long long)n);
-                if (at + n > (unsigned long long)sh.scratch_cap) {
-                    cc_raise(ctl, CC_ERR_SCRATCH, t);
-                    go = false;
-                    pending = false;
-                } else {
-                    seg = reinterpret_cast<Ev*>(sh.scratch) + at;
-                    atomicAdd(&ctl->spilled_total, 1ull);
+        bool go = pending && (off + n <= (uint32_t)NEURON_WCAP);
+        bool big = false;                       // alone larger than the buffer
+        if (!__any_sync(0xffffffffu, go)) {     // first pending lane has > WCAP inputs
+            const unsigned pm = __ballot_sync(0xffffffffu, pending);
+            big = lane == __ffs(pm) - 1;
+            go = big;
+        }
+        const uint32_t my_len = go ? n : 0u;
+        const uint32_t my_off = big ? 0u : off;
+        // segment table (in this round's buffer coordinates)
+        uint32_t rtot;
+        const uint32_t roff = warp_excl_scan(my_len, rtot);
+        (void)my_off;
+        B.seg[lane] = (int)roff;
+        if (lane == 31) B.seg[32] = (int)rtot;
+        // event arrays: shared buffer, or global scratch for a single huge neuron
+        double* Et = B.t; uint32_t* Es = B.src; float* Ew = B.w; uint16_t* Ep = B.perm;
+        double* Fm = B.em; double* Fc = B.ec; double* Ff = B.f;
+        bool ok = true;
+        if (__any_sync(0xffffffffu, big)) {
+            unsigned long long at = 0;
+            if (big) {
+                if (n > 65535u) { cc_raise(ctl, CC_ERR_SCRATCH, t); ok = false; }
+                at = atomicAdd(&ctl->scratch_used, (unsigned long long)n);
+                if (at + n > (unsigned long long)sh.scratch_cap) { cc_raise(ctl, CC_ERR_SCRATCH, t); ok = false; }
+                atomicAdd(&ctl->spilled_total, 1ull);
+            }
+            ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, __ffs(__ballot_sync(0xffffffffu, big)) - 1);
+            at = __shfl_sync(0xffffffffu, at, __ffs(__ballot_sync(0xffffffffu, big)) - 1);
+            // spill layout: 6 words of 8 B per event (t, em, ec, f, src|w, perm)
+            double* base = reinterpret_cast<double*>(sh.scratch) + at * 6;
+            const uint32_t cap = rtot;
+            Et = base; Fm = base + cap; Fc = base + 2 * cap; Ff = base + 3 * cap;
+            Es = reinterpret_cast<uint32_t*>(base + 4 * cap);
+            Ew = reinterpret_cast<float*>(Es + cap);
+            Ep = reinterpret_cast<uint16_t*>(base + 5 * cap);
+            if (!ok) { pending = false; go = false; }
+        }
+        __syncwarp();
+        // ---- 1 gather recurrent records, k-major flattened
+        const uint32_t nbr = go ? nb : 0u;
+        uint32_t kmax = nbr;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+        {
+            uint32_t acc = 0;
+            for (uint32_t k = 0; k < kmax; ++k) {
+                const unsigned m = __ballot_sync(0xffffffffu, nbr > k);
+                if (lane == 0) { B.lvl_mask[k] = m; B.lvl_off[k] = acc; }
+                acc += __popc(m);
+            }
+            if (lane == 0) B.lvl_off[kmax] = acc;
+        }
+        __syncwarp();
+        const uint32_t R = B.lvl_off[kmax];
+        {
+            const uint64_t* bins = sh.bin_rec + (size_t)slot * K * sh.n_local + li0;
+            uint32_t k = 0;
+            for (uint32_t r0 = 0; r0 < R; r0 += 128) {
+                uint64_t rec[4];
+                int dst[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t r = r0 + u * 32 + lane;
+                    dst[u] = -1;
+                    if (r < R) {
+                        while (B.lvl_off[k + 1] <= r) ++k;
+                        const unsigned m = B.lvl_mask[k];
+                        const int owner = __fns(m, 0, (int)(r - B.lvl_off[k]) + 1);
+                        rec[u] = bins[(size_t)k * sh.n_local + owner];
+                        dst[u] = B.seg[owner] + (int)k;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (dst[u] >= 0) {
+                        const Ev ev = make_rec_event(sh, rec[u], t_mod_l);
+                        Et[dst[u]] = ev.t; Es[dst[u]] = ev.src; Ew[dst[u]] = ev.w;
+                    }
                 }
             }
         }
-        // recurrent records, k-major: lanes of a warp read consecutive words
-        const uint32_t mine = go ? nb : 0u;
-        uint32_t kmax = mine;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-        for (uint32_t k = 0; k < kmax; ++k) {
-            if (k < mine) {
-                const uint64_t rec = sh.bin_rec[((size_t)slot * sh.bin_cap + k) * sh.n_local + li];
-                seg[k] = make_rec_event(sh, rec, t_mod_l);
+        // ---- overflow surplus (grouped by k_deliver) and external drive
+        if (go) {
+            const int b0 = (int)roff;
+            if (n_r > nb) {
+                const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + sh.ovf_off[li];
+                for (uint32_t k = 0; k < n_r - nb; ++k) {
+                    const uint4 r = ov[k];
+                    const Ev ev = make_rec_event(sh, (uint64_t)r.y | ((uint64_t)r.z << 32), t_mod_l);
+                    Et[b0 + nb + k] = ev.t; Es[b0 + nb + k] = ev.src; Ew[b0 + nb + k] = ev.w;
+                }
             }
-        }
-        if (go && n_r > nb) {           // this neuron's surplus sits in the overflow list
-            uint32_t got = nb;
-            const uint32_t no = min(sh.ovf_cnt[slot], (uint32_t)sh.ovf_cap);
-            const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_rec) + (size_t)slot * sh.ovf_cap;
-            for (uint32_t i = 0; i < no && got < n_r; ++i) {
-                const uint4 r = ov[i];
-                if (r.x == (uint32_t)li)
-                    seg[got++] = make_rec_event(sh, (uint64_t)r.y | ((uint64_t)r.z << 32), t_mod_l);
-            }
-        }
-        if (go && n_e) {
-            // event times (t_step + u) * dt, u = counter_uniforms(EXTERNAL_TIME, gid, t, j)
-            const uint64_t h4 = cc_splitmix64(cc_splitmix64(sh.h2_time ^ (uint64_t)gid)
-                                              ^ (uint64_t)t);
-            for (uint32_t k = 0; k < n_e; ++k) {
-                Ev ev;
-                ev.t = ((double)t + cc_u53(cc_splitmix64(h4 ^ (uint64_t)k))) * sh.dt;
-                ev.src = CC_EXT_SRC;
-                ev.w = 0.0f;
-                seg[n_r + k] = ev;
+            if (n_e) {
+                // event times (t_step + u) * dt, u = counter_uniforms(EXTERNAL_TIME, gid, t, j)
+                const uint64_t h4 = cc_splitmix64(cc_splitmix64(sh.h2_time ^ (uint64_t)gid)
+                                                  ^ (uint64_t)t);
+                for (uint32_t k = 0; k < n_e; ++k) {
+                    Et[b0 + n_r + k] = ((double)t + cc_u53(cc_splitmix64(h4 ^ (uint64_t)k))) * sh.dt;
+                    Es[b0 + n_r + k] = CC_EXT_SRC;
+                    Ew[b0 + n_r + k] = 0.0f;
+                }
             }
         }
         __syncwarp();
-        if (go) {
-            // insertion sort of this neuron's inputs
-            for (uint32_t i = 1; i < n; ++i) {
-                const Ev key = seg[i];
-                uint32_t j = i;
-                while (j > 0 && ev_less(key, seg[j - 1])) { seg[j] = seg[j - 1]; --j; }
-                seg[j] = key;
+        // ---- 3 rank sort: perm[seg + rank(e)] = e
+        {
+            int owner = 0;
+            for (uint32_t e = lane; e < rtot; e += 32) {
+                while (B.seg[owner + 1] <= (int)e) ++owner;
+                const int a = B.seg[owner], z = B.seg[owner + 1];
+                const double te = Et[e];
+                const uint32_t se = Es[e];
+                int rank = 0;
+                for (int q = a; q < z; ++q) {
+                    const double tq = Et[q];
+                    const uint32_t sq = Es[q];
+                    rank += (tq < te || (tq == te && (sq < se || (sq == se && q < (int)e)))) ? 1 : 0;
+                }
+                Ep[a + rank] = (uint16_t)(e - a);
             }
+        }
+        __syncwarp();
+        // ---- 4 decay factors for every event, assuming step-start ru and c
+        {
+            int owner = 0;
+            for (uint32_t p = lane; p < rtot; p += 32) {
+                while (B.seg[owner + 1] <= (int)p) ++owner;
+                const int a = B.seg[owner];
+                const double te = Et[a + Ep[p]];
+                const double last = (int)p == a ? B.o_last[owner] : Et[a + Ep[p - 1]];
+                const double ru = B.o_ru[owner];
+                const uint32_t fl = B.o_flag[owner];
+                const double ff = fmin(fmax(last, ru), te);
+                double em, ec, f;
+                decay_factors(sh.pop[fl & 1u], te - ff, (fl & 2u) != 0, em, ec, f);
+                Fm[p] = em; Fc[p] = ec; Ff[p] = f;
+            }
+        }
+        __syncwarp();
+        // ---- 5 in-order update per neuron
+        if (go) {
+            const int a = (int)roff;
+            bool dirty = false;                   // spiked: factors must be recomputed
             for (uint32_t i = 0; i < n; ++i) {
-                const Ev ev = seg[i];
-                advance(s, P, ev.t);
-                if (ev.t >= s.ru) {
-                    const double w = (ev.src == CC_EXT_SRC) ? sh.ext_weight : (double)ev.w;
+                const int e = a + Ep[a + i];
+                const double te = Et[e];
+                const double ff = fmin(fmax(s.last, s.ru), te);
+                double cs = s.c;
+                if (ff != s.last && cs != 0.0)
+                    cs = cs * exp(-(ff - s.last) / P.tau_c);
+                const double Vs = (s.last < s.ru) ? P.V_r : s.V;
+                double em, ec, f;
+                if (dirty) {
+                    decay_factors(P, te - ff, cs != 0.0, em, ec, f);
+                } else {
+                    em = Fm[a + i]; ec = Fc[a + i]; f = Ff[a + i];
+                }
+                double Vt = P.E + (Vs - P.E) * em;
+                double ct = cs;
+                if (cs != 0.0) {
+                    Vt = Vt - P.sfa * cs * f;
+                    ct = cs * ec;
+                }
+                s.V = (te < s.ru) ? P.V_r : Vt;
+                s.c = ct;
+                s.last = te;
+                if (te >= s.ru) {
+                    const uint32_t src = Es[e];
+                    const double w = (src == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
                     const double V = s.V + w;
                     if (V > P.V_theta) {                 // strict threshold
                         s.V = P.V_r;
                         s.c = s.c + P.alpha_c;
-                        s.ru = ev.t + P.tau_arp;
+                        s.ru = te + P.tau_arp;
+                        dirty = true;
                         ++my_spikes;
                         if (sh.direct_log) {
-                            log_spike(sh, t, gid, ev.t);
+                            log_spike(sh, t, gid, te);
                         } else {
                             const unsigned o = atomicAdd(&ctl->out_n, 1u);
-                            if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = ev.t; }
+                            if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = te; }
                             else cc_raise(ctl, CC_ERR_OUTLIST, t);
                         }
                         const unsigned long long r = atomicAdd(&ctl->raster_n, 1ull);
                         if (r < (unsigned long long)sh.raster_cap) {
                             sh.raster_gid[r] = gid;
-                            sh.raster_t[r] = ev.t;
+                            sh.raster_t[r] = te;
                         } else {
                             cc_raise(ctl, CC_ERR_RASTER, t);
                         }
@@ -316,6 +512,56 @@ k_neuron(const cc_shard sh) {
             *(volatile long long*)&ctl->t = t + 1;
         }
     }
+}
+
+// Counting sort of one slot's overflow records by target, by a single block
+// (only runs in steps that overflowed the dense bins).
+__device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
+    __shared__ uint32_t wsum[32];
+    __shared__ uint32_t carry;
+    const int n = sh.n_local;
+    const uint32_t K = (uint32_t)sh.bin_cap;
+    const uint32_t* cnt = sh.bin_cnt + (size_t)s * n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const uint32_t c = i < n ? cnt[i] : 0u;
+        const uint32_t v = c > K ? c - K : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = lane < nwarp ? wsum[lane] : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            if (lane < nwarp) wsum[lane] = w;
+        }
+        __syncthreads();
+        const uint32_t before = carry + (warp ? wsum[warp - 1] : 0u) + x - v;
+        if (v) sh.ovf_off[i] = (int32_t)before;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += wsum[nwarp - 1];
+        __syncthreads();
+    }
+    const uint4* rec = reinterpret_cast<const uint4*>(sh.ovf_rec) + (size_t)s * sh.ovf_cap;
+    uint4* out = reinterpret_cast<uint4*>(sh.ovf_sorted);
+    for (unsigned j = threadIdx.x; j < m; j += blockDim.x) {
+        const uint4 r = rec[j];
+        const int p = sh.ovf_off[r.x] + atomicAdd(&sh.ovf_fill[r.x], 1);
+        out[p] = r;
+    }
+    __syncthreads();
+    for (unsigned j = threadIdx.x; j < m; j += blockDim.x) sh.ovf_fill[rec[j].x] = 0;
 }
 
 // One warp per delivery piece (<= piece_len synapses of one spiking source).
@@ -386,6 +632,23 @@ k_deliver(const cc_shard sh) {
         }
     }
     if (lane == 0 && events) atomicAdd(&ctl->rec_events, events);
+
+    // Arrival step t is complete now (k_deliver(t) is its last depositor): the
+    // last block out groups its overflow records by target for k_neuron(t).
+    __shared__ bool am_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        am_last = atomicAdd(&ctl->done_deliver, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    const int s = (int)pos_mod(t, D);
+    const unsigned m = min(*(volatile unsigned*)&sh.ovf_cnt[s], (unsigned)sh.ovf_cap);
+    if (threadIdx.x == 0) { ctl->done_deliver = 0; ctl->ovf_grouped = m; }
+    if (m == 0) return;
+    group_overflow(sh, s, m);
 }
 
 // Multi-shard receive: log the AER events of step ctl->t - 1 that have rows here.
@@ -467,10 +730,17 @@ extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_neuron_step: null shard");
     if (sh->n_local <= 0) return cc_set_error("cc_neuron_step: empty shard");
     const int blocks = (sh->n_local + NEURON_BLOCK - 1) / NEURON_BLOCK;
+    const size_t smem = WarpLayout{NEURON_WCAP, sh->bin_cap}.bytes() * WARPS_PER_BLOCK;
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaFuncSetAttribute(k_neuron<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_neuron<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
     if (sh->n_probe > 0)
-        k_neuron<true><<<blocks, NEURON_BLOCK, 0, (cudaStream_t)stream>>>(*sh);
+        k_neuron<true><<<blocks, NEURON_BLOCK, smem, (cudaStream_t)stream>>>(*sh);
     else
-        k_neuron<false><<<blocks, NEURON_BLOCK, 0, (cudaStream_t)stream>>>(*sh);
+        k_neuron<false><<<blocks, NEURON_BLOCK, smem, (cudaStream_t)stream>>>(*sh);
     return cc_check_launch("k_neuron");
 }
 

@@ -108,6 +108,15 @@ def _pop(p) -> _lib.Pop:
     return q
 
 
+def default_bin_cap(cfg) -> int:
+    """Dense records per (slot, neuron): ~3x the mean recurrent input per step
+    at 20 Hz plus headroom, a power of two in [64, 512]; the surplus of rarer
+    bursts goes through the grouped overflow list."""
+    from .geometry import expected_fanout
+    want = 3.0 * expected_fanout(cfg.kernel, cfg.grid) * 0.02 * cfg.timestep_ms + 32
+    return int(min(512, max(64, 1 << int(math.ceil(math.log2(want))))))
+
+
 def _spikes_per_step_bound(cfg) -> int:
     taus = [cfg.exc_params.tau_arp, cfg.inh_params.tau_arp]
     if min(taus) <= 0:
@@ -137,7 +146,7 @@ class Simulator:
         D = cfg.d_max
         bound = _spikes_per_step_bound(cfg)
         if bin_cap is None:
-            bin_cap = 64
+            bin_cap = default_bin_cap(cfg)
         self.chunk = max(1, int(chunk))
         self.use_graphs = use_graphs
         direct = (net.size == 1) if direct_log is None else direct_log
@@ -147,9 +156,9 @@ class Simulator:
         if spk_cap * (D + 1) >= 2 ** 32:
             raise MemoryBudgetError("spike log references exceed 32 bits")
         piece_cap = max(1, net.pieces_upper_bound(piece_len) * bound)
-        ovf_cap = max(1024, n_local * 2)
+        ovf_cap = max(4096, n_local * 8)
         raster_cap = max(1024, n_local * bound * max(self.chunk, raster_steps or 0))
-        scratch_cap = max(4096, n_local * 16)
+        scratch_cap = max(1 << 16, n_local * 16)
         self.buf = dict(
             gid=T.from_numpy(gids.astype(np.uint32).view(np.int32)).to(dev),
             state=T.zeros((n_local, 4), dtype=f64, device=dev),
@@ -157,6 +166,9 @@ class Simulator:
             bin_rec=T.empty((D, bin_cap, n_local), dtype=i64, device=dev),
             ovf_rec=T.empty((D, ovf_cap, 4), dtype=i32, device=dev),
             ovf_cnt=T.zeros(D, dtype=i32, device=dev),
+            ovf_sorted=T.empty((ovf_cap, 4), dtype=i32, device=dev),
+            ovf_off=T.empty(n_local, dtype=i32, device=dev),
+            ovf_fill=T.zeros(n_local, dtype=i32, device=dev),
             log_t=T.empty((D + 1, spk_cap), dtype=f64, device=dev),
             log_gid=T.empty((D + 1, spk_cap), dtype=i32, device=dev),
             log_ctr=T.zeros(D + 1, dtype=i64, device=dev),
@@ -165,7 +177,7 @@ class Simulator:
             raster_t=T.empty(raster_cap, dtype=f64, device=dev),
             out_gid=T.empty(max(1, n_local * bound), dtype=i32, device=dev),
             out_t=T.empty(max(1, n_local * bound), dtype=f64, device=dev),
-            scratch=T.empty((scratch_cap, 4), dtype=T.float32, device=dev),
+            scratch=T.empty((scratch_cap, 12), dtype=T.float32, device=dev),   # 48 B/event
             probe_map=T.full((n_local,), -1, dtype=i32, device=dev),
             ctl=T.zeros(C.sizeof(_lib.Ctl) // 8, dtype=i64, device=dev),
         )
@@ -203,7 +215,8 @@ class Simulator:
         sh.gid, sh.state = b["gid"].data_ptr(), b["state"].data_ptr()
         sh.row_off, sh.syn_tgt = net.row_off.data_ptr(), net.syn_tgt.data_ptr()
         sh.syn_w, sh.syn_d = net.syn_w.data_ptr(), net.syn_d.data_ptr()
-        for k in ("bin_cnt", "bin_rec", "ovf_rec", "ovf_cnt", "log_t", "log_gid", "log_ctr",
+        for k in ("bin_cnt", "bin_rec", "ovf_rec", "ovf_cnt", "ovf_sorted", "ovf_off",
+                  "ovf_fill", "log_t", "log_gid", "log_ctr",
                   "pieces", "raster_gid", "raster_t", "out_gid", "out_t", "scratch",
                   "probe_map", "probe_out", "ctl"):
             setattr(sh, k, b[k].data_ptr())
