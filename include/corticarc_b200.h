@@ -121,7 +121,7 @@ typedef struct cc_shard {
     double* raster_t;       /* [raster_cap]                                    */
     uint32_t* out_gid;      /* [out_cap] exchange out-list (direct_log == 0)   */
     double* out_t;          /* [out_cap]                                       */
-    float* scratch;         /* [scratch_cap][12] spill staging (48 B per event) */
+    float* scratch;         /* [scratch_cap][14] spill staging (56 B per event) */
     const int32_t* probe_map; /* [n_local] probe slot or -1                    */
     double* probe_out;      /* [steps][n_probe][5] V c last refr V_end         */
     int64_t probe_steps;    /* rows in probe_out                               */

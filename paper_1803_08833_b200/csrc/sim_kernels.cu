@@ -139,62 +139,65 @@ __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, i
 }
 
 // ------------------------------------------------------------------ k_neuron
-// A warp owns 32 consecutive neurons.  Their inputs pass through a per-warp
-// shared-memory buffer in rounds (all of a round's work is spread over the 32
-// lanes, so one bursty neuron does not serialise its warp):
-//   1 gather   recurrent records, flattened in k-major order (coalesced)
-//   2 drive    external Poisson events (per lane)
-//   3 sort     rank sort of every neuron's segment by (t, src), flattened
-//   4 factors  em = exp(-dt/tau_m), ec, f (model.py:116-143) for every event,
-//              flattened, assuming refractory window and fatigue as at step
-//              start (exactly the values the serial update would compute)
-//   5 update   per lane, in event order: the cheap affine update, jump,
-//              threshold, reset; after a spike the remaining factors of that
-//              neuron are recomputed in line.
-struct WarpLayout {
-    int wcap, kcap;
-    __host__ __device__ size_t bytes() const {
-        size_t b = (size_t)wcap * (8 * 4 + 4 + 4 + 2);
-        b = (b + 15) & ~(size_t)15;
-        b += (size_t)(kcap + 1) * 4 + (size_t)kcap * 4 + 33 * 4 + 32 * (8 + 8 + 4);
-        return (b + 15) & ~(size_t)15;
-    }
-};
+// One warp (= one block) owns 32 consecutive neurons.  Their inputs pass
+// through the warp's shared-memory buffer in rounds, and every stage of a
+// round is spread over the 32 lanes so that a bursty neuron does not
+// serialise the warp:
+//   1 gather   recurrent records (owner-major, 4 loads in flight per lane),
+//              overflow surplus, external Poisson events
+//   2 sort     per neuron, counting sort on a monotone time bucket
+//              b(t) = clamp(floor((t - t0) * NB / dt)), then an insertion
+//              pass that only fixes order inside buckets: exact (t, src) order
+//   3 factors  em = exp(-dt/tau_m), ec, f (model.py:116-143) for every event,
+//              assuming the step-start refractory window and fatigue; these
+//              are exactly the values the serial update computes
+//   4 update   per lane, in event order: the affine update, jump, threshold,
+//              reset; after a spike the neuron's remaining factors are
+//              recomputed in line.
+constexpr int NEURON_WCAP = 320;           // events per round (10 per lane)
+constexpr int NBUCKET = 32;                // time buckets per neuron
 
 struct WarpBuf {
-    double* t; double* em; double* ec; double* f;
-    uint32_t* src; float* w; uint16_t* perm;
-    uint32_t* lvl_off; uint32_t* lvl_mask; int* seg;
+    double* t; double* em; double* ec; double* f; double* cd;
+    uint32_t* src; float* w; uint16_t* perm; uint8_t* own;
+    uint32_t* hist; int* seg;
     double* o_last; double* o_ru; uint32_t* o_flag;
 };
 
-__device__ __forceinline__ WarpBuf carve(char* base, int wcap, int kcap) {
+__host__ __device__ constexpr size_t warp_smem_bytes() {
+    return (size_t)NEURON_WCAP * (8 * 5 + 4 + 4 + 2 + 1) + 32 * NBUCKET * 4 + 34 * 4
+           + 32 * (8 + 8 + 4) + 64;
+}
+
+__device__ __forceinline__ WarpBuf carve(char* p) {
     WarpBuf b;
-    char* p = base;
-    b.t = (double*)p; p += wcap * 8;
-    b.em = (double*)p; p += wcap * 8;
-    b.ec = (double*)p; p += wcap * 8;
-    b.f = (double*)p; p += wcap * 8;
-    b.src = (uint32_t*)p; p += wcap * 4;
-    b.w = (float*)p; p += wcap * 4;
-    b.perm = (uint16_t*)p; p += wcap * 2;
-    p = (char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
-    b.lvl_off = (uint32_t*)p; p += (kcap + 1) * 4;
-    b.lvl_mask = (uint32_t*)p; p += kcap * 4;
-    b.seg = (int*)p; p += 33 * 4;
-    p = (char*)(((uintptr_t)p + 7) & ~(uintptr_t)7);
+    b.t = (double*)p; p += NEURON_WCAP * 8;
+    b.em = (double*)p; p += NEURON_WCAP * 8;
+    b.ec = (double*)p; p += NEURON_WCAP * 8;
+    b.f = (double*)p; p += NEURON_WCAP * 8;
+    b.cd = (double*)p; p += NEURON_WCAP * 8;
     b.o_last = (double*)p; p += 32 * 8;
     b.o_ru = (double*)p; p += 32 * 8;
-    b.o_flag = (uint32_t*)p;
+    b.src = (uint32_t*)p; p += NEURON_WCAP * 4;
+    b.w = (float*)p; p += NEURON_WCAP * 4;
+    b.hist = (uint32_t*)p; p += 32 * NBUCKET * 4;
+    b.seg = (int*)p; p += 34 * 4;
+    b.o_flag = (uint32_t*)p; p += 32 * 4;
+    b.perm = (uint16_t*)p; p += NEURON_WCAP * 2;
+    b.own = (uint8_t*)p;
     return b;
 }
 
 // decay factors of one event (the dt-dependent part of _voltage_decay)
 __device__ __forceinline__ void decay_factors(const cc_pop& P, double dt, bool with_c,
                                               double& em, double& ec, double& f) {
-    em = exp(-dt / P.tau_m);
     ec = 1.0;
     f = 0.0;
+    if (dt == 0.0) {            // exp(-0/tau) == 1, x == 0 -> f = 0 * 1: exact shortcut
+        em = 1.0;
+        return;
+    }
+    em = exp(-dt / P.tau_m);
     if (with_c) {
         ec = exp(-dt / P.tau_c);
         const double x = dt * P.k1 / P.k2;
@@ -207,25 +210,23 @@ __device__ __forceinline__ void decay_factors(const cc_pop& P, double dt, bool w
     }
 }
 
-constexpr int NEURON_WCAP = 320;
-
 template <bool PROBE>
-__global__ void __launch_bounds__(NEURON_BLOCK)
+__global__ void __launch_bounds__(32)
 k_neuron(const cc_shard sh) {
     extern __shared__ __align__(16) char nsm[];
     cc_ctl* ctl = sh.ctl;
     const long long t = *(volatile long long*)&ctl->t;
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const WarpLayout lay{NEURON_WCAP, sh.bin_cap};
-    WarpBuf B = carve(nsm + warp * lay.bytes(), NEURON_WCAP, sh.bin_cap);
-    const int li0 = blockIdx.x * NEURON_BLOCK + warp * 32;
+    const int lane = threadIdx.x;
+    WarpBuf B = carve(nsm);
+    const int li0 = blockIdx.x * 32;
     const int li = li0 + lane;
     const bool active = li < sh.n_local;
     const int D = sh.d_max;
     const int slot = (int)pos_mod(t, D);
     const int t_mod_l = (int)pos_mod(t, sh.log_slots);
     const uint32_t K = (uint32_t)sh.bin_cap;
+    const double t0 = (double)t * sh.dt;
+    const double bscale = (double)NBUCKET / sh.dt;
 
     uint32_t gid = 0, n_r = 0, n_e = 0;
     int pop = 0;
@@ -264,6 +265,7 @@ k_neuron(const cc_shard sh) {
     B.o_last[lane] = s.last;
     B.o_ru[lane] = s.ru;
     B.o_flag[lane] = (uint32_t)pop | (s.c != 0.0 ? 2u : 0u);
+    const uint64_t* bins = sh.bin_rec + (size_t)slot * K * sh.n_local + li0;
     uint32_t my_spikes = 0;
     bool pending = active && n > 0;
     while (__any_sync(0xffffffffu, pending)) {
@@ -271,76 +273,69 @@ k_neuron(const cc_shard sh) {
         uint32_t tot;
         const uint32_t off = warp_excl_scan(pending ? n : 0u, tot);
         bool go = pending && (off + n <= (uint32_t)NEURON_WCAP);
-        bool big = false;                       // alone larger than the buffer
-        if (!__any_sync(0xffffffffu, go)) {     // first pending lane has > WCAP inputs
+        bool big = false;                       // a single neuron larger than the buffer
+        if (!__any_sync(0xffffffffu, go)) {
             const unsigned pm = __ballot_sync(0xffffffffu, pending);
             big = lane == __ffs(pm) - 1;
             go = big;
         }
-        const uint32_t my_len = go ? n : 0u;
-        const uint32_t my_off = big ? 0u : off;
-        // segment table (in this round's buffer coordinates)
         uint32_t rtot;
-        const uint32_t roff = warp_excl_scan(my_len, rtot);
-        (void)my_off;
+        const uint32_t roff = warp_excl_scan(go ? n : 0u, rtot);
         B.seg[lane] = (int)roff;
         if (lane == 31) B.seg[32] = (int)rtot;
-        // event arrays: shared buffer, or global scratch for a single huge neuron
         double* Et = B.t; uint32_t* Es = B.src; float* Ew = B.w; uint16_t* Ep = B.perm;
-        double* Fm = B.em; double* Fc = B.ec; double* Ff = B.f;
-        bool ok = true;
+        double* Fm = B.em; double* Fc = B.ec; double* Ff = B.f; double* Fd = B.cd;
+        uint8_t* Eo = B.own;
         if (__any_sync(0xffffffffu, big)) {
+            const int bl = __ffs(__ballot_sync(0xffffffffu, big)) - 1;
             unsigned long long at = 0;
+            int ok = 1;
             if (big) {
-                if (n > 65535u) { cc_raise(ctl, CC_ERR_SCRATCH, t); ok = false; }
+                if (n > 65535u) ok = 0;
                 at = atomicAdd(&ctl->scratch_used, (unsigned long long)n);
-                if (at + n > (unsigned long long)sh.scratch_cap) { cc_raise(ctl, CC_ERR_SCRATCH, t); ok = false; }
+                if (at + n > (unsigned long long)sh.scratch_cap) ok = 0;
+                if (!ok) cc_raise(ctl, CC_ERR_SCRATCH, t);
                 atomicAdd(&ctl->spilled_total, 1ull);
             }
-            ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, __ffs(__ballot_sync(0xffffffffu, big)) - 1);
-            at = __shfl_sync(0xffffffffu, at, __ffs(__ballot_sync(0xffffffffu, big)) - 1);
-            // spill layout: 6 words of 8 B per event (t, em, ec, f, src|w, perm)
-            double* base = reinterpret_cast<double*>(sh.scratch) + at * 6;
+            ok = __shfl_sync(0xffffffffu, ok, bl);
+            at = __shfl_sync(0xffffffffu, at, bl);
+            // spill layout: 7 words of 8 B per event
+            double* base = reinterpret_cast<double*>(sh.scratch) + at * 7;
             const uint32_t cap = rtot;
             Et = base; Fm = base + cap; Fc = base + 2 * cap; Ff = base + 3 * cap;
-            Es = reinterpret_cast<uint32_t*>(base + 4 * cap);
+            Fd = base + 4 * cap;
+            Es = reinterpret_cast<uint32_t*>(base + 5 * cap);
             Ew = reinterpret_cast<float*>(Es + cap);
-            Ep = reinterpret_cast<uint16_t*>(base + 5 * cap);
-            if (!ok) { pending = false; go = false; }
+            Ep = reinterpret_cast<uint16_t*>(base + 6 * cap);
+            Eo = reinterpret_cast<uint8_t*>(Ep + cap);
+            if (!ok) { pending = false; go = false; B.seg[lane] = 0; if (lane == 31) B.seg[32] = 0; rtot = 0; }
         }
         __syncwarp();
-        // ---- 1 gather recurrent records, k-major flattened
-        const uint32_t nbr = go ? nb : 0u;
-        uint32_t kmax = nbr;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+        // ---- 1a gather recurrent records (owner-major flattened)
         {
-            uint32_t acc = 0;
-            for (uint32_t k = 0; k < kmax; ++k) {
-                const unsigned m = __ballot_sync(0xffffffffu, nbr > k);
-                if (lane == 0) { B.lvl_mask[k] = m; B.lvl_off[k] = acc; }
-                acc += __popc(m);
-            }
-            if (lane == 0) B.lvl_off[kmax] = acc;
-        }
-        __syncwarp();
-        const uint32_t R = B.lvl_off[kmax];
-        {
-            const uint64_t* bins = sh.bin_rec + (size_t)slot * K * sh.n_local + li0;
-            uint32_t k = 0;
+            const uint32_t nbr = go ? nb : 0u;
+            uint32_t R;
+            const uint32_t pr = warp_excl_scan(nbr, R);
+            B.hist[lane] = pr + nbr;                  // record ends (hist is reset below)
+            B.hist[32 + lane] = pr;                   // record starts
+            __syncwarp();
             for (uint32_t r0 = 0; r0 < R; r0 += 128) {
                 uint64_t rec[4];
-                int dst[4];
+                int dst[4], own[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t r = r0 + u * 32 + lane;
                     dst[u] = -1;
                     if (r < R) {
-                        while (B.lvl_off[k + 1] <= r) ++k;
-                        const unsigned m = B.lvl_mask[k];
-                        const int owner = __fns(m, 0, (int)(r - B.lvl_off[k]) + 1);
-                        rec[u] = bins[(size_t)k * sh.n_local + owner];
-                        dst[u] = B.seg[owner] + (int)k;
+                        int lo = 0, hi = 31;              // first lane whose records end after r
+                        while (lo < hi) {
+                            const int mid = (lo + hi) >> 1;
+                            if (B.hist[mid] > r) hi = mid; else lo = mid + 1;
+                        }
+                        const uint32_t k = r - B.hist[32 + lo];
+                        rec[u] = bins[(size_t)k * sh.n_local + lo];
+                        dst[u] = B.seg[lo] + (int)k;
+                        own[u] = lo;
                     }
                 }
 #pragma unroll
@@ -348,11 +343,13 @@ k_neuron(const cc_shard sh) {
                     if (dst[u] >= 0) {
                         const Ev ev = make_rec_event(sh, rec[u], t_mod_l);
                         Et[dst[u]] = ev.t; Es[dst[u]] = ev.src; Ew[dst[u]] = ev.w;
+                        Eo[dst[u]] = (uint8_t)own[u];
                     }
                 }
             }
+            __syncwarp();
         }
-        // ---- overflow surplus (grouped by k_deliver) and external drive
+        // ---- 1b overflow surplus (grouped by k_deliver) and external drive
         if (go) {
             const int b0 = (int)roff;
             if (n_r > nb) {
@@ -361,6 +358,7 @@ k_neuron(const cc_shard sh) {
                     const uint4 r = ov[k];
                     const Ev ev = make_rec_event(sh, (uint64_t)r.y | ((uint64_t)r.z << 32), t_mod_l);
                     Et[b0 + nb + k] = ev.t; Es[b0 + nb + k] = ev.src; Ew[b0 + nb + k] = ev.w;
+                    Eo[b0 + nb + k] = (uint8_t)lane;
                 }
             }
             if (n_e) {
@@ -371,46 +369,88 @@ k_neuron(const cc_shard sh) {
                     Et[b0 + n_r + k] = ((double)t + cc_u53(cc_splitmix64(h4 ^ (uint64_t)k))) * sh.dt;
                     Es[b0 + n_r + k] = CC_EXT_SRC;
                     Ew[b0 + n_r + k] = 0.0f;
+                    Eo[b0 + n_r + k] = (uint8_t)lane;
                 }
             }
         }
+#pragma unroll
+        for (int b = 0; b < NBUCKET; ++b) B.hist[lane * NBUCKET + b] = 0u;
         __syncwarp();
-        // ---- 3 rank sort: perm[seg + rank(e)] = e
+        // ---- 2 counting sort on the time bucket, then exact order inside buckets
         {
-            int owner = 0;
+            // (bucket key << 16 | rank in bucket) parked in the cd array until stage 3
+            uint32_t* keep = reinterpret_cast<uint32_t*>(Fd);
             for (uint32_t e = lane; e < rtot; e += 32) {
-                while (B.seg[owner + 1] <= (int)e) ++owner;
-                const int a = B.seg[owner], z = B.seg[owner + 1];
-                const double te = Et[e];
-                const uint32_t se = Es[e];
-                int rank = 0;
-                for (int q = a; q < z; ++q) {
-                    const double tq = Et[q];
-                    const uint32_t sq = Es[q];
-                    rank += (tq < te || (tq == te && (sq < se || (sq == se && q < (int)e)))) ? 1 : 0;
+                const int o = Eo[e];
+                double x = (Et[e] - t0) * bscale;
+                x = fmin(fmax(x, 0.0), (double)(NBUCKET - 1));
+                const uint32_t key = (uint32_t)(o * NBUCKET + (int)x);
+                keep[e] = (key << 16) | atomicAdd(&B.hist[key], 1u);
+            }
+            __syncwarp();
+            if (go) {                                   // per-neuron bucket starts
+                uint32_t acc = roff;
+#pragma unroll 4
+                for (int b = 0; b < NBUCKET; ++b) {
+                    const uint32_t c = B.hist[lane * NBUCKET + b];
+                    B.hist[lane * NBUCKET + b] = acc;
+                    acc += c;
                 }
-                Ep[a + rank] = (uint16_t)(e - a);
+            }
+            __syncwarp();
+            for (uint32_t e = lane; e < rtot; e += 32) {
+                const uint32_t kp = keep[e];
+                const uint32_t key = kp >> 16;
+                const int o = (int)(key / NBUCKET);
+                const uint32_t pos = B.hist[key] + (kp & 0xffffu);
+                Ep[pos] = (uint16_t)(e - (uint32_t)B.seg[o]);
+                Eo[pos] = (uint8_t)o;                   // owners now in sorted order
+            }
+            __syncwarp();
+            // lane b orders bucket b of every neuron (runs are short)
+            for (int o = 0; o < 32; ++o) {
+                const int a = B.seg[o];
+                if (B.seg[o + 1] == a) continue;
+                const int key = o * NBUCKET + lane;
+                const int r0 = (int)B.hist[key];
+                const int r1 = lane == NBUCKET - 1 ? B.seg[o + 1] : (int)B.hist[key + 1];
+                for (int i = r0 + 1; i < r1; ++i) {
+                    const uint16_t pi = Ep[i];
+                    const double ti = Et[a + pi];
+                    const uint32_t si = Es[a + pi];
+                    int j = i;
+                    while (j > r0) {
+                        const uint16_t pj = Ep[j - 1];
+                        const double tj = Et[a + pj];
+                        if (!(ti < tj || (ti == tj && si < Es[a + pj]))) break;
+                        Ep[j] = pj;
+                        --j;
+                    }
+                    Ep[j] = pi;
+                }
             }
         }
         __syncwarp();
-        // ---- 4 decay factors for every event, assuming step-start ru and c
+        // ---- 3 decay factors of every event, assuming the step-start refractory
+        //      window ru0 and fatigue flag (exactly the serial update's values)
         {
-            int owner = 0;
             for (uint32_t p = lane; p < rtot; p += 32) {
-                while (B.seg[owner + 1] <= (int)p) ++owner;
-                const int a = B.seg[owner];
+                const int o = Eo[p];
+                const int a = B.seg[o];
                 const double te = Et[a + Ep[p]];
-                const double last = (int)p == a ? B.o_last[owner] : Et[a + Ep[p - 1]];
-                const double ru = B.o_ru[owner];
-                const uint32_t fl = B.o_flag[owner];
+                const double last = (int)p == a ? B.o_last[o] : Et[a + Ep[p - 1]];
+                const double ru = B.o_ru[o];
+                const uint32_t fl = B.o_flag[o];
+                const cc_pop& Q = sh.pop[fl & 1u];
                 const double ff = fmin(fmax(last, ru), te);
                 double em, ec, f;
-                decay_factors(sh.pop[fl & 1u], te - ff, (fl & 2u) != 0, em, ec, f);
+                decay_factors(Q, te - ff, (fl & 2u) != 0, em, ec, f);
                 Fm[p] = em; Fc[p] = ec; Ff[p] = f;
+                Fd[p] = (ff != last && (fl & 2u)) ? exp(-(ff - last) / Q.tau_c) : 1.0;
             }
         }
         __syncwarp();
-        // ---- 5 in-order update per neuron
+        // ---- 4 in-order update per neuron
         if (go) {
             const int a = (int)roff;
             bool dirty = false;                   // spiked: factors must be recomputed
@@ -419,15 +459,16 @@ k_neuron(const cc_shard sh) {
                 const double te = Et[e];
                 const double ff = fmin(fmax(s.last, s.ru), te);
                 double cs = s.c;
-                if (ff != s.last && cs != 0.0)
-                    cs = cs * exp(-(ff - s.last) / P.tau_c);
-                const double Vs = (s.last < s.ru) ? P.V_r : s.V;
                 double em, ec, f;
-                if (dirty) {
-                    decay_factors(P, te - ff, cs != 0.0, em, ec, f);
-                } else {
+                if (!dirty) {
                     em = Fm[a + i]; ec = Fc[a + i]; f = Ff[a + i];
+                    if (ff != s.last && cs != 0.0) cs = cs * Fd[a + i];
+                } else {
+                    if (ff != s.last && cs != 0.0)
+                        cs = cs * exp(-(ff - s.last) / P.tau_c);
+                    decay_factors(P, te - ff, cs != 0.0, em, ec, f);
                 }
+                const double Vs = (s.last < s.ru) ? P.V_r : s.V;
                 double Vt = P.E + (Vs - P.E) * em;
                 double ct = cs;
                 if (cs != 0.0) {
@@ -499,10 +540,7 @@ k_neuron(const cc_shard sh) {
         if (s_sum) atomicAdd(&ctl->n_spikes, s_sum);
         if (mx_b > 0) atomicMax(&ctl->max_bin, mx_b);
         if (mx_e > 0) atomicMax(&ctl->max_events, mx_e);
-    }
-    // last block out advances the step counter and retires the slot
-    __syncthreads();
-    if (threadIdx.x == 0) {
+        // last block out advances the step counter and retires the slot
         __threadfence();
         const unsigned prev = atomicAdd(&ctl->done_blocks, 1u);
         if (prev == gridDim.x - 1) {
@@ -729,18 +767,18 @@ extern "C" int cc_deliver(const cc_shard* sh, void* stream) {
 extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_neuron_step: null shard");
     if (sh->n_local <= 0) return cc_set_error("cc_neuron_step: empty shard");
-    const int blocks = (sh->n_local + NEURON_BLOCK - 1) / NEURON_BLOCK;
-    const size_t smem = WarpLayout{NEURON_WCAP, sh->bin_cap}.bytes() * WARPS_PER_BLOCK;
-    static size_t configured = 0;
-    if (smem > configured) {
+    const int blocks = (sh->n_local + 31) / 32;
+    const size_t smem = warp_smem_bytes();
+    static bool configured = false;
+    if (!configured) {
         cudaFuncSetAttribute(k_neuron<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_neuron<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
+        configured = true;
     }
     if (sh->n_probe > 0)
-        k_neuron<true><<<blocks, NEURON_BLOCK, smem, (cudaStream_t)stream>>>(*sh);
+        k_neuron<true><<<blocks, 32, smem, (cudaStream_t)stream>>>(*sh);
     else
-        k_neuron<false><<<blocks, NEURON_BLOCK, smem, (cudaStream_t)stream>>>(*sh);
+        k_neuron<false><<<blocks, 32, smem, (cudaStream_t)stream>>>(*sh);
     return cc_check_launch("k_neuron");
 }
 

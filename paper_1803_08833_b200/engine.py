@@ -177,7 +177,7 @@ class Simulator:
             raster_t=T.empty(raster_cap, dtype=f64, device=dev),
             out_gid=T.empty(max(1, n_local * bound), dtype=i32, device=dev),
             out_t=T.empty(max(1, n_local * bound), dtype=f64, device=dev),
-            scratch=T.empty((scratch_cap, 12), dtype=T.float32, device=dev),   # 48 B/event
+            scratch=T.empty((scratch_cap, 14), dtype=T.float32, device=dev),   # 56 B/event
             probe_map=T.full((n_local,), -1, dtype=i32, device=dev),
             ctl=T.zeros(C.sizeof(_lib.Ctl) // 8, dtype=i64, device=dev),
         )
