@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 5
+#define CC_ABI_VERSION 6
 
 /* error bits raised by kernels into cc_ctl.error_bits */
 #define CC_ERR_SPIKE_LOG      0x01u  /* more spikes in one step than log capacity   */
@@ -83,6 +83,8 @@ typedef struct cc_shard {
     int32_t ext_budget;     /* m = ceil(lam + 12 sqrt(lam)) + 20; 0 = no drive */
     int32_t n_probe;
     int32_t direct_log;     /* 1: neuron kernel feeds the delivery log itself  */
+    int32_t debug_skip;     /* timing experiments only: bit mask of k_neuron stages to skip */
+    int32_t pad_;
     uint64_t h2_ext;        /* splitmix chain prefix for EXTERNAL (rng.py:85-86)      */
     uint64_t h2_time;       /* ... for EXTERNAL_TIME                                  */
     uint64_t h2_init;       /* ... for INIT_STATE                                     */

@@ -14,7 +14,7 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BIT
            "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 ERR_BITS = {
     0x01: "spike log full (more spikes in one step than planned)",
@@ -59,7 +59,7 @@ class Shard(C.Structure):
         ("ovf_cap", C.c_int64), ("piece_cap", C.c_int64), ("raster_cap", C.c_int64),
         ("scratch_cap", C.c_int64), ("n_rows", C.c_int64),
         ("out_cap", C.c_int32), ("ext_budget", C.c_int32), ("n_probe", C.c_int32),
-        ("direct_log", C.c_int32),
+        ("direct_log", C.c_int32), ("debug_skip", C.c_int32), ("pad_", C.c_int32),
         ("h2_ext", C.c_uint64), ("h2_time", C.c_uint64), ("h2_init", C.c_uint64),
         ("dt", C.c_double), ("ext_weight", C.c_double), ("ext_thresh", C.c_double),
         ("pop", Pop * 2),

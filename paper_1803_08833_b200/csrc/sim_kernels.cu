@@ -154,18 +154,18 @@ __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, i
 //   4 update   per lane, in event order: the affine update, jump, threshold,
 //              reset; after a spike the neuron's remaining factors are
 //              recomputed in line.
-constexpr int NEURON_WCAP = 320;           // events per round (10 per lane)
-constexpr int NBUCKET = 32;                // time buckets per neuron
+constexpr int NEURON_WCAP = 512;           // events per round (16 per lane)
+constexpr int NBUCKET = 8;                 // time buckets per neuron
 
 struct WarpBuf {
-    double* t; double* em; double* ec; double* f; double* cd;
+    double* t; double* em; double* ec; double* f;
     uint32_t* src; float* w; uint16_t* perm; uint8_t* own;
-    uint32_t* hist; int* seg;
+    uint32_t* hist; uint32_t* keep; int* seg;
     double* o_last; double* o_ru; uint32_t* o_flag;
 };
 
 __host__ __device__ constexpr size_t warp_smem_bytes() {
-    return (size_t)NEURON_WCAP * (8 * 5 + 4 + 4 + 2 + 1) + 32 * NBUCKET * 4 + 34 * 4
+    return (size_t)NEURON_WCAP * (8 * 4 + 4 + 4 + 2 + 1) + 64 * 4 + 34 * 4
            + 32 * (8 + 8 + 4) + 64;
 }
 
@@ -175,16 +175,16 @@ __device__ __forceinline__ WarpBuf carve(char* p) {
     b.em = (double*)p; p += NEURON_WCAP * 8;
     b.ec = (double*)p; p += NEURON_WCAP * 8;
     b.f = (double*)p; p += NEURON_WCAP * 8;
-    b.cd = (double*)p; p += NEURON_WCAP * 8;
     b.o_last = (double*)p; p += 32 * 8;
     b.o_ru = (double*)p; p += 32 * 8;
     b.src = (uint32_t*)p; p += NEURON_WCAP * 4;
     b.w = (float*)p; p += NEURON_WCAP * 4;
-    b.hist = (uint32_t*)p; p += 32 * NBUCKET * 4;
+    b.hist = (uint32_t*)p; p += 64 * 4;          // gather prefix tables (64 words)
     b.seg = (int*)p; p += 34 * 4;
     b.o_flag = (uint32_t*)p; p += 32 * 4;
     b.perm = (uint16_t*)p; p += NEURON_WCAP * 2;
     b.own = (uint8_t*)p;
+    b.keep = reinterpret_cast<uint32_t*>(b.f);   // sort scratch, dead before factors
     return b;
 }
 
@@ -284,7 +284,7 @@ k_neuron(const cc_shard sh) {
         B.seg[lane] = (int)roff;
         if (lane == 31) B.seg[32] = (int)rtot;
         double* Et = B.t; uint32_t* Es = B.src; float* Ew = B.w; uint16_t* Ep = B.perm;
-        double* Fm = B.em; double* Fc = B.ec; double* Ff = B.f; double* Fd = B.cd;
+        double* Fm = B.em; double* Fc = B.ec; double* Ff = B.f;
         uint8_t* Eo = B.own;
         if (__any_sync(0xffffffffu, big)) {
             const int bl = __ffs(__ballot_sync(0xffffffffu, big)) - 1;
@@ -299,20 +299,19 @@ k_neuron(const cc_shard sh) {
             }
             ok = __shfl_sync(0xffffffffu, ok, bl);
             at = __shfl_sync(0xffffffffu, at, bl);
-            // spill layout: 7 words of 8 B per event
-            double* base = reinterpret_cast<double*>(sh.scratch) + at * 7;
+            // spill layout: 6 words of 8 B per event
+            double* base = reinterpret_cast<double*>(sh.scratch) + at * 6;
             const uint32_t cap = rtot;
             Et = base; Fm = base + cap; Fc = base + 2 * cap; Ff = base + 3 * cap;
-            Fd = base + 4 * cap;
-            Es = reinterpret_cast<uint32_t*>(base + 5 * cap);
+            Es = reinterpret_cast<uint32_t*>(base + 4 * cap);
             Ew = reinterpret_cast<float*>(Es + cap);
-            Ep = reinterpret_cast<uint16_t*>(base + 6 * cap);
+            Ep = reinterpret_cast<uint16_t*>(base + 5 * cap);
             Eo = reinterpret_cast<uint8_t*>(Ep + cap);
             if (!ok) { pending = false; go = false; B.seg[lane] = 0; if (lane == 31) B.seg[32] = 0; rtot = 0; }
         }
         __syncwarp();
         // ---- 1a gather recurrent records (owner-major flattened)
-        {
+        if (!(sh.debug_skip & 1)) {
             const uint32_t nbr = go ? nb : 0u;
             uint32_t R;
             const uint32_t pr = warp_excl_scan(nbr, R);
@@ -373,67 +372,58 @@ k_neuron(const cc_shard sh) {
                 }
             }
         }
+        // ---- 2 counting sort on a monotone time bucket, per-lane exact fix-up
+        if (!(sh.debug_skip & 2)) {
+            uint32_t cnt[NBUCKET];
 #pragma unroll
-        for (int b = 0; b < NBUCKET; ++b) B.hist[lane * NBUCKET + b] = 0u;
-        __syncwarp();
-        // ---- 2 counting sort on the time bucket, then exact order inside buckets
-        {
-            // (bucket key << 16 | rank in bucket) parked in the cd array until stage 3
-            uint32_t* keep = reinterpret_cast<uint32_t*>(Fd);
-            for (uint32_t e = lane; e < rtot; e += 32) {
-                const int o = Eo[e];
-                double x = (Et[e] - t0) * bscale;
-                x = fmin(fmax(x, 0.0), (double)(NBUCKET - 1));
-                const uint32_t key = (uint32_t)(o * NBUCKET + (int)x);
-                keep[e] = (key << 16) | atomicAdd(&B.hist[key], 1u);
-            }
-            __syncwarp();
-            if (go) {                                   // per-neuron bucket starts
-                uint32_t acc = roff;
-#pragma unroll 4
-                for (int b = 0; b < NBUCKET; ++b) {
-                    const uint32_t c = B.hist[lane * NBUCKET + b];
-                    B.hist[lane * NBUCKET + b] = acc;
-                    acc += c;
+            for (int b = 0; b < NBUCKET; ++b) cnt[b] = 0u;
+            uint32_t* keep = reinterpret_cast<uint32_t*>(Ff);   // bucket | rank, dead before stage 3
+            if (go) {
+                // each lane buckets its own neuron's events (n is small at steady state)
+                const int a = (int)roff;
+                for (uint32_t i = 0; i < n; ++i) {
+                    double x = (Et[a + i] - t0) * bscale;
+                    x = fmin(fmax(x, 0.0), (double)(NBUCKET - 1));
+                    const int b = (int)x;
+                    uint32_t r = 0;
+#pragma unroll
+                    for (int q = 0; q < NBUCKET; ++q) if (q == b) { r = cnt[q]; cnt[q] = r + 1; }
+                    keep[a + i] = ((uint32_t)b << 16) | r;
                 }
-            }
-            __syncwarp();
-            for (uint32_t e = lane; e < rtot; e += 32) {
-                const uint32_t kp = keep[e];
-                const uint32_t key = kp >> 16;
-                const int o = (int)(key / NBUCKET);
-                const uint32_t pos = B.hist[key] + (kp & 0xffffu);
-                Ep[pos] = (uint16_t)(e - (uint32_t)B.seg[o]);
-                Eo[pos] = (uint8_t)o;                   // owners now in sorted order
-            }
-            __syncwarp();
-            // lane b orders bucket b of every neuron (runs are short)
-            for (int o = 0; o < 32; ++o) {
-                const int a = B.seg[o];
-                if (B.seg[o + 1] == a) continue;
-                const int key = o * NBUCKET + lane;
-                const int r0 = (int)B.hist[key];
-                const int r1 = lane == NBUCKET - 1 ? B.seg[o + 1] : (int)B.hist[key + 1];
-                for (int i = r0 + 1; i < r1; ++i) {
-                    const uint16_t pi = Ep[i];
+                uint32_t acc = 0;
+#pragma unroll
+                for (int b = 0; b < NBUCKET; ++b) { const uint32_t c = cnt[b]; cnt[b] = acc; acc += c; }
+                for (uint32_t i = 0; i < n; ++i) {
+                    const uint32_t kp = keep[a + i];
+                    const int b = (int)(kp >> 16);
+                    uint32_t base = 0;
+#pragma unroll
+                    for (int q = 0; q < NBUCKET; ++q) if (q == b) base = cnt[q];
+                    Ep[a + base + (kp & 0xffffu)] = (uint16_t)i;
+                }
+                // only intra-bucket inversions remain: insertion pass by exact (t, src)
+                for (uint32_t i = 1; i < n; ++i) {
+                    const uint16_t pi = Ep[a + i];
                     const double ti = Et[a + pi];
                     const uint32_t si = Es[a + pi];
-                    int j = i;
-                    while (j > r0) {
-                        const uint16_t pj = Ep[j - 1];
+                    uint32_t j = i;
+                    while (j > 0) {
+                        const uint16_t pj = Ep[a + j - 1];
                         const double tj = Et[a + pj];
                         if (!(ti < tj || (ti == tj && si < Es[a + pj]))) break;
-                        Ep[j] = pj;
+                        Ep[a + j] = pj;
                         --j;
                     }
-                    Ep[j] = pi;
+                    Ep[a + j] = pi;
                 }
+#pragma unroll 4
+                for (uint32_t i = 0; i < n; ++i) Eo[a + i] = (uint8_t)lane;
             }
         }
         __syncwarp();
         // ---- 3 decay factors of every event, assuming the step-start refractory
         //      window ru0 and fatigue flag (exactly the serial update's values)
-        {
+        if (!(sh.debug_skip & 4)) {
             for (uint32_t p = lane; p < rtot; p += 32) {
                 const int o = Eo[p];
                 const int a = B.seg[o];
@@ -446,12 +436,12 @@ k_neuron(const cc_shard sh) {
                 double em, ec, f;
                 decay_factors(Q, te - ff, (fl & 2u) != 0, em, ec, f);
                 Fm[p] = em; Fc[p] = ec; Ff[p] = f;
-                Fd[p] = (ff != last && (fl & 2u)) ? exp(-(ff - last) / Q.tau_c) : 1.0;
             }
         }
         __syncwarp();
         // ---- 4 in-order update per neuron
-        if (go) {
+        if (go && (sh.debug_skip & 8)) pending = false;
+        if (go && !(sh.debug_skip & 8)) {
             const int a = (int)roff;
             bool dirty = false;                   // spiked: factors must be recomputed
             for (uint32_t i = 0; i < n; ++i) {
@@ -460,12 +450,11 @@ k_neuron(const cc_shard sh) {
                 const double ff = fmin(fmax(s.last, s.ru), te);
                 double cs = s.c;
                 double em, ec, f;
+                if (ff != s.last && cs != 0.0)          // leaving a refractory window: rare
+                    cs = cs * exp(-(ff - s.last) / P.tau_c);
                 if (!dirty) {
                     em = Fm[a + i]; ec = Fc[a + i]; f = Ff[a + i];
-                    if (ff != s.last && cs != 0.0) cs = cs * Fd[a + i];
                 } else {
-                    if (ff != s.last && cs != 0.0)
-                        cs = cs * exp(-(ff - s.last) / P.tau_c);
                     decay_factors(P, te - ff, cs != 0.0, em, ec, f);
                 }
                 const double Vs = (s.last < s.ru) ? P.V_r : s.V;
