@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 6
+#define CC_ABI_VERSION 7
 
 /* error bits raised by kernels into cc_ctl.error_bits */
 #define CC_ERR_SPIKE_LOG      0x01u  /* more spikes in one step than log capacity   */
@@ -61,6 +61,9 @@ typedef struct cc_ctl {
     unsigned long long ovf_total;         /* records that went to overflow    */
     unsigned int done_deliver;            /* last-block detection (deliver k.) */
     unsigned int ovf_grouped;             /* records grouped for this step    */
+    unsigned long long stream_used;       /* staged-event slots used this step */
+    unsigned int done_stage;              /* last-block detection (stage k.)  */
+    unsigned int pad1;
 } cc_ctl;
 
 /* One shard's device state.  Layout documented in DESIGN.md section 3. */
@@ -124,6 +127,14 @@ typedef struct cc_shard {
     uint32_t* out_gid;      /* [out_cap] exchange out-list (direct_log == 0)   */
     double* out_t;          /* [out_cap]                                       */
     float* scratch;         /* [scratch_cap][14] spill staging (56 B per event) */
+    double* ev_t;           /* [stream_cap] staged events of this step, sorted, */
+    double* ev_em;          /*   lane-interleaved per warp: event i of lane L  */
+    double* ev_ec;          /*   at ev_base[warp] + 32 * i + L; time, decay    */
+    double* ev_f;           /*   factors em, ec, f and weight (float64)        */
+    double* ev_w;
+    int32_t* ev_n;          /* [n_local] events staged for each neuron          */
+    long long* ev_base;     /* [ceil(n_local / 32)] stream base of each warp    */
+    int64_t stream_cap;
     const int32_t* probe_map; /* [n_local] probe slot or -1                    */
     double* probe_out;      /* [steps][n_probe][5] V c last refr V_end         */
     int64_t probe_steps;    /* rows in probe_out                               */

@@ -16,8 +16,6 @@
 
 namespace {
 
-constexpr int NEURON_BLOCK = 128;       // 4 warps
-constexpr int WARPS_PER_BLOCK = NEURON_BLOCK / 32;
 
 struct Ev {                              // one input event, 16 B
     double t;                            // arrival time, ms
@@ -138,53 +136,46 @@ __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, i
     return ev;
 }
 
-// ------------------------------------------------------------------ k_neuron
-// One warp (= one block) owns 32 consecutive neurons.  Their inputs pass
-// through the warp's shared-memory buffer in rounds, and every stage of a
-// round is spread over the 32 lanes so that a bursty neuron does not
-// serialise the warp:
+// ------------------------------------------------------------------ k_stage
+// Phase A of the neuron step.  One warp owns 32 consecutive neurons; their
+// inputs pass through the warp's shared-memory buffer in rounds and every
+// stage is spread over the 32 lanes:
 //   1 gather   recurrent records (owner-major, 4 loads in flight per lane),
 //              overflow surplus, external Poisson events
-//   2 sort     per neuron, counting sort on a monotone time bucket
-//              b(t) = clamp(floor((t - t0) * NB / dt)), then an insertion
-//              pass that only fixes order inside buckets: exact (t, src) order
-//   3 factors  em = exp(-dt/tau_m), ec, f (model.py:116-143) for every event,
-//              assuming the step-start refractory window and fatigue; these
-//              are exactly the values the serial update computes
-//   4 update   per lane, in event order: the affine update, jump, threshold,
-//              reset; after a spike the neuron's remaining factors are
-//              recomputed in line.
+//   2 sort     per neuron: counting sort on a monotone time bucket
+//              b(t) = clamp(floor((t - t0) * NB / dt)) then an insertion pass
+//              fixing order inside buckets: exact (t, src) order
+//   3 factors  em = exp(-dt/tau_m), ec, f (model.py:116-143) of every event,
+//              assuming the step-start refractory window and fatigue flag
+//              (exactly the values the serial update computes), written with
+//              the event time and float64 weight to a lane-interleaved stream
+//              (event i of lane L at ev_base[warp] + 32 i + L) for k_update.
 constexpr int NEURON_WCAP = 512;           // events per round (16 per lane)
 constexpr int NBUCKET = 8;                 // time buckets per neuron
+constexpr int STAGE_WARPS = 4;
 
-struct WarpBuf {
-    double* t; double* em; double* ec; double* f;
-    uint32_t* src; float* w; uint16_t* perm; uint8_t* own;
-    uint32_t* hist; uint32_t* keep; int* seg;
+struct StageBuf {
+    double* t; uint32_t* src; float* w; uint16_t* perm;
+    uint32_t* keep; uint32_t* tab; int* seg;
     double* o_last; double* o_ru; uint32_t* o_flag;
 };
 
-__host__ __device__ constexpr size_t warp_smem_bytes() {
-    return (size_t)NEURON_WCAP * (8 * 4 + 4 + 4 + 2 + 1) + 64 * 4 + 34 * 4
-           + 32 * (8 + 8 + 4) + 64;
+__host__ __device__ constexpr size_t stage_warp_bytes() {
+    return (size_t)NEURON_WCAP * (8 + 4 + 4 + 4 + 2) + 64 * 4 + 34 * 4 + 32 * (8 + 8 + 4) + 32;
 }
 
-__device__ __forceinline__ WarpBuf carve(char* p) {
-    WarpBuf b;
+__device__ __forceinline__ StageBuf carve(char* p) {
+    StageBuf b;
     b.t = (double*)p; p += NEURON_WCAP * 8;
-    b.em = (double*)p; p += NEURON_WCAP * 8;
-    b.ec = (double*)p; p += NEURON_WCAP * 8;
-    b.f = (double*)p; p += NEURON_WCAP * 8;
     b.o_last = (double*)p; p += 32 * 8;
     b.o_ru = (double*)p; p += 32 * 8;
     b.src = (uint32_t*)p; p += NEURON_WCAP * 4;
     b.w = (float*)p; p += NEURON_WCAP * 4;
-    b.hist = (uint32_t*)p; p += 64 * 4;          // gather prefix tables (64 words)
+    b.keep = (uint32_t*)p; p += NEURON_WCAP * 4;
+    b.tab = (uint32_t*)p; p += 64 * 4;
     b.seg = (int*)p; p += 34 * 4;
     b.o_flag = (uint32_t*)p; p += 32 * 4;
-    b.perm = (uint16_t*)p; p += NEURON_WCAP * 2;
-    b.own = (uint8_t*)p;
-    b.keep = reinterpret_cast<uint32_t*>(b.f);   // sort scratch, dead before factors
+    b.perm = (uint16_t*)p;
     return b;
 }
 
@@ -210,15 +201,20 @@ __device__ __forceinline__ void decay_factors(const cc_pop& P, double dt, bool w
     }
 }
 
-template <bool PROBE>
-__global__ void __launch_bounds__(32)
-k_neuron(const cc_shard sh) {
+__device__ __forceinline__ int neuron_pop(const cc_shard& sh, uint32_t gid) {
+    return ((int)(gid % (uint32_t)sh.n_col) < sh.n_exc_col) ? 0 : 1;
+}
+
+__global__ void __launch_bounds__(32 * STAGE_WARPS)
+k_stage(const cc_shard sh) {
     extern __shared__ __align__(16) char nsm[];
     cc_ctl* ctl = sh.ctl;
     const long long t = *(volatile long long*)&ctl->t;
-    const int lane = threadIdx.x;
-    WarpBuf B = carve(nsm);
-    const int li0 = blockIdx.x * 32;
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    StageBuf B = carve(nsm + wib * stage_warp_bytes());
+    const int warp_id = blockIdx.x * STAGE_WARPS + wib;
+    const int li0 = warp_id * 32;
     const int li = li0 + lane;
     const bool active = li < sh.n_local;
     const int D = sh.d_max;
@@ -232,7 +228,7 @@ k_neuron(const cc_shard sh) {
     int pop = 0;
     if (active) {
         gid = sh.gid[li];
-        pop = ((int)(gid % (uint32_t)sh.n_col) < sh.n_exc_col) ? 0 : 1;
+        pop = neuron_pop(sh, gid);
         const size_t ci = (size_t)slot * sh.n_local + li;
         n_r = sh.bin_cnt[ci];
         if (n_r) sh.bin_cnt[ci] = 0;
@@ -254,20 +250,32 @@ k_neuron(const cc_shard sh) {
     }
     const uint32_t n = n_r + n_e;
     const uint32_t nb = min(n_r, K);
-    NState s{0.0, 0.0, 0.0, 0.0};
-    double* st = sh.state + (size_t)(active ? li : 0) * 4;
-    if (active && (n || PROBE)) {
-        const double2 a = reinterpret_cast<const double2*>(st)[0];
-        const double2 b = reinterpret_cast<const double2*>(st)[1];
-        s = NState{a.x, a.y, b.x, b.y};
+    if (active) {
+        const double2 b = reinterpret_cast<const double2*>(sh.state + (size_t)li * 4)[1];
+        const double c = sh.state[(size_t)li * 4 + 1];
+        B.o_last[lane] = b.x;
+        B.o_ru[lane] = b.y;
+        B.o_flag[lane] = (uint32_t)pop | (c != 0.0 ? 2u : 0u);
     }
-    const cc_pop& P = sh.pop[pop];
-    B.o_last[lane] = s.last;
-    B.o_ru[lane] = s.ru;
-    B.o_flag[lane] = (uint32_t)pop | (s.c != 0.0 ? 2u : 0u);
+    // stream region of this warp: 32 x (max events of its neurons)
+    uint32_t nmax = active ? n : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+    unsigned long long sbase = 0;
+    if (lane == 0 && nmax) {
+        sbase = atomicAdd(&ctl->stream_used, 32ull * nmax);
+        if (sbase + 32ull * nmax > (unsigned long long)sh.stream_cap) {
+            cc_raise(ctl, CC_ERR_SCRATCH, t);
+            nmax = 0;
+        }
+        sh.ev_base[warp_id] = (long long)sbase;
+    }
+    sbase = __shfl_sync(0xffffffffu, sbase, 0);
+    nmax = __shfl_sync(0xffffffffu, nmax, 0);
+    if (nmax == 0 && lane == 0 && li0 < sh.n_local) sh.ev_base[warp_id] = 0;
+    if (active) sh.ev_n[li] = nmax ? (int32_t)n : 0;
     const uint64_t* bins = sh.bin_rec + (size_t)slot * K * sh.n_local + li0;
-    uint32_t my_spikes = 0;
-    bool pending = active && n > 0;
+    bool pending = active && n > 0 && nmax > 0;
     while (__any_sync(0xffffffffu, pending)) {
         // ---- admission: lanes whose inputs fit behind the earlier ones
         uint32_t tot;
@@ -284,8 +292,7 @@ k_neuron(const cc_shard sh) {
         B.seg[lane] = (int)roff;
         if (lane == 31) B.seg[32] = (int)rtot;
         double* Et = B.t; uint32_t* Es = B.src; float* Ew = B.w; uint16_t* Ep = B.perm;
-        double* Fm = B.em; double* Fc = B.ec; double* Ff = B.f;
-        uint8_t* Eo = B.own;
+        uint32_t* Ek = B.keep;
         if (__any_sync(0xffffffffu, big)) {
             const int bl = __ffs(__ballot_sync(0xffffffffu, big)) - 1;
             unsigned long long at = 0;
@@ -299,14 +306,14 @@ k_neuron(const cc_shard sh) {
             }
             ok = __shfl_sync(0xffffffffu, ok, bl);
             at = __shfl_sync(0xffffffffu, at, bl);
-            // spill layout: 6 words of 8 B per event
-            double* base = reinterpret_cast<double*>(sh.scratch) + at * 6;
+            // spill layout: 3 words of 8 B per event (t, src|w, keep|perm)
+            double* base = reinterpret_cast<double*>(sh.scratch) + at * 3;
             const uint32_t cap = rtot;
-            Et = base; Fm = base + cap; Fc = base + 2 * cap; Ff = base + 3 * cap;
-            Es = reinterpret_cast<uint32_t*>(base + 4 * cap);
+            Et = base;
+            Es = reinterpret_cast<uint32_t*>(base + cap);
             Ew = reinterpret_cast<float*>(Es + cap);
-            Ep = reinterpret_cast<uint16_t*>(base + 5 * cap);
-            Eo = reinterpret_cast<uint8_t*>(Ep + cap);
+            Ek = reinterpret_cast<uint32_t*>(base + 2 * cap);
+            Ep = reinterpret_cast<uint16_t*>(Ek + cap);
             if (!ok) { pending = false; go = false; B.seg[lane] = 0; if (lane == 31) B.seg[32] = 0; rtot = 0; }
         }
         __syncwarp();
@@ -315,12 +322,12 @@ k_neuron(const cc_shard sh) {
             const uint32_t nbr = go ? nb : 0u;
             uint32_t R;
             const uint32_t pr = warp_excl_scan(nbr, R);
-            B.hist[lane] = pr + nbr;                  // record ends (hist is reset below)
-            B.hist[32 + lane] = pr;                   // record starts
+            B.tab[lane] = pr + nbr;                   // record ends
+            B.tab[32 + lane] = pr;                    // record starts
             __syncwarp();
             for (uint32_t r0 = 0; r0 < R; r0 += 128) {
                 uint64_t rec[4];
-                int dst[4], own[4];
+                int dst[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t r = r0 + u * 32 + lane;
@@ -329,12 +336,11 @@ k_neuron(const cc_shard sh) {
                         int lo = 0, hi = 31;              // first lane whose records end after r
                         while (lo < hi) {
                             const int mid = (lo + hi) >> 1;
-                            if (B.hist[mid] > r) hi = mid; else lo = mid + 1;
+                            if (B.tab[mid] > r) hi = mid; else lo = mid + 1;
                         }
-                        const uint32_t k = r - B.hist[32 + lo];
+                        const uint32_t k = r - B.tab[32 + lo];
                         rec[u] = bins[(size_t)k * sh.n_local + lo];
                         dst[u] = B.seg[lo] + (int)k;
-                        own[u] = lo;
                     }
                 }
 #pragma unroll
@@ -342,7 +348,6 @@ k_neuron(const cc_shard sh) {
                     if (dst[u] >= 0) {
                         const Ev ev = make_rec_event(sh, rec[u], t_mod_l);
                         Et[dst[u]] = ev.t; Es[dst[u]] = ev.src; Ew[dst[u]] = ev.w;
-                        Eo[dst[u]] = (uint8_t)own[u];
                     }
                 }
             }
@@ -357,7 +362,6 @@ k_neuron(const cc_shard sh) {
                     const uint4 r = ov[k];
                     const Ev ev = make_rec_event(sh, (uint64_t)r.y | ((uint64_t)r.z << 32), t_mod_l);
                     Et[b0 + nb + k] = ev.t; Es[b0 + nb + k] = ev.src; Ew[b0 + nb + k] = ev.w;
-                    Eo[b0 + nb + k] = (uint8_t)lane;
                 }
             }
             if (n_e) {
@@ -368,173 +372,223 @@ k_neuron(const cc_shard sh) {
                     Et[b0 + n_r + k] = ((double)t + cc_u53(cc_splitmix64(h4 ^ (uint64_t)k))) * sh.dt;
                     Es[b0 + n_r + k] = CC_EXT_SRC;
                     Ew[b0 + n_r + k] = 0.0f;
-                    Eo[b0 + n_r + k] = (uint8_t)lane;
                 }
-            }
-        }
-        // ---- 2 counting sort on a monotone time bucket, per-lane exact fix-up
-        if (!(sh.debug_skip & 2)) {
-            uint32_t cnt[NBUCKET];
-#pragma unroll
-            for (int b = 0; b < NBUCKET; ++b) cnt[b] = 0u;
-            uint32_t* keep = reinterpret_cast<uint32_t*>(Ff);   // bucket | rank, dead before stage 3
-            if (go) {
-                // each lane buckets its own neuron's events (n is small at steady state)
-                const int a = (int)roff;
-                for (uint32_t i = 0; i < n; ++i) {
-                    double x = (Et[a + i] - t0) * bscale;
-                    x = fmin(fmax(x, 0.0), (double)(NBUCKET - 1));
-                    const int b = (int)x;
-                    uint32_t r = 0;
-#pragma unroll
-                    for (int q = 0; q < NBUCKET; ++q) if (q == b) { r = cnt[q]; cnt[q] = r + 1; }
-                    keep[a + i] = ((uint32_t)b << 16) | r;
-                }
-                uint32_t acc = 0;
-#pragma unroll
-                for (int b = 0; b < NBUCKET; ++b) { const uint32_t c = cnt[b]; cnt[b] = acc; acc += c; }
-                for (uint32_t i = 0; i < n; ++i) {
-                    const uint32_t kp = keep[a + i];
-                    const int b = (int)(kp >> 16);
-                    uint32_t base = 0;
-#pragma unroll
-                    for (int q = 0; q < NBUCKET; ++q) if (q == b) base = cnt[q];
-                    Ep[a + base + (kp & 0xffffu)] = (uint16_t)i;
-                }
-                // only intra-bucket inversions remain: insertion pass by exact (t, src)
-                for (uint32_t i = 1; i < n; ++i) {
-                    const uint16_t pi = Ep[a + i];
-                    const double ti = Et[a + pi];
-                    const uint32_t si = Es[a + pi];
-                    uint32_t j = i;
-                    while (j > 0) {
-                        const uint16_t pj = Ep[a + j - 1];
-                        const double tj = Et[a + pj];
-                        if (!(ti < tj || (ti == tj && si < Es[a + pj]))) break;
-                        Ep[a + j] = pj;
-                        --j;
-                    }
-                    Ep[a + j] = pi;
-                }
-#pragma unroll 4
-                for (uint32_t i = 0; i < n; ++i) Eo[a + i] = (uint8_t)lane;
             }
         }
         __syncwarp();
-        // ---- 3 decay factors of every event, assuming the step-start refractory
-        //      window ru0 and fatigue flag (exactly the serial update's values)
+        // ---- 2 counting sort on a monotone time bucket, per-lane exact fix-up
+        if (go && !(sh.debug_skip & 2)) {
+            uint32_t cnt[NBUCKET];
+#pragma unroll
+            for (int b = 0; b < NBUCKET; ++b) cnt[b] = 0u;
+            const int a = (int)roff;
+            for (uint32_t i = 0; i < n; ++i) {
+                double x = (Et[a + i] - t0) * bscale;
+                x = fmin(fmax(x, 0.0), (double)(NBUCKET - 1));
+                const int b = (int)x;
+                uint32_t r = 0;
+#pragma unroll
+                for (int q = 0; q < NBUCKET; ++q) if (q == b) { r = cnt[q]; cnt[q] = r + 1; }
+                Ek[a + i] = ((uint32_t)b << 16) | r;
+            }
+            uint32_t acc = 0;
+#pragma unroll
+            for (int b = 0; b < NBUCKET; ++b) { const uint32_t c = cnt[b]; cnt[b] = acc; acc += c; }
+            for (uint32_t i = 0; i < n; ++i) {
+                const uint32_t kp = Ek[a + i];
+                const int b = (int)(kp >> 16);
+                uint32_t base = 0;
+#pragma unroll
+                for (int q = 0; q < NBUCKET; ++q) if (q == b) base = cnt[q];
+                Ep[a + base + (kp & 0xffffu)] = (uint16_t)i;
+            }
+            // only intra-bucket inversions remain: insertion pass by exact (t, src)
+            for (uint32_t i = 1; i < n; ++i) {
+                const uint16_t pi = Ep[a + i];
+                const double ti = Et[a + pi];
+                const uint32_t si = Es[a + pi];
+                uint32_t j = i;
+                while (j > 0) {
+                    const uint16_t pj = Ep[a + j - 1];
+                    const double tj = Et[a + pj];
+                    if (!(ti < tj || (ti == tj && si < Es[a + pj]))) break;
+                    Ep[a + j] = pj;
+                    --j;
+                }
+                Ep[a + j] = pi;
+            }
+#pragma unroll 4
+            for (uint32_t i = 0; i < n; ++i) Ek[a + i] = (uint32_t)lane;   // owner per sorted slot
+        }
+        __syncwarp();
+        // ---- 3 decay factors of every event -> lane-interleaved stream
         if (!(sh.debug_skip & 4)) {
             for (uint32_t p = lane; p < rtot; p += 32) {
-                const int o = Eo[p];
+                const int o = (int)Ek[p];
                 const int a = B.seg[o];
-                const double te = Et[a + Ep[p]];
-                const double last = (int)p == a ? B.o_last[o] : Et[a + Ep[p - 1]];
+                const uint32_t i = p - (uint32_t)a;           // rank within the neuron
+                const int e = a + Ep[p];
+                const double te = Et[e];
+                const double last = i == 0 ? B.o_last[o] : Et[a + Ep[p - 1]];
                 const double ru = B.o_ru[o];
                 const uint32_t fl = B.o_flag[o];
                 const cc_pop& Q = sh.pop[fl & 1u];
                 const double ff = fmin(fmax(last, ru), te);
                 double em, ec, f;
                 decay_factors(Q, te - ff, (fl & 2u) != 0, em, ec, f);
-                Fm[p] = em; Fc[p] = ec; Ff[p] = f;
+                const size_t q = sbase + 32ull * i + (uint32_t)o;
+                sh.ev_t[q] = te;
+                sh.ev_em[q] = em;
+                sh.ev_ec[q] = ec;
+                sh.ev_f[q] = f;
+                sh.ev_w[q] = (Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
             }
         }
-        __syncwarp();
-        // ---- 4 in-order update per neuron
-        if (go && (sh.debug_skip & 8)) pending = false;
-        if (go && !(sh.debug_skip & 8)) {
-            const int a = (int)roff;
-            bool dirty = false;                   // spiked: factors must be recomputed
-            for (uint32_t i = 0; i < n; ++i) {
-                const int e = a + Ep[a + i];
-                const double te = Et[e];
-                const double ff = fmin(fmax(s.last, s.ru), te);
-                double cs = s.c;
-                double em, ec, f;
-                if (ff != s.last && cs != 0.0)          // leaving a refractory window: rare
-                    cs = cs * exp(-(ff - s.last) / P.tau_c);
-                if (!dirty) {
-                    em = Fm[a + i]; ec = Fc[a + i]; f = Ff[a + i];
-                } else {
-                    decay_factors(P, te - ff, cs != 0.0, em, ec, f);
-                }
-                const double Vs = (s.last < s.ru) ? P.V_r : s.V;
-                double Vt = P.E + (Vs - P.E) * em;
-                double ct = cs;
-                if (cs != 0.0) {
-                    Vt = Vt - P.sfa * cs * f;
-                    ct = cs * ec;
-                }
-                s.V = (te < s.ru) ? P.V_r : Vt;
-                s.c = ct;
-                s.last = te;
-                if (te >= s.ru) {
-                    const uint32_t src = Es[e];
-                    const double w = (src == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
-                    const double V = s.V + w;
-                    if (V > P.V_theta) {                 // strict threshold
-                        s.V = P.V_r;
-                        s.c = s.c + P.alpha_c;
-                        s.ru = te + P.tau_arp;
-                        dirty = true;
-                        ++my_spikes;
-                        if (sh.direct_log) {
-                            log_spike(sh, t, gid, te);
-                        } else {
-                            const unsigned o = atomicAdd(&ctl->out_n, 1u);
-                            if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = te; }
-                            else cc_raise(ctl, CC_ERR_OUTLIST, t);
-                        }
-                        const unsigned long long r = atomicAdd(&ctl->raster_n, 1ull);
-                        if (r < (unsigned long long)sh.raster_cap) {
-                            sh.raster_gid[r] = gid;
-                            sh.raster_t[r] = te;
-                        } else {
-                            cc_raise(ctl, CC_ERR_RASTER, t);
-                        }
-                    } else {
-                        s.V = V;
-                    }
-                } else {
-                    s.V = P.V_r;                         // refractory: input discarded
-                }
-            }
-            reinterpret_cast<double2*>(st)[0] = make_double2(s.V, s.c);
-            reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
-            pending = false;
-        }
+        pending = pending && !go;
         __syncwarp();
     }
-    if (PROBE && active) {
-        const int ps = sh.probe_map[li];
-        if (ps >= 0 && t < sh.probe_steps) {
-            double* o = sh.probe_out + ((size_t)t * sh.n_probe + ps) * 5;
-            o[0] = s.V; o[1] = s.c; o[2] = s.last; o[3] = s.ru;
-            NState q = s;
-            advance(q, P, (double)(t + 1) * sh.dt);
-            o[4] = q.V;
-        }
-    }
-    // counters: one atomic per warp
-    unsigned long long e_sum = n_e, s_sum = my_spikes;
+    // external-event counter: one atomic per warp
+    unsigned long long e_sum = n_e;
     uint32_t mx_b = n_r, mx_e = n;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         e_sum += __shfl_xor_sync(0xffffffffu, e_sum, o);
-        s_sum += __shfl_xor_sync(0xffffffffu, s_sum, o);
         mx_b = max(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, o));
         mx_e = max(mx_e, __shfl_xor_sync(0xffffffffu, mx_e, o));
     }
+    __shared__ unsigned long long blk_e;
+    __shared__ unsigned blk_b, blk_m;
+    if (threadIdx.x == 0) { blk_e = 0; blk_b = 0; blk_m = 0; }
+    __syncthreads();
     if (lane == 0) {
-        if (e_sum) atomicAdd(&ctl->ext_events, e_sum);
-        if (s_sum) atomicAdd(&ctl->n_spikes, s_sum);
-        if (mx_b > 0) atomicMax(&ctl->max_bin, mx_b);
-        if (mx_e > 0) atomicMax(&ctl->max_events, mx_e);
-        // last block out advances the step counter and retires the slot
+        atomicAdd(&blk_e, e_sum);
+        atomicMax(&blk_b, mx_b);
+        atomicMax(&blk_m, mx_e);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (blk_e) atomicAdd(&ctl->ext_events, blk_e);
+        if (blk_b) atomicMax(&ctl->max_bin, blk_b);
+        if (blk_m) atomicMax(&ctl->max_events, blk_m);
+        // last block out retires the ring slot's overflow list
         __threadfence();
-        const unsigned prev = atomicAdd(&ctl->done_blocks, 1u);
-        if (prev == gridDim.x - 1) {
-            ctl->done_blocks = 0;
+        if (atomicAdd(&ctl->done_stage, 1u) == gridDim.x - 1) {
+            ctl->done_stage = 0;
             sh.ovf_cnt[slot] = 0;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ k_update
+// Phase B: one thread per neuron walks its staged events in order (coalesced:
+// lane L reads slot 32 i + L) and applies the closed-form update, jump,
+// strict threshold, reset and refractory rule of NeuronBlock.integrate_sorted
+// (model.py:289-337).  After a spike the remaining factors of that neuron are
+// recomputed in line (the staged ones assumed the old refractory window).
+template <bool PROBE>
+__global__ void __launch_bounds__(128)
+k_update(const cc_shard sh) {
+    cc_ctl* ctl = sh.ctl;
+    const long long t = *(volatile long long*)&ctl->t;
+    const int li = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool active = li < sh.n_local;
+    uint32_t my_spikes = 0;
+    if (active && !(sh.debug_skip & 8)) {
+        const uint32_t n = (uint32_t)sh.ev_n[li];
+        if (n || PROBE) {
+            const uint32_t gid = sh.gid[li];
+            const cc_pop& P = sh.pop[neuron_pop(sh, gid)];
+            double* st = sh.state + (size_t)li * 4;
+            const double2 a0 = reinterpret_cast<const double2*>(st)[0];
+            const double2 b0 = reinterpret_cast<const double2*>(st)[1];
+            NState s{a0.x, a0.y, b0.x, b0.y};
+            if (n) {
+                const size_t base = (size_t)sh.ev_base[li >> 5] + lane;
+                bool dirty = false;
+                double te_n = sh.ev_t[base], em_n = sh.ev_em[base], ec_n = sh.ev_ec[base];
+                double f_n = sh.ev_f[base], w_n = sh.ev_w[base];
+                for (uint32_t i = 0; i < n; ++i) {
+                    const double te = te_n, w = w_n;
+                    double em = em_n, ec = ec_n, f = f_n;
+                    if (i + 1 < n) {                       // prefetch the next event
+                        const size_t q = base + 32ull * (i + 1);
+                        te_n = sh.ev_t[q]; em_n = sh.ev_em[q]; ec_n = sh.ev_ec[q];
+                        f_n = sh.ev_f[q]; w_n = sh.ev_w[q];
+                    }
+                    const double ff = fmin(fmax(s.last, s.ru), te);
+                    double cs = s.c;
+                    if (ff != s.last && cs != 0.0)        // leaving a refractory window: rare
+                        cs = cs * exp(-(ff - s.last) / P.tau_c);
+                    if (dirty) decay_factors(P, te - ff, cs != 0.0, em, ec, f);
+                    const double Vs = (s.last < s.ru) ? P.V_r : s.V;
+                    double Vt = P.E + (Vs - P.E) * em;
+                    double ct = cs;
+                    if (cs != 0.0) {
+                        Vt = Vt - P.sfa * cs * f;
+                        ct = cs * ec;
+                    }
+                    s.V = (te < s.ru) ? P.V_r : Vt;
+                    s.c = ct;
+                    s.last = te;
+                    if (te >= s.ru) {
+                        const double V = s.V + w;
+                        if (V > P.V_theta) {                 // strict threshold
+                            s.V = P.V_r;
+                            s.c = s.c + P.alpha_c;
+                            s.ru = te + P.tau_arp;
+                            dirty = true;
+                            ++my_spikes;
+                            if (sh.direct_log) {
+                                log_spike(sh, t, gid, te);
+                            } else {
+                                const unsigned o = atomicAdd(&ctl->out_n, 1u);
+                                if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = te; }
+                                else cc_raise(ctl, CC_ERR_OUTLIST, t);
+                            }
+                            const unsigned long long r = atomicAdd(&ctl->raster_n, 1ull);
+                            if (r < (unsigned long long)sh.raster_cap) {
+                                sh.raster_gid[r] = gid;
+                                sh.raster_t[r] = te;
+                            } else {
+                                cc_raise(ctl, CC_ERR_RASTER, t);
+                            }
+                        } else {
+                            s.V = V;
+                        }
+                    } else {
+                        s.V = P.V_r;                         // refractory: input discarded
+                    }
+                }
+                reinterpret_cast<double2*>(st)[0] = make_double2(s.V, s.c);
+                reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
+            }
+            if (PROBE) {
+                const int ps = sh.probe_map[li];
+                if (ps >= 0 && t < sh.probe_steps) {
+                    double* o = sh.probe_out + ((size_t)t * sh.n_probe + ps) * 5;
+                    o[0] = s.V; o[1] = s.c; o[2] = s.last; o[3] = s.ru;
+                    NState q = s;
+                    advance(q, P, (double)(t + 1) * sh.dt);
+                    o[4] = q.V;
+                }
+            }
+        }
+    }
+    unsigned s_sum = my_spikes;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s_sum += __shfl_xor_sync(0xffffffffu, s_sum, o);
+    __shared__ unsigned blk_s;
+    if (threadIdx.x == 0) blk_s = 0;
+    __syncthreads();
+    if (lane == 0 && s_sum) atomicAdd(&blk_s, s_sum);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (blk_s) atomicAdd(&ctl->n_spikes, (unsigned long long)blk_s);
+        // last block out advances the step counter
+        __threadfence();
+        if (atomicAdd(&ctl->done_blocks, 1u) == gridDim.x - 1) {
+            ctl->done_blocks = 0;
             __threadfence();
             *(volatile long long*)&ctl->t = t + 1;
         }
@@ -599,6 +653,7 @@ k_deliver(const cc_shard sh) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         sh.log_ctr[pos_mod(t, sh.log_slots)] = 0ull;   // the slot k_neuron(t) fills
         ctl->scratch_used = 0ull;
+        ctl->stream_used = 0ull;
     }
     const int ep = (int)pos_mod(t - 1, sh.log_slots);
     const unsigned long long n_pieces = sh.log_ctr[ep] >> 32;
@@ -756,19 +811,22 @@ extern "C" int cc_deliver(const cc_shard* sh, void* stream) {
 extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_neuron_step: null shard");
     if (sh->n_local <= 0) return cc_set_error("cc_neuron_step: empty shard");
-    const int blocks = (sh->n_local + 31) / 32;
-    const size_t smem = warp_smem_bytes();
+    const int warps = (sh->n_local + 31) / 32;
+    const int sblocks = (warps + STAGE_WARPS - 1) / STAGE_WARPS;
+    const size_t smem = stage_warp_bytes() * STAGE_WARPS;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_neuron<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_neuron<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
+    k_stage<<<sblocks, 32 * STAGE_WARPS, smem, (cudaStream_t)stream>>>(*sh);
+    if (const int rc = cc_check_launch("k_stage")) return rc;
+    const int ublocks = (sh->n_local + 127) / 128;
     if (sh->n_probe > 0)
-        k_neuron<true><<<blocks, 32, smem, (cudaStream_t)stream>>>(*sh);
+        k_update<true><<<ublocks, 128, 0, (cudaStream_t)stream>>>(*sh);
     else
-        k_neuron<false><<<blocks, 32, smem, (cudaStream_t)stream>>>(*sh);
-    return cc_check_launch("k_neuron");
+        k_update<false><<<ublocks, 128, 0, (cudaStream_t)stream>>>(*sh);
+    return cc_check_launch("k_update");
 }
 
 extern "C" int cc_ingest(const cc_shard* sh, const uint32_t* in_gid, const double* in_t,
