@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 7
+#define CC_ABI_VERSION 8
 
 /* error bits raised by kernels into cc_ctl.error_bits */
 #define CC_ERR_SPIKE_LOG      0x01u  /* more spikes in one step than log capacity   */
@@ -63,6 +63,8 @@ typedef struct cc_ctl {
     unsigned int ovf_grouped;             /* records grouped for this step    */
     unsigned long long stream_used;       /* staged-event slots used this step */
     unsigned int done_stage;              /* last-block detection (stage k.)  */
+    unsigned int n_rounds;                /* staging work items planned this step */
+    unsigned int round_next;              /* next work item to claim          */
     unsigned int pad1;
 } cc_ctl;
 
@@ -133,6 +135,9 @@ typedef struct cc_shard {
     double* ev_f;           /*   factors em, ec, f and weight (float64)        */
     double* ev_w;
     int32_t* ev_n;          /* [n_local] events staged for each neuron          */
+    int32_t* ev_nr;         /* [n_local] of which recurrent                     */
+    uint32_t* rounds;       /* [round_cap][2] work items: {group, l0 | l1 << 8}   */
+    int64_t round_cap;
     long long* ev_base;     /* [ceil(n_local / 32)] stream base of each warp    */
     int64_t stream_cap;
     const int32_t* probe_map; /* [n_local] probe slot or -1                    */

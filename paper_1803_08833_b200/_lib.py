@@ -14,7 +14,7 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BIT
            "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 ERR_BITS = {
     0x01: "spike log full (more spikes in one step than planned)",
@@ -45,7 +45,8 @@ class Ctl(C.Structure):
         ("max_bin", C.c_uint), ("max_events", C.c_uint), ("scratch_used", C.c_ulonglong),
         ("out_n", C.c_uint), ("pad0", C.c_uint), ("spilled_total", C.c_ulonglong),
         ("ovf_total", C.c_ulonglong), ("done_deliver", C.c_uint), ("ovf_grouped", C.c_uint),
-        ("stream_used", C.c_ulonglong), ("done_stage", C.c_uint), ("pad1", C.c_uint),
+        ("stream_used", C.c_ulonglong), ("done_stage", C.c_uint), ("n_rounds", C.c_uint),
+        ("round_next", C.c_uint), ("pad1", C.c_uint),
     ]
 
 
@@ -71,7 +72,8 @@ class Shard(C.Structure):
         ("log_t", _P), ("log_gid", _P), ("log_ctr", _P), ("pieces", _P),
         ("raster_gid", _P), ("raster_t", _P), ("out_gid", _P), ("out_t", _P),
         ("scratch", _P), ("ev_t", _P), ("ev_em", _P), ("ev_ec", _P), ("ev_f", _P),
-        ("ev_w", _P), ("ev_n", _P), ("ev_base", _P), ("stream_cap", C.c_int64),
+        ("ev_w", _P), ("ev_n", _P), ("ev_nr", _P), ("rounds", _P), ("round_cap", C.c_int64),
+        ("ev_base", _P), ("stream_cap", C.c_int64),
         ("probe_map", _P), ("probe_out", _P),
         ("probe_steps", C.c_int64), ("ctl", _P),
     ]

@@ -150,18 +150,19 @@ __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, i
 //              (exactly the values the serial update computes), written with
 //              the event time and float64 weight to a lane-interleaved stream
 //              (event i of lane L at ev_base[warp] + 32 i + L) for k_update.
-constexpr int NEURON_WCAP = 512;           // events per round (16 per lane)
+constexpr int NEURON_WCAP = 384;           // events per round (12 per lane)
 constexpr int NBUCKET = 8;                 // time buckets per neuron
-constexpr int STAGE_WARPS = 4;
+constexpr int STAGE_WARPS = 2;
 
 struct StageBuf {
-    double* t; uint32_t* src; float* w; uint16_t* perm;
-    uint32_t* keep; uint32_t* tab; int* seg;
+    double* t; uint32_t* src; float* w; uint16_t* perm; uint8_t* own;
+    uint32_t* keep; uint32_t* tab; uint32_t* hist; int* seg;
     double* o_last; double* o_ru; uint32_t* o_flag;
 };
 
 __host__ __device__ constexpr size_t stage_warp_bytes() {
-    return (size_t)NEURON_WCAP * (8 + 4 + 4 + 4 + 2) + 64 * 4 + 34 * 4 + 32 * (8 + 8 + 4) + 32;
+    return (size_t)NEURON_WCAP * (8 + 4 + 4 + 4 + 2 + 1) + 64 * 4 + 32 * NBUCKET * 4 + 34 * 4
+           + 32 * (8 + 8 + 4) + 32;
 }
 
 __device__ __forceinline__ StageBuf carve(char* p) {
@@ -173,9 +174,11 @@ __device__ __forceinline__ StageBuf carve(char* p) {
     b.w = (float*)p; p += NEURON_WCAP * 4;
     b.keep = (uint32_t*)p; p += NEURON_WCAP * 4;
     b.tab = (uint32_t*)p; p += 64 * 4;
+    b.hist = (uint32_t*)p; p += 32 * NBUCKET * 4;
     b.seg = (int*)p; p += 34 * 4;
     b.o_flag = (uint32_t*)p; p += 32 * 4;
-    b.perm = (uint16_t*)p;
+    b.perm = (uint16_t*)p; p += NEURON_WCAP * 2;
+    b.own = (uint8_t*)p;
     return b;
 }
 
@@ -201,37 +204,34 @@ __device__ __forceinline__ void decay_factors(const cc_pop& P, double dt, bool w
     }
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    return v;
+}
+
 __device__ __forceinline__ int neuron_pop(const cc_shard& sh, uint32_t gid) {
     return ((int)(gid % (uint32_t)sh.n_col) < sh.n_exc_col) ? 0 : 1;
 }
 
-__global__ void __launch_bounds__(32 * STAGE_WARPS)
-k_stage(const cc_shard sh) {
-    extern __shared__ __align__(16) char nsm[];
+// Planning pass of phase A: per group of 32 neurons, the input counts
+// (ring-slot occupancy and the Poisson draw), the group's stream region and
+// its split into work items ("rounds") of at most NEURON_WCAP inputs, appended
+// to a global queue so that heavy groups are spread over many warps.
+__global__ void __launch_bounds__(128)
+k_plan(const cc_shard sh) {
     cc_ctl* ctl = sh.ctl;
     const long long t = *(volatile long long*)&ctl->t;
     const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    StageBuf B = carve(nsm + wib * stage_warp_bytes());
-    const int warp_id = blockIdx.x * STAGE_WARPS + wib;
-    const int li0 = warp_id * 32;
-    const int li = li0 + lane;
+    const int group = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int li = group * 32 + lane;
+    if (group * 32 >= sh.n_local) return;
     const bool active = li < sh.n_local;
-    const int D = sh.d_max;
-    const int slot = (int)pos_mod(t, D);
-    const int t_mod_l = (int)pos_mod(t, sh.log_slots);
-    const uint32_t K = (uint32_t)sh.bin_cap;
-    const double t0 = (double)t * sh.dt;
-    const double bscale = (double)NBUCKET / sh.dt;
-
-    uint32_t gid = 0, n_r = 0, n_e = 0;
-    int pop = 0;
+    const int slot = (int)pos_mod(t, sh.d_max);
+    uint32_t n_r = 0, n_e = 0;
     if (active) {
-        gid = sh.gid[li];
-        pop = neuron_pop(sh, gid);
-        const size_t ci = (size_t)slot * sh.n_local + li;
-        n_r = sh.bin_cnt[ci];
-        if (n_r) sh.bin_cnt[ci] = 0;
+        const uint32_t gid = sh.gid[li];
+        n_r = sh.bin_cnt[(size_t)slot * sh.n_local + li];
         if (sh.ext_budget > 0) {
             // Poisson count by product of uniforms (engine.py:172-188): the
             // prefix product never increases, so stopping at the first
@@ -249,64 +249,135 @@ k_stage(const cc_shard sh) {
         }
     }
     const uint32_t n = n_r + n_e;
-    const uint32_t nb = min(n_r, K);
-    if (active) {
-        const double2 b = reinterpret_cast<const double2*>(sh.state + (size_t)li * 4)[1];
-        const double c = sh.state[(size_t)li * 4 + 1];
-        B.o_last[lane] = b.x;
-        B.o_ru[lane] = b.y;
-        B.o_flag[lane] = (uint32_t)pop | (c != 0.0 ? 2u : 0u);
-    }
-    // stream region of this warp: 32 x (max events of its neurons)
-    uint32_t nmax = active ? n : 0u;
+    uint32_t nmax = n;
+    unsigned long long es = n_e;
+    uint32_t mb = n_r;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+    for (int o = 16; o > 0; o >>= 1) {
+        nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+        mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+        es += __shfl_xor_sync(0xffffffffu, es, o);
+    }
     unsigned long long sbase = 0;
+    int ok = 1;
     if (lane == 0 && nmax) {
         sbase = atomicAdd(&ctl->stream_used, 32ull * nmax);
         if (sbase + 32ull * nmax > (unsigned long long)sh.stream_cap) {
             cc_raise(ctl, CC_ERR_SCRATCH, t);
-            nmax = 0;
+            ok = 0;
         }
-        sh.ev_base[warp_id] = (long long)sbase;
     }
-    sbase = __shfl_sync(0xffffffffu, sbase, 0);
-    nmax = __shfl_sync(0xffffffffu, nmax, 0);
-    if (nmax == 0 && lane == 0 && li0 < sh.n_local) sh.ev_base[warp_id] = 0;
-    if (active) sh.ev_n[li] = nmax ? (int32_t)n : 0;
-    const uint64_t* bins = sh.bin_rec + (size_t)slot * K * sh.n_local + li0;
-    bool pending = active && n > 0 && nmax > 0;
-    while (__any_sync(0xffffffffu, pending)) {
-        // ---- admission: lanes whose inputs fit behind the earlier ones
-        uint32_t tot;
-        const uint32_t off = warp_excl_scan(pending ? n : 0u, tot);
-        bool go = pending && (off + n <= (uint32_t)NEURON_WCAP);
-        bool big = false;                       // a single neuron larger than the buffer
-        if (!__any_sync(0xffffffffu, go)) {
-            const unsigned pm = __ballot_sync(0xffffffffu, pending);
-            big = lane == __ffs(pm) - 1;
-            go = big;
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    if (lane == 0) sh.ev_base[group] = (long long)sbase;
+    if (active) {
+        sh.ev_n[li] = ok ? (int32_t)n : 0;
+        sh.ev_nr[li] = (int32_t)n_r;
+    }
+    // greedy split of lanes 0..31 into rounds of <= NEURON_WCAP inputs; lane 0
+    // walks the 32 counts (cheap, through shared memory)
+    const unsigned has = __ballot_sync(0xffffffffu, ok && n > 0);
+    __shared__ uint32_t cnts[4][32];
+    const int wib = threadIdx.x >> 5;
+    cnts[wib][lane] = (ok && active) ? n : 0u;
+    __syncwarp();
+    if (lane == 0 && has) {
+        uint32_t items[64];
+        int ni = 0;
+        int l0 = -1;
+        uint32_t tot = 0;
+        for (int l = 0; l < 32; ++l) {
+            const uint32_t nl = cnts[wib][l];
+            if (nl == 0) continue;
+            if (l0 >= 0 && tot + nl > (uint32_t)NEURON_WCAP) {
+                items[ni++] = (uint32_t)l0 | ((uint32_t)l << 8);
+                l0 = -1;
+                tot = 0;
+            }
+            if (l0 < 0) { l0 = l; tot = 0; }
+            tot += nl;
         }
+        if (l0 >= 0) items[ni++] = (uint32_t)l0 | (32u << 8);
+        const unsigned at = atomicAdd(&ctl->n_rounds, (unsigned)ni);
+        if (at + ni > (unsigned)sh.round_cap) {
+            cc_raise(ctl, CC_ERR_SCRATCH, t);
+        } else {
+            for (int k = 0; k < ni; ++k) {
+                sh.rounds[2 * (size_t)(at + k)] = (uint32_t)group;
+                sh.rounds[2 * (size_t)(at + k) + 1] = items[k];
+            }
+        }
+    }
+    if (lane == 0) {
+        if (es) atomicAdd(&ctl->ext_events, es);
+        if (mb) atomicMax(&ctl->max_bin, mb);
+        if (nmax) atomicMax(&ctl->max_events, nmax);
+    }
+}
+
+// Phase A proper: persistent warps claim work items from the queue.
+__global__ void __launch_bounds__(32 * STAGE_WARPS)
+k_stage(const cc_shard sh) {
+    extern __shared__ __align__(16) char nsm[];
+    cc_ctl* ctl = sh.ctl;
+    const long long t = *(volatile long long*)&ctl->t;
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    StageBuf B = carve(nsm + wib * stage_warp_bytes());
+    const int D = sh.d_max;
+    const int slot = (int)pos_mod(t, D);
+    const int t_mod_l = (int)pos_mod(t, sh.log_slots);
+    const uint32_t K = (uint32_t)sh.bin_cap;
+    const double t0 = (double)t * sh.dt;
+    const double bscale = (double)NBUCKET / sh.dt;
+    const unsigned n_items = *(volatile unsigned*)&ctl->n_rounds;
+    for (;;) {
+        unsigned item = 0;
+        if (lane == 0) item = atomicAdd(&ctl->round_next, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= n_items || item >= (unsigned)sh.round_cap) break;
+        const int group = (int)sh.rounds[2 * (size_t)item];
+        const uint32_t lr = sh.rounds[2 * (size_t)item + 1];
+        const int l0 = (int)(lr & 0xff), l1 = (int)(lr >> 8);
+        const int li0 = group * 32;
+        const int li = li0 + lane;
+        const bool in = lane >= l0 && lane < l1 && li < sh.n_local;
+        uint32_t n = 0, n_r = 0, gid = 0;
+        if (in) {
+            n = (uint32_t)sh.ev_n[li];
+            n_r = (uint32_t)sh.ev_nr[li];
+            gid = sh.gid[li];
+            const double2 b = reinterpret_cast<const double2*>(sh.state + (size_t)li * 4)[1];
+            const double c = sh.state[(size_t)li * 4 + 1];
+            B.o_last[lane] = b.x;
+            B.o_ru[lane] = b.y;
+            B.o_flag[lane] = (uint32_t)neuron_pop(sh, gid) | (c != 0.0 ? 2u : 0u);
+        }
+        const uint32_t n_e = n - min(n, n_r);
+        const uint32_t nb = min(n_r, K);
+        const bool go = in && n > 0;
+        const unsigned long long sbase = (unsigned long long)sh.ev_base[group];
         uint32_t rtot;
         const uint32_t roff = warp_excl_scan(go ? n : 0u, rtot);
         B.seg[lane] = (int)roff;
         if (lane == 31) B.seg[32] = (int)rtot;
         double* Et = B.t; uint32_t* Es = B.src; float* Ew = B.w; uint16_t* Ep = B.perm;
         uint32_t* Ek = B.keep;
-        if (__any_sync(0xffffffffu, big)) {
-            const int bl = __ffs(__ballot_sync(0xffffffffu, big)) - 1;
+        uint8_t* Eo = B.own;
+        if (rtot > (uint32_t)NEURON_WCAP) {
+            // a single neuron larger than the shared buffer: stage in global scratch
             unsigned long long at = 0;
             int ok = 1;
-            if (big) {
-                if (n > 65535u) ok = 0;
-                at = atomicAdd(&ctl->scratch_used, (unsigned long long)n);
-                if (at + n > (unsigned long long)sh.scratch_cap) ok = 0;
+            if (lane == 0) {
+                if (rtot > 65535u) ok = 0;
+                at = atomicAdd(&ctl->scratch_used, (unsigned long long)rtot);
+                if (at + rtot > (unsigned long long)sh.scratch_cap) ok = 0;
                 if (!ok) cc_raise(ctl, CC_ERR_SCRATCH, t);
                 atomicAdd(&ctl->spilled_total, 1ull);
             }
-            ok = __shfl_sync(0xffffffffu, ok, bl);
-            at = __shfl_sync(0xffffffffu, at, bl);
-            // spill layout: 3 words of 8 B per event (t, src|w, keep|perm)
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if (!ok) continue;
+            // spill layout: 3 words of 8 B per event (t, src|w, keep|perm|own)
             double* base = reinterpret_cast<double*>(sh.scratch) + at * 3;
             const uint32_t cap = rtot;
             Et = base;
@@ -314,11 +385,12 @@ k_stage(const cc_shard sh) {
             Ew = reinterpret_cast<float*>(Es + cap);
             Ek = reinterpret_cast<uint32_t*>(base + 2 * cap);
             Ep = reinterpret_cast<uint16_t*>(Ek + cap);
-            if (!ok) { pending = false; go = false; B.seg[lane] = 0; if (lane == 31) B.seg[32] = 0; rtot = 0; }
+            Eo = reinterpret_cast<uint8_t*>(Ep + cap);
         }
         __syncwarp();
         // ---- 1a gather recurrent records (owner-major flattened)
-        if (!(sh.debug_skip & 1)) {
+        {
+            const uint64_t* bins = sh.bin_rec + (size_t)slot * K * sh.n_local + li0;
             const uint32_t nbr = go ? nb : 0u;
             uint32_t R;
             const uint32_t pr = warp_excl_scan(nbr, R);
@@ -341,6 +413,7 @@ k_stage(const cc_shard sh) {
                         const uint32_t k = r - B.tab[32 + lo];
                         rec[u] = bins[(size_t)k * sh.n_local + lo];
                         dst[u] = B.seg[lo] + (int)k;
+                        Eo[dst[u]] = (uint8_t)lo;
                     }
                 }
 #pragma unroll
@@ -351,7 +424,6 @@ k_stage(const cc_shard sh) {
                     }
                 }
             }
-            __syncwarp();
         }
         // ---- 1b overflow surplus (grouped by k_deliver) and external drive
         if (go) {
@@ -362,6 +434,7 @@ k_stage(const cc_shard sh) {
                     const uint4 r = ov[k];
                     const Ev ev = make_rec_event(sh, (uint64_t)r.y | ((uint64_t)r.z << 32), t_mod_l);
                     Et[b0 + nb + k] = ev.t; Es[b0 + nb + k] = ev.src; Ew[b0 + nb + k] = ev.w;
+                    Eo[b0 + nb + k] = (uint8_t)lane;
                 }
             }
             if (n_e) {
@@ -372,110 +445,84 @@ k_stage(const cc_shard sh) {
                     Et[b0 + n_r + k] = ((double)t + cc_u53(cc_splitmix64(h4 ^ (uint64_t)k))) * sh.dt;
                     Es[b0 + n_r + k] = CC_EXT_SRC;
                     Ew[b0 + n_r + k] = 0.0f;
+                    Eo[b0 + n_r + k] = (uint8_t)lane;
                 }
             }
         }
+#pragma unroll
+        for (int b = 0; b < NBUCKET; ++b) B.hist[lane * NBUCKET + b] = 0u;
         __syncwarp();
-        // ---- 2 counting sort on a monotone time bucket, per-lane exact fix-up
-        if (go && !(sh.debug_skip & 2)) {
-            uint32_t cnt[NBUCKET];
+        // ---- 2 counting sort on a monotone time bucket (flattened over the
+        //      warp), then exact (t, src) order inside each bucket run
+        for (uint32_t e = lane; e < rtot; e += 32) {
+            double x = (Et[e] - t0) * bscale;
+            x = fmin(fmax(x, 0.0), (double)(NBUCKET - 1));
+            const uint32_t key = (uint32_t)Eo[e] * NBUCKET + (uint32_t)x;
+            Ek[e] = (key << 16) | atomicAdd(&B.hist[key], 1u);
+        }
+        __syncwarp();
+        {                                               // bucket starts of neuron `lane`
+            uint32_t acc = (uint32_t)B.seg[lane];
 #pragma unroll
-            for (int b = 0; b < NBUCKET; ++b) cnt[b] = 0u;
-            const int a = (int)roff;
-            for (uint32_t i = 0; i < n; ++i) {
-                double x = (Et[a + i] - t0) * bscale;
-                x = fmin(fmax(x, 0.0), (double)(NBUCKET - 1));
-                const int b = (int)x;
-                uint32_t r = 0;
-#pragma unroll
-                for (int q = 0; q < NBUCKET; ++q) if (q == b) { r = cnt[q]; cnt[q] = r + 1; }
-                Ek[a + i] = ((uint32_t)b << 16) | r;
+            for (int b = 0; b < NBUCKET; ++b) {
+                const uint32_t c = B.hist[lane * NBUCKET + b];
+                B.hist[lane * NBUCKET + b] = acc;
+                acc += c;
             }
-            uint32_t acc = 0;
-#pragma unroll
-            for (int b = 0; b < NBUCKET; ++b) { const uint32_t c = cnt[b]; cnt[b] = acc; acc += c; }
-            for (uint32_t i = 0; i < n; ++i) {
-                const uint32_t kp = Ek[a + i];
-                const int b = (int)(kp >> 16);
-                uint32_t base = 0;
-#pragma unroll
-                for (int q = 0; q < NBUCKET; ++q) if (q == b) base = cnt[q];
-                Ep[a + base + (kp & 0xffffu)] = (uint16_t)i;
-            }
-            // only intra-bucket inversions remain: insertion pass by exact (t, src)
-            for (uint32_t i = 1; i < n; ++i) {
-                const uint16_t pi = Ep[a + i];
+        }
+        __syncwarp();
+        for (uint32_t e = lane; e < rtot; e += 32) {
+            const uint32_t kp = Ek[e];
+            const uint32_t key = kp >> 16;
+            Ep[B.hist[key] + (kp & 0xffffu)] = (uint16_t)(e - (uint32_t)B.seg[key / NBUCKET]);
+        }
+        __syncwarp();
+        for (int i = B.seg[lane]; i < B.seg[lane + 1]; ++i) Eo[i] = (uint8_t)lane;
+        for (int run = lane; run < 32 * NBUCKET; run += 32) {
+            const int o = run / NBUCKET;
+            const int a = B.seg[o];
+            const int r0 = (int)B.hist[run];
+            const int r1 = (run % NBUCKET == NBUCKET - 1) ? B.seg[o + 1] : (int)B.hist[run + 1];
+            for (int i = r0 + 1; i < r1; ++i) {
+                const uint16_t pi = Ep[i];
                 const double ti = Et[a + pi];
                 const uint32_t si = Es[a + pi];
-                uint32_t j = i;
-                while (j > 0) {
-                    const uint16_t pj = Ep[a + j - 1];
+                int j = i;
+                while (j > r0) {
+                    const uint16_t pj = Ep[j - 1];
                     const double tj = Et[a + pj];
                     if (!(ti < tj || (ti == tj && si < Es[a + pj]))) break;
-                    Ep[a + j] = pj;
+                    Ep[j] = pj;
                     --j;
                 }
-                Ep[a + j] = pi;
+                Ep[j] = pi;
             }
-#pragma unroll 4
-            for (uint32_t i = 0; i < n; ++i) Ek[a + i] = (uint32_t)lane;   // owner per sorted slot
         }
         __syncwarp();
         // ---- 3 decay factors of every event -> lane-interleaved stream
-        if (!(sh.debug_skip & 4)) {
-            for (uint32_t p = lane; p < rtot; p += 32) {
-                const int o = (int)Ek[p];
-                const int a = B.seg[o];
-                const uint32_t i = p - (uint32_t)a;           // rank within the neuron
-                const int e = a + Ep[p];
-                const double te = Et[e];
-                const double last = i == 0 ? B.o_last[o] : Et[a + Ep[p - 1]];
-                const double ru = B.o_ru[o];
-                const uint32_t fl = B.o_flag[o];
-                const cc_pop& Q = sh.pop[fl & 1u];
-                const double ff = fmin(fmax(last, ru), te);
-                double em, ec, f;
-                decay_factors(Q, te - ff, (fl & 2u) != 0, em, ec, f);
-                const size_t q = sbase + 32ull * i + (uint32_t)o;
-                sh.ev_t[q] = te;
-                sh.ev_em[q] = em;
-                sh.ev_ec[q] = ec;
-                sh.ev_f[q] = f;
-                sh.ev_w[q] = (Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
-            }
+#pragma unroll 4
+        for (uint32_t p = lane; p < rtot; p += 32) {
+            const int o = Eo[p];
+            const int a = B.seg[o];
+            const uint32_t i = p - (uint32_t)a;           // rank within the neuron
+            const int e = a + Ep[p];
+            const double te = Et[e];
+            const double last = i == 0 ? B.o_last[o] : Et[a + Ep[p - 1]];
+            const double ru = B.o_ru[o];
+            const uint32_t fl = B.o_flag[o];
+            const cc_pop& Q = sh.pop[fl & 1u];
+            const double ff = fmin(fmax(last, ru), te);
+            double em, ec, f;
+            decay_factors(Q, te - ff, (fl & 2u) != 0, em, ec, f);
+            const size_t q = sbase + 32ull * i + (uint32_t)o;
+            sh.ev_t[q] = te;
+            sh.ev_em[q] = em;
+            sh.ev_ec[q] = ec;
+            sh.ev_f[q] = f;
+            sh.ev_w[q] = (Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
         }
-        pending = pending && !go;
         __syncwarp();
-    }
-    // external-event counter: one atomic per warp
-    unsigned long long e_sum = n_e;
-    uint32_t mx_b = n_r, mx_e = n;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        e_sum += __shfl_xor_sync(0xffffffffu, e_sum, o);
-        mx_b = max(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, o));
-        mx_e = max(mx_e, __shfl_xor_sync(0xffffffffu, mx_e, o));
-    }
-    __shared__ unsigned long long blk_e;
-    __shared__ unsigned blk_b, blk_m;
-    if (threadIdx.x == 0) { blk_e = 0; blk_b = 0; blk_m = 0; }
-    __syncthreads();
-    if (lane == 0) {
-        atomicAdd(&blk_e, e_sum);
-        atomicMax(&blk_b, mx_b);
-        atomicMax(&blk_m, mx_e);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (blk_e) atomicAdd(&ctl->ext_events, blk_e);
-        if (blk_b) atomicMax(&ctl->max_bin, blk_b);
-        if (blk_m) atomicMax(&ctl->max_events, blk_m);
-        // last block out retires the ring slot's overflow list
-        __threadfence();
-        if (atomicAdd(&ctl->done_stage, 1u) == gridDim.x - 1) {
-            ctl->done_stage = 0;
-            sh.ovf_cnt[slot] = 0;
-        }
+        if (in) sh.bin_cnt[(size_t)slot * sh.n_local + li] = 0;   // drain the ring slot
     }
 }
 
@@ -494,6 +541,7 @@ k_update(const cc_shard sh) {
     const int lane = threadIdx.x & 31;
     const bool active = li < sh.n_local;
     uint32_t my_spikes = 0;
+    if (li == 0) sh.ovf_cnt[(int)pos_mod(t, sh.d_max)] = 0;   // slot t fully consumed by k_stage
     if (active && !(sh.debug_skip & 8)) {
         const uint32_t n = (uint32_t)sh.ev_n[li];
         if (n || PROBE) {
@@ -646,7 +694,7 @@ __device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
 }
 
 // One warp per delivery piece (<= piece_len synapses of one spiking source).
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
 k_deliver(const cc_shard sh) {
     cc_ctl* ctl = sh.ctl;
     const long long t = *(volatile long long*)&ctl->t;
@@ -654,6 +702,8 @@ k_deliver(const cc_shard sh) {
         sh.log_ctr[pos_mod(t, sh.log_slots)] = 0ull;   // the slot k_neuron(t) fills
         ctl->scratch_used = 0ull;
         ctl->stream_used = 0ull;
+        ctl->n_rounds = 0u;
+        ctl->round_next = 0u;
     }
     const int ep = (int)pos_mod(t - 1, sh.log_slots);
     const unsigned long long n_pieces = sh.log_ctr[ep] >> 32;
@@ -713,7 +763,12 @@ k_deliver(const cc_shard sh) {
             }
         }
     }
-    if (lane == 0 && events) atomicAdd(&ctl->rec_events, events);
+    __shared__ unsigned long long blk_ev;
+    if (threadIdx.x == 0) blk_ev = 0;
+    __syncthreads();
+    if (lane == 0 && events) atomicAdd(&blk_ev, events);
+    __syncthreads();
+    if (threadIdx.x == 0 && blk_ev) atomicAdd(&ctl->rec_events, blk_ev);
 
     // Arrival step t is complete now (k_deliver(t) is its last depositor): the
     // last block out groups its overflow records by target for k_neuron(t).
@@ -804,22 +859,25 @@ extern "C" int cc_init_state(const cc_shard* sh, void* stream) {
 
 extern "C" int cc_deliver(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_deliver: null shard");
-    k_deliver<<<sm_count() * 8, 256, 0, (cudaStream_t)stream>>>(*sh);
+    k_deliver<<<sm_count() * 2, 512, 0, (cudaStream_t)stream>>>(*sh);
     return cc_check_launch("k_deliver");
 }
 
 extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_neuron_step: null shard");
     if (sh->n_local <= 0) return cc_set_error("cc_neuron_step: empty shard");
-    const int warps = (sh->n_local + 31) / 32;
-    const int sblocks = (warps + STAGE_WARPS - 1) / STAGE_WARPS;
+    const int groups = (sh->n_local + 31) / 32;
+    k_plan<<<(groups + 3) / 4, 128, 0, (cudaStream_t)stream>>>(*sh);
+    if (const int rc = cc_check_launch("k_plan")) return rc;
     const size_t smem = stage_warp_bytes() * STAGE_WARPS;
-    static bool configured = false;
-    if (!configured) {
+    static int stage_blocks = 0;
+    if (!stage_blocks) {
         cudaFuncSetAttribute(k_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage, 32 * STAGE_WARPS, smem);
+        stage_blocks = sm_count() * (per_sm > 0 ? per_sm : 1);
     }
-    k_stage<<<sblocks, 32 * STAGE_WARPS, smem, (cudaStream_t)stream>>>(*sh);
+    k_stage<<<stage_blocks, 32 * STAGE_WARPS, smem, (cudaStream_t)stream>>>(*sh);
     if (const int rc = cc_check_launch("k_stage")) return rc;
     const int ublocks = (sh->n_local + 127) / 128;
     if (sh->n_probe > 0)

@@ -186,6 +186,8 @@ class Simulator:
             ev_f=T.empty(stream_cap, dtype=f64, device=dev),
             ev_w=T.empty(stream_cap, dtype=f64, device=dev),
             ev_n=T.zeros(n_local, dtype=i32, device=dev),
+            ev_nr=T.zeros(n_local, dtype=i32, device=dev),
+            rounds=T.zeros(((n_local + 31) // 32) * 32 * 2, dtype=i32, device=dev),
             ev_base=T.zeros((n_local + 31) // 32, dtype=i64, device=dev),
             ctl=T.zeros(C.sizeof(_lib.Ctl) // 8, dtype=i64, device=dev),
         )
@@ -205,6 +207,7 @@ class Simulator:
         sh.ovf_cap, sh.piece_cap, sh.raster_cap = ovf_cap, piece_cap, raster_cap
         sh.scratch_cap, sh.n_rows = scratch_cap, grid.n_neurons
         sh.stream_cap = stream_cap
+        sh.round_cap = ((n_local + 31) // 32) * 32
         sh.out_cap = b["out_gid"].numel()
         lam = cfg.external.mean_per_step(cfg.timestep_ms)
         if lam > 0:
@@ -227,7 +230,7 @@ class Simulator:
         for k in ("bin_cnt", "bin_rec", "ovf_rec", "ovf_cnt", "ovf_sorted", "ovf_off",
                   "ovf_fill", "log_t", "log_gid", "log_ctr",
                   "pieces", "raster_gid", "raster_t", "out_gid", "out_t", "scratch",
-                  "ev_t", "ev_em", "ev_ec", "ev_f", "ev_w", "ev_n", "ev_base",
+                  "ev_t", "ev_em", "ev_ec", "ev_f", "ev_w", "ev_n", "ev_nr", "rounds", "ev_base",
                   "probe_map", "probe_out", "ctl"):
             setattr(sh, k, b[k].data_ptr())
         sh.probe_steps = b["probe_out"].shape[0] if n_probe else 0
