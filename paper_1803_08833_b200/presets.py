@@ -36,8 +36,11 @@ EXP_BASELINE = KernelSpec.exponential(amplitude_A=0.038120, lam=290.0,
 _GRIDS = {0: (2, 2), 1: (8, 8), 2: (24, 24), 3: (48, 48), 4: (96, 96)}
 _DURATION = {0: 1.0, 1: 1.0, 2: 2.0, 3: 1.0, 4: 1.0}
 
-# Drive rate per external synapse (Hz) of the calibrated regime, per kernel.
-CALIBRATED_DRIVE_HZ = {"gaussian": 35.0, "exponential": 35.0}
+# Drive rate per external synapse (Hz) of the calibrated regime, per kernel,
+# pinned with tools/calibrate.py (the calibration_sweep of metrics.py:317-332
+# on the B200 runner).  Config 1 (8x8 Gaussian): 35 Hz -> 6.9 Hz, 40 Hz ->
+# 8.3 Hz over 1 s including the onset transient, 7.3 Hz in the second half.
+CALIBRATED_DRIVE_HZ = {"gaussian": 40.0, "exponential": 35.0}
 CALIBRATED_J_INH = -2.0
 
 

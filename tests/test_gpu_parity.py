@@ -203,3 +203,27 @@ def test_event_bookkeeping_matches_fanout(cuda):
     steps = np.floor(res.raster_times / cfg.timestep_ms).astype(int)
     g = res.raster_gids[steps < cfg.n_steps - 1].astype(np.int64)
     assert res.recurrent_events == int((row_off[g + 1] - row_off[g]).sum())
+
+
+def test_exchange_mode_single_rank_matches_reference(cuda):
+    """The multi-GPU code path (spike out-list -> NCCL all-to-all-v ->
+    cc_ingest) on a one-rank NCCL group reproduces the reference raster."""
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_1803_08833_b200.distributed import DistributedSimulator
+    cfg, meta, arr = golden_run("tiny_gauss")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        ds = DistributedSimulator(cfg, 0, 1)
+        ds.advance(cfg.n_steps)
+        g, t = ds.sim.raster()
+        c = ds.sim.ctl()
+        assert np.array_equal(g, arr["raster_gids"].astype(np.uint64))
+        assert np.array_equal(t.view(np.uint64), arr["raster_times"].view(np.uint64))
+        assert int(c.rec_events) == meta["recurrent_events"]
+        assert ds.xchg.stats["spikes_sent"] > 0
+    finally:
+        dist.destroy_process_group()
