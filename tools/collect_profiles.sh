@@ -1,0 +1,14 @@
+#!/bin/bash
+# Run on the GPU box:  tools/collect_profiles.sh <tag>
+# 1) plain bench run (must exit 0), 2) launch list with gpu__time_duration
+# (serialised, cold cache), 3) --set full captures of the steady-state step
+# kernels.  Outputs land in gpurun_out/; tools/summarize_profiles.py turns them
+# into profiles/<tag>_*.
+set -e
+TAG=${1:-r01}
+CMD="python bench.py --steps 100 --warmup 400 --no-cpu --no-e2e --instrument-steps 10"
+$CMD > gpurun_out/${TAG}_plain.json 2> gpurun_out/${TAG}_plain.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 2200 --csv \
+    --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launches.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_deliver|k_plan|k_stage|k_update" \
+    -s 1350 -c 4 -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
