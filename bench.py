@@ -40,7 +40,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BYTES_PER_EVENT = 17          # 9 B CSR record + 8 B deposit
-KERNELS_PER_STEP = 4          # k_deliver, k_plan, k_stage, k_update
+KERNELS_PER_STEP = 3          # k_deliver, k_plan, k_stage
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 

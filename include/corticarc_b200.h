@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 8
+#define CC_ABI_VERSION 11
 
 /* error bits raised by kernels into cc_ctl.error_bits */
 #define CC_ERR_SPIKE_LOG      0x01u  /* more spikes in one step than log capacity   */
@@ -82,7 +82,7 @@ typedef struct cc_shard {
     int64_t ovf_cap;        /* overflow records per slot                       */
     int64_t piece_cap;      /* delivery pieces per step                        */
     int64_t raster_cap;     /* raster entries                                  */
-    int64_t scratch_cap;    /* staging events (global spill)                   */
+    int64_t scratch_cap;    /* staging events (global spill, 56 B each)        */
     int64_t n_rows;         /* CSR rows (= global neuron count)                */
     int32_t out_cap;        /* exchange out-list capacity                      */
     int32_t ext_budget;     /* m = ceil(lam + 12 sqrt(lam)) + 20; 0 = no drive */
@@ -129,17 +129,10 @@ typedef struct cc_shard {
     uint32_t* out_gid;      /* [out_cap] exchange out-list (direct_log == 0)   */
     double* out_t;          /* [out_cap]                                       */
     float* scratch;         /* [scratch_cap][14] spill staging (56 B per event) */
-    double* ev_t;           /* [stream_cap] staged events of this step, sorted, */
-    double* ev_em;          /*   lane-interleaved per warp: event i of lane L  */
-    double* ev_ec;          /*   at ev_base[warp] + 32 * i + L; time, decay    */
-    double* ev_f;           /*   factors em, ec, f and weight (float64)        */
-    double* ev_w;
     int32_t* ev_n;          /* [n_local] events staged for each neuron          */
     int32_t* ev_nr;         /* [n_local] of which recurrent                     */
     uint32_t* rounds;       /* [round_cap][2] work items: {group, l0 | l1 << 8}   */
     int64_t round_cap;
-    long long* ev_base;     /* [ceil(n_local / 32)] stream base of each warp    */
-    int64_t stream_cap;
     const int32_t* probe_map; /* [n_local] probe slot or -1                    */
     double* probe_out;      /* [steps][n_probe][5] V c last refr V_end         */
     int64_t probe_steps;    /* rows in probe_out                               */

@@ -14,7 +14,7 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BIT
            "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 8
+ABI_VERSION = 11
 
 ERR_BITS = {
     0x01: "spike log full (more spikes in one step than planned)",
@@ -71,9 +71,7 @@ class Shard(C.Structure):
         ("ovf_sorted", _P), ("ovf_off", _P), ("ovf_fill", _P),
         ("log_t", _P), ("log_gid", _P), ("log_ctr", _P), ("pieces", _P),
         ("raster_gid", _P), ("raster_t", _P), ("out_gid", _P), ("out_t", _P),
-        ("scratch", _P), ("ev_t", _P), ("ev_em", _P), ("ev_ec", _P), ("ev_f", _P),
-        ("ev_w", _P), ("ev_n", _P), ("ev_nr", _P), ("rounds", _P), ("round_cap", C.c_int64),
-        ("ev_base", _P), ("stream_cap", C.c_int64),
+        ("scratch", _P), ("ev_n", _P), ("ev_nr", _P), ("rounds", _P), ("round_cap", C.c_int64),
         ("probe_map", _P), ("probe_out", _P),
         ("probe_steps", C.c_int64), ("ctl", _P),
     ]

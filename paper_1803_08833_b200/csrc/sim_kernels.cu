@@ -61,10 +61,11 @@ __device__ __forceinline__ void advance(NState& s, const cc_pop& P, double te) {
         cs = cs * exp(-(ff - s.last) / P.tau_c);
     const double Vs = (s.last < s.ru) ? P.V_r : s.V;
     const double dt = te - ff;
-    const double em = exp(-dt / P.tau_m);
+    // dt == 0: em = exp(-0/tau) = 1 and f = 0 * 1 exactly
+    const double em = dt == 0.0 ? 1.0 : exp(-dt / P.tau_m);
     double Vt = P.E + (Vs - P.E) * em;
     double ct = cs;
-    if (cs != 0.0) {
+    if (cs != 0.0 && dt != 0.0) {
         // with c == 0 the fatigue term is (sfa*0)*f == 0 for the always
         // finite f, and c*ec == 0: both skipped exactly
         const double ec = exp(-dt / P.tau_c);
@@ -78,6 +79,8 @@ __device__ __forceinline__ void advance(NState& s, const cc_pop& P, double te) {
             f = dt * (ec - em) / x;
         Vt = Vt - P.sfa * cs * f;
         ct = cs * ec;
+    } else if (cs != 0.0) {
+        Vt = Vt - P.sfa * cs * 0.0;                            // f = dt * em = +0
     }
     s.V = (te < s.ru) ? P.V_r : Vt;
     s.c = ct;
@@ -137,7 +140,7 @@ __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, i
 }
 
 // ------------------------------------------------------------------ k_stage
-// Phase A of the neuron step.  One warp owns 32 consecutive neurons; their
+// The neuron step.  One warp owns 32 consecutive neurons; their
 // inputs pass through the warp's shared-memory buffer in rounds and every
 // stage is spread over the 32 lanes:
 //   1 gather   recurrent records (owner-major, 4 loads in flight per lane),
@@ -145,29 +148,34 @@ __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, i
 //   2 sort     per neuron: counting sort on a monotone time bucket
 //              b(t) = clamp(floor((t - t0) * NB / dt)) then an insertion pass
 //              fixing order inside buckets: exact (t, src) order
-//   3 factors  em = exp(-dt/tau_m), ec, f (model.py:116-143) of every event,
-//              assuming the step-start refractory window and fatigue flag
-//              (exactly the values the serial update computes), written with
-//              the event time and float64 weight to a lane-interleaved stream
-//              (event i of lane L at ev_base[warp] + 32 i + L) for k_update.
-constexpr int NEURON_WCAP = 384;           // events per round (12 per lane)
+//   3 factors  em = exp(-dt/tau_m), ec, f (model.py:116-143) of every input,
+//              flattened, assuming the step-start refractory window and
+//              fatigue flag: exactly the values the serial update computes
+//   4 update   per lane, in order: affine update, jump, strict threshold,
+//              reset, refractory discard, spike emission; after a spike the
+//              neuron's remaining factors are recomputed in line.
+constexpr int NEURON_WCAP = 256;           // events per round (8 per lane)
 constexpr int NBUCKET = 8;                 // time buckets per neuron
 constexpr int STAGE_WARPS = 2;
 
 struct StageBuf {
-    double* t; uint32_t* src; float* w; uint16_t* perm; uint8_t* own;
+    double* t; double* em; double* ec; double* f;
+    uint32_t* src; float* w; uint16_t* perm; uint8_t* own;
     uint32_t* keep; uint32_t* tab; uint32_t* hist; int* seg;
     double* o_last; double* o_ru; uint32_t* o_flag;
 };
 
 __host__ __device__ constexpr size_t stage_warp_bytes() {
-    return (size_t)NEURON_WCAP * (8 + 4 + 4 + 4 + 2 + 1) + 64 * 4 + 32 * NBUCKET * 4 + 34 * 4
+    return (size_t)NEURON_WCAP * (8 * 4 + 4 + 4 + 4 + 2 + 1) + 64 * 4 + 32 * NBUCKET * 4 + 34 * 4
            + 32 * (8 + 8 + 4) + 32;
 }
 
 __device__ __forceinline__ StageBuf carve(char* p) {
     StageBuf b;
     b.t = (double*)p; p += NEURON_WCAP * 8;
+    b.em = (double*)p; p += NEURON_WCAP * 8;
+    b.ec = (double*)p; p += NEURON_WCAP * 8;
+    b.f = (double*)p; p += NEURON_WCAP * 8;
     b.o_last = (double*)p; p += 32 * 8;
     b.o_ru = (double*)p; p += 32 * 8;
     b.src = (uint32_t*)p; p += NEURON_WCAP * 4;
@@ -209,6 +217,19 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
     return v;
 }
+
+
+// debug_skip & 32 (timing experiments only): per work item, 8 timestamps
+// {claim, gathered, sorted, factors, updated, sm, rtot, warp} written to the
+// tail of the scratch buffer.
+#define CC_DBG(slot_i, val)                                                              \
+    do {                                                                                 \
+        if ((sh.debug_skip & 32) && lane == 0 && item < 65536u) {                        \
+            unsigned long long* d_ = reinterpret_cast<unsigned long long*>(sh.scratch)    \
+                                     + (size_t)sh.scratch_cap * 7 - (size_t)(item + 1) * 8; \
+            d_[slot_i] = (val);                                                          \
+        }                                                                                \
+    } while (0)
 
 __device__ __forceinline__ int neuron_pop(const cc_shard& sh, uint32_t gid) {
     return ((int)(gid % (uint32_t)sh.n_col) < sh.n_exc_col) ? 0 : 1;
@@ -258,19 +279,9 @@ k_plan(const cc_shard sh) {
         mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
         es += __shfl_xor_sync(0xffffffffu, es, o);
     }
-    unsigned long long sbase = 0;
-    int ok = 1;
-    if (lane == 0 && nmax) {
-        sbase = atomicAdd(&ctl->stream_used, 32ull * nmax);
-        if (sbase + 32ull * nmax > (unsigned long long)sh.stream_cap) {
-            cc_raise(ctl, CC_ERR_SCRATCH, t);
-            ok = 0;
-        }
-    }
-    ok = __shfl_sync(0xffffffffu, ok, 0);
-    if (lane == 0) sh.ev_base[group] = (long long)sbase;
+    const int ok = 1;
     if (active) {
-        sh.ev_n[li] = ok ? (int32_t)n : 0;
+        sh.ev_n[li] = (int32_t)n;
         sh.ev_nr[li] = (int32_t)n_r;
     }
     // greedy split of lanes 0..31 into rounds of <= NEURON_WCAP inputs; lane 0
@@ -330,11 +341,13 @@ k_stage(const cc_shard sh) {
     const double t0 = (double)t * sh.dt;
     const double bscale = (double)NBUCKET / sh.dt;
     const unsigned n_items = *(volatile unsigned*)&ctl->n_rounds;
+    uint32_t my_spikes = 0;
     for (;;) {
         unsigned item = 0;
         if (lane == 0) item = atomicAdd(&ctl->round_next, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= n_items || item >= (unsigned)sh.round_cap) break;
+        CC_DBG(0, gtimer());
         const int group = (int)sh.rounds[2 * (size_t)item];
         const uint32_t lr = sh.rounds[2 * (size_t)item + 1];
         const int l0 = (int)(lr & 0xff), l1 = (int)(lr >> 8);
@@ -355,7 +368,6 @@ k_stage(const cc_shard sh) {
         const uint32_t n_e = n - min(n, n_r);
         const uint32_t nb = min(n_r, K);
         const bool go = in && n > 0;
-        const unsigned long long sbase = (unsigned long long)sh.ev_base[group];
         uint32_t rtot;
         const uint32_t roff = warp_excl_scan(go ? n : 0u, rtot);
         B.seg[lane] = (int)roff;
@@ -363,6 +375,7 @@ k_stage(const cc_shard sh) {
         double* Et = B.t; uint32_t* Es = B.src; float* Ew = B.w; uint16_t* Ep = B.perm;
         uint32_t* Ek = B.keep;
         uint8_t* Eo = B.own;
+        unsigned long long spill_at = 0;
         if (rtot > (uint32_t)NEURON_WCAP) {
             // a single neuron larger than the shared buffer: stage in global scratch
             unsigned long long at = 0;
@@ -377,6 +390,7 @@ k_stage(const cc_shard sh) {
             ok = __shfl_sync(0xffffffffu, ok, 0);
             at = __shfl_sync(0xffffffffu, at, 0);
             if (!ok) continue;
+            spill_at = at;
             // spill layout: 3 words of 8 B per event (t, src|w, keep|perm|own)
             double* base = reinterpret_cast<double*>(sh.scratch) + at * 3;
             const uint32_t cap = rtot;
@@ -425,6 +439,7 @@ k_stage(const cc_shard sh) {
                 }
             }
         }
+        CC_DBG(1, gtimer());
         // ---- 1b overflow surplus (grouped by k_deliver) and external drive
         if (go) {
             const int b0 = (int)roff;
@@ -499,130 +514,126 @@ k_stage(const cc_shard sh) {
             }
         }
         __syncwarp();
-        // ---- 3 decay factors of every event -> lane-interleaved stream
-#pragma unroll 4
-        for (uint32_t p = lane; p < rtot; p += 32) {
-            const int o = Eo[p];
-            const int a = B.seg[o];
-            const uint32_t i = p - (uint32_t)a;           // rank within the neuron
-            const int e = a + Ep[p];
-            const double te = Et[e];
-            const double last = i == 0 ? B.o_last[o] : Et[a + Ep[p - 1]];
-            const double ru = B.o_ru[o];
-            const uint32_t fl = B.o_flag[o];
-            const cc_pop& Q = sh.pop[fl & 1u];
-            const double ff = fmin(fmax(last, ru), te);
-            double em, ec, f;
-            decay_factors(Q, te - ff, (fl & 2u) != 0, em, ec, f);
-            const size_t q = sbase + 32ull * i + (uint32_t)o;
-            sh.ev_t[q] = te;
-            sh.ev_em[q] = em;
-            sh.ev_ec[q] = ec;
-            sh.ev_f[q] = f;
-            sh.ev_w[q] = (Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
+        CC_DBG(2, gtimer());
+        // ---- 3 decay factors of every input (flattened over the warp), valid
+        //      under the step-start refractory window and fatigue flag
+        double* Fm = B.em; double* Fc = B.ec; double* Ff = B.f;
+        if (rtot > (uint32_t)NEURON_WCAP) {     // spilled round: factors in scratch too
+            double* base = reinterpret_cast<double*>(sh.scratch) + 3ull * sh.scratch_cap
+                           + 3ull * spill_at;
+            Fm = base; Fc = base + rtot; Ff = base + 2 * rtot;
+        }
+        {
+#pragma unroll 2
+            for (uint32_t p = lane; p < rtot; p += 32) {
+                {
+                    const int o = Eo[p];
+                    const int a = B.seg[o];
+                    const double te = Et[a + Ep[p]];
+                    const double last = (int)p == a ? B.o_last[o] : Et[a + Ep[p - 1]];
+                    const double ru = B.o_ru[o];
+                    const uint32_t fl = B.o_flag[o];
+                    const double ff = fmin(fmax(last, ru), te);
+                    double em, ec, f;
+                    decay_factors(sh.pop[fl & 1u], te - ff, (fl & 2u) != 0, em, ec, f);
+                    Fm[p] = em; Fc[p] = ec; Ff[p] = f;
+                }
+            }
         }
         __syncwarp();
-        if (in) sh.bin_cnt[(size_t)slot * sh.n_local + li] = 0;   // drain the ring slot
-    }
-}
-
-// ------------------------------------------------------------------ k_update
-// Phase B: one thread per neuron walks its staged events in order (coalesced:
-// lane L reads slot 32 i + L) and applies the closed-form update, jump,
-// strict threshold, reset and refractory rule of NeuronBlock.integrate_sorted
-// (model.py:289-337).  After a spike the remaining factors of that neuron are
-// recomputed in line (the staged ones assumed the old refractory window).
-template <bool PROBE>
-__global__ void __launch_bounds__(128)
-k_update(const cc_shard sh) {
-    cc_ctl* ctl = sh.ctl;
-    const long long t = *(volatile long long*)&ctl->t;
-    const int li = blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    const bool active = li < sh.n_local;
-    uint32_t my_spikes = 0;
-    if (li == 0) sh.ovf_cnt[(int)pos_mod(t, sh.d_max)] = 0;   // slot t fully consumed by k_stage
-    if (active && !(sh.debug_skip & 8)) {
-        const uint32_t n = (uint32_t)sh.ev_n[li];
-        if (n || PROBE) {
-            const uint32_t gid = sh.gid[li];
+        CC_DBG(3, gtimer());
+        // ---- 4 in-order update of each neuron (NeuronBlock.integrate_sorted,
+        //      model.py:289-337): affine update, jump, strict threshold, reset
+        if (go) {
             const cc_pop& P = sh.pop[neuron_pop(sh, gid)];
             double* st = sh.state + (size_t)li * 4;
             const double2 a0 = reinterpret_cast<const double2*>(st)[0];
-            const double2 b0 = reinterpret_cast<const double2*>(st)[1];
-            NState s{a0.x, a0.y, b0.x, b0.y};
-            if (n) {
-                const size_t base = (size_t)sh.ev_base[li >> 5] + lane;
-                bool dirty = false;
-                double te_n = sh.ev_t[base], em_n = sh.ev_em[base], ec_n = sh.ev_ec[base];
-                double f_n = sh.ev_f[base], w_n = sh.ev_w[base];
-                for (uint32_t i = 0; i < n; ++i) {
-                    const double te = te_n, w = w_n;
-                    double em = em_n, ec = ec_n, f = f_n;
-                    if (i + 1 < n) {                       // prefetch the next event
-                        const size_t q = base + 32ull * (i + 1);
-                        te_n = sh.ev_t[q]; em_n = sh.ev_em[q]; ec_n = sh.ev_ec[q];
-                        f_n = sh.ev_f[q]; w_n = sh.ev_w[q];
+            NState s{a0.x, a0.y, B.o_last[lane], B.o_ru[lane]};
+            const bool cflag = s.c != 0.0;
+            const int a = (int)roff;
+            bool stale = false;                      // spiked: factors need recomputing
+            for (uint32_t i = 0; i < n; ++i) {
+                const int e = a + Ep[a + i];
+                const double tj = Et[e];
+                bool spike = false;
+                if (!stale && s.ru <= s.last) {
+                    // fast path (no refractory window involved, factors valid):
+                    // free_from == last, V_s == V, not refractory
+                    double Vt = P.E + (s.V - P.E) * Fm[a + i];
+                    if (s.c != 0.0) {
+                        Vt = Vt - P.sfa * s.c * (cflag ? Ff[a + i] : 0.0);
+                        s.c = s.c * (cflag ? Fc[a + i] : 1.0);
                     }
-                    const double ff = fmin(fmax(s.last, s.ru), te);
+                    s.last = tj;
+                    const double V = Vt + ((Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e]);
+                    if (V > P.V_theta) spike = true; else s.V = V;
+                } else {
+                    const double ff = fmin(fmax(s.last, s.ru), tj);
                     double cs = s.c;
-                    if (ff != s.last && cs != 0.0)        // leaving a refractory window: rare
+                    if (ff != s.last && cs != 0.0)   // leaving / inside a refractory window
                         cs = cs * exp(-(ff - s.last) / P.tau_c);
-                    if (dirty) decay_factors(P, te - ff, cs != 0.0, em, ec, f);
+                    double emj, ecj = 1.0, fj = 0.0;
+                    if (stale) {
+                        decay_factors(P, tj - ff, cs != 0.0, emj, ecj, fj);
+                    } else {
+                        emj = Fm[a + i];
+                        if (cflag) { ecj = Fc[a + i]; fj = Ff[a + i]; }
+                    }
+                    // model.py:116-143 and 272-287, reference op order
                     const double Vs = (s.last < s.ru) ? P.V_r : s.V;
-                    double Vt = P.E + (Vs - P.E) * em;
+                    double Vt = P.E + (Vs - P.E) * emj;
                     double ct = cs;
                     if (cs != 0.0) {
-                        Vt = Vt - P.sfa * cs * f;
-                        ct = cs * ec;
+                        Vt = Vt - P.sfa * cs * fj;
+                        ct = cs * ecj;
                     }
-                    s.V = (te < s.ru) ? P.V_r : Vt;
+                    s.V = (tj < s.ru) ? P.V_r : Vt;
                     s.c = ct;
-                    s.last = te;
-                    if (te >= s.ru) {
-                        const double V = s.V + w;
-                        if (V > P.V_theta) {                 // strict threshold
-                            s.V = P.V_r;
-                            s.c = s.c + P.alpha_c;
-                            s.ru = te + P.tau_arp;
-                            dirty = true;
-                            ++my_spikes;
-                            if (sh.direct_log) {
-                                log_spike(sh, t, gid, te);
-                            } else {
-                                const unsigned o = atomicAdd(&ctl->out_n, 1u);
-                                if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = te; }
-                                else cc_raise(ctl, CC_ERR_OUTLIST, t);
-                            }
-                            const unsigned long long r = atomicAdd(&ctl->raster_n, 1ull);
-                            if (r < (unsigned long long)sh.raster_cap) {
-                                sh.raster_gid[r] = gid;
-                                sh.raster_t[r] = te;
-                            } else {
-                                cc_raise(ctl, CC_ERR_RASTER, t);
-                            }
-                        } else {
-                            s.V = V;
-                        }
+                    s.last = tj;
+                    if (tj >= s.ru) {
+                        const double V = s.V + ((Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e]);
+                        if (V > P.V_theta) spike = true; else s.V = V;
                     } else {
-                        s.V = P.V_r;                         // refractory: input discarded
+                        s.V = P.V_r;                     // refractory: input discarded
                     }
                 }
-                reinterpret_cast<double2*>(st)[0] = make_double2(s.V, s.c);
-                reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
-            }
-            if (PROBE) {
-                const int ps = sh.probe_map[li];
-                if (ps >= 0 && t < sh.probe_steps) {
-                    double* o = sh.probe_out + ((size_t)t * sh.n_probe + ps) * 5;
-                    o[0] = s.V; o[1] = s.c; o[2] = s.last; o[3] = s.ru;
-                    NState q = s;
-                    advance(q, P, (double)(t + 1) * sh.dt);
-                    o[4] = q.V;
+                if (spike) {                             // strict threshold crossed
+                    s.V = P.V_r;
+                    s.c = s.c + P.alpha_c;
+                    s.ru = tj + P.tau_arp;
+                    stale = true;
+                    ++my_spikes;
+                    if (sh.direct_log) {
+                        log_spike(sh, t, gid, tj);
+                    } else {
+                        const unsigned o = atomicAdd(&ctl->out_n, 1u);
+                        if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = tj; }
+                        else cc_raise(ctl, CC_ERR_OUTLIST, t);
+                    }
+                    const unsigned long long r = atomicAdd(&ctl->raster_n, 1ull);
+                    if (r < (unsigned long long)sh.raster_cap) {
+                        sh.raster_gid[r] = gid;
+                        sh.raster_t[r] = tj;
+                    } else {
+                        cc_raise(ctl, CC_ERR_RASTER, t);
+                    }
                 }
             }
+            reinterpret_cast<double2*>(st)[0] = make_double2(s.V, s.c);
+            reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
+        }
+        __syncwarp();
+        if (in) sh.bin_cnt[(size_t)slot * sh.n_local + li] = 0;   // drain the ring slot
+        {
+            unsigned smid_;
+            asm volatile("mov.u32 %0, %smid;" : "=r"(smid_));
+            CC_DBG(4, gtimer());
+            CC_DBG(5, (unsigned long long)smid_);
+            CC_DBG(6, (unsigned long long)rtot);
+            CC_DBG(7, (unsigned long long)(blockIdx.x * STAGE_WARPS + wib));
         }
     }
+    // spike counter: one atomic per block; last block out retires the step
     unsigned s_sum = my_spikes;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s_sum += __shfl_xor_sync(0xffffffffu, s_sum, o);
@@ -633,14 +644,36 @@ k_update(const cc_shard sh) {
     __syncthreads();
     if (threadIdx.x == 0) {
         if (blk_s) atomicAdd(&ctl->n_spikes, (unsigned long long)blk_s);
-        // last block out advances the step counter
         __threadfence();
-        if (atomicAdd(&ctl->done_blocks, 1u) == gridDim.x - 1) {
-            ctl->done_blocks = 0;
+        if (atomicAdd(&ctl->done_stage, 1u) == gridDim.x - 1) {
+            ctl->done_stage = 0;
+            sh.ovf_cnt[slot] = 0;              // ring slot t fully consumed
             __threadfence();
             *(volatile long long*)&ctl->t = t + 1;
         }
     }
+}
+
+// ------------------------------------------------------------------ k_update
+// Phase B: one thread per neuron walks its staged events in order (coalesced:
+// lane L reads slot 32 i + L) and applies the closed-form update, jump,
+// strict threshold, reset and refractory rule of NeuronBlock.integrate_sorted
+// (model.py:289-337).  After a spike the remaining factors of that neuron are
+// recomputed in line (the staged ones assumed the old refractory window).
+// Probe recording (tests only): state of the probed neurons after step t and
+// V advanced to (t+1)*dt on a copy, the harness of oracle/make_golden.py.
+__global__ void k_probe(const cc_shard sh) {
+    const long long t = *(volatile long long*)&sh.ctl->t - 1;
+    const int li = blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= sh.n_local || t < 0 || t >= sh.probe_steps) return;
+    const int ps = sh.probe_map[li];
+    if (ps < 0) return;
+    const double* st = sh.state + (size_t)li * 4;
+    NState s{st[0], st[1], st[2], st[3]};
+    double* o = sh.probe_out + ((size_t)t * sh.n_probe + ps) * 5;
+    o[0] = s.V; o[1] = s.c; o[2] = s.last; o[3] = s.ru;
+    advance(s, sh.pop[neuron_pop(sh, sh.gid[li])], (double)(t + 1) * sh.dt);
+    o[4] = s.V;
 }
 
 // Counting sort of one slot's overflow records by target, by a single block
@@ -879,12 +912,12 @@ extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
     }
     k_stage<<<stage_blocks, 32 * STAGE_WARPS, smem, (cudaStream_t)stream>>>(*sh);
     if (const int rc = cc_check_launch("k_stage")) return rc;
-    const int ublocks = (sh->n_local + 127) / 128;
-    if (sh->n_probe > 0)
-        k_update<true><<<ublocks, 128, 0, (cudaStream_t)stream>>>(*sh);
-    else
-        k_update<false><<<ublocks, 128, 0, (cudaStream_t)stream>>>(*sh);
-    return cc_check_launch("k_update");
+    if (sh->n_probe > 0) {
+        k_probe<<<(sh->n_local + 255) / 256, 256, 0, (cudaStream_t)stream>>>(*sh);
+        if (const int rc = cc_check_launch("k_probe")) return rc;
+    }
+    return 0;
+
 }
 
 extern "C" int cc_ingest(const cc_shard* sh, const uint32_t* in_gid, const double* in_t,

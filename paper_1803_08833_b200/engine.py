@@ -159,7 +159,6 @@ class Simulator:
         ovf_cap = max(4096, n_local * 8)
         raster_cap = max(1024, n_local * bound * max(self.chunk, raster_steps or 0))
         scratch_cap = max(1 << 16, n_local * 16)
-        stream_cap = max(1 << 20, n_local * 128)
         self.buf = dict(
             gid=T.from_numpy(gids.astype(np.uint32).view(np.int32)).to(dev),
             state=T.zeros((n_local, 4), dtype=f64, device=dev),
@@ -180,15 +179,10 @@ class Simulator:
             out_t=T.empty(max(1, n_local * bound), dtype=f64, device=dev),
             scratch=T.empty((scratch_cap, 14), dtype=T.float32, device=dev),   # 56 B/event
             probe_map=T.full((n_local,), -1, dtype=i32, device=dev),
-            ev_t=T.empty(stream_cap, dtype=f64, device=dev),
-            ev_em=T.empty(stream_cap, dtype=f64, device=dev),
-            ev_ec=T.empty(stream_cap, dtype=f64, device=dev),
-            ev_f=T.empty(stream_cap, dtype=f64, device=dev),
-            ev_w=T.empty(stream_cap, dtype=f64, device=dev),
             ev_n=T.zeros(n_local, dtype=i32, device=dev),
             ev_nr=T.zeros(n_local, dtype=i32, device=dev),
             rounds=T.zeros(((n_local + 31) // 32) * 32 * 2, dtype=i32, device=dev),
-            ev_base=T.zeros((n_local + 31) // 32, dtype=i64, device=dev),
+
             ctl=T.zeros(C.sizeof(_lib.Ctl) // 8, dtype=i64, device=dev),
         )
         self.probes = None if probes is None else np.asarray(probes, np.int64)
@@ -206,7 +200,6 @@ class Simulator:
         sh.spk_cap, sh.piece_len = spk_cap, piece_len
         sh.ovf_cap, sh.piece_cap, sh.raster_cap = ovf_cap, piece_cap, raster_cap
         sh.scratch_cap, sh.n_rows = scratch_cap, grid.n_neurons
-        sh.stream_cap = stream_cap
         sh.round_cap = ((n_local + 31) // 32) * 32
         sh.out_cap = b["out_gid"].numel()
         lam = cfg.external.mean_per_step(cfg.timestep_ms)
@@ -230,7 +223,7 @@ class Simulator:
         for k in ("bin_cnt", "bin_rec", "ovf_rec", "ovf_cnt", "ovf_sorted", "ovf_off",
                   "ovf_fill", "log_t", "log_gid", "log_ctr",
                   "pieces", "raster_gid", "raster_t", "out_gid", "out_t", "scratch",
-                  "ev_t", "ev_em", "ev_ec", "ev_f", "ev_w", "ev_n", "ev_nr", "rounds", "ev_base",
+                  "ev_n", "ev_nr", "rounds",
                   "probe_map", "probe_out", "ctl"):
             setattr(sh, k, b[k].data_ptr())
         sh.probe_steps = b["probe_out"].shape[0] if n_probe else 0
