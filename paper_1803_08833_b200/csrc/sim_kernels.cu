@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(128)
 k_plan(const cc_shard sh) {
     cc_ctl* ctl = sh.ctl;
     const long long t = *(volatile long long*)&ctl->t;
+    if (*(volatile unsigned*)&ctl->error_bits) return;      // failed run: stop working
     const int lane = threadIdx.x & 31;
     const int group = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int li = group * 32 + lane;
@@ -340,7 +341,8 @@ k_stage(const cc_shard sh) {
     const uint32_t K = (uint32_t)sh.bin_cap;
     const double t0 = (double)t * sh.dt;
     const double bscale = (double)NBUCKET / sh.dt;
-    const unsigned n_items = *(volatile unsigned*)&ctl->n_rounds;
+    const unsigned n_items = *(volatile unsigned*)&ctl->error_bits ? 0u
+                             : *(volatile unsigned*)&ctl->n_rounds;
     uint32_t my_spikes = 0;
     for (;;) {
         unsigned item = 0;
@@ -444,8 +446,15 @@ k_stage(const cc_shard sh) {
         if (go) {
             const int b0 = (int)roff;
             if (n_r > nb) {
-                const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + sh.ovf_off[li];
+                const long long o0 = sh.ovf_off[li];
+                const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + o0;
+                const uint32_t nv = (uint32_t)max(0ll, min((long long)(n_r - nb), sh.ovf_cap - o0));
                 for (uint32_t k = 0; k < n_r - nb; ++k) {
+                    if (k >= nv) {                // dropped by a full overflow list (error raised)
+                        Et[b0 + nb + k] = 1e300; Es[b0 + nb + k] = 0; Ew[b0 + nb + k] = 0.0f;
+                        Eo[b0 + nb + k] = (uint8_t)lane;
+                        continue;
+                    }
                     const uint4 r = ov[k];
                     const Ev ev = make_rec_event(sh, (uint64_t)r.y | ((uint64_t)r.z << 32), t_mod_l);
                     Et[b0 + nb + k] = ev.t; Es[b0 + nb + k] = ev.src; Ew[b0 + nb + k] = ev.w;
@@ -719,8 +728,8 @@ __device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
     uint4* out = reinterpret_cast<uint4*>(sh.ovf_sorted);
     for (unsigned j = threadIdx.x; j < m; j += blockDim.x) {
         const uint4 r = rec[j];
-        const int p = sh.ovf_off[r.x] + atomicAdd(&sh.ovf_fill[r.x], 1);
-        out[p] = r;
+        const long long p = (long long)sh.ovf_off[r.x] + atomicAdd(&sh.ovf_fill[r.x], 1);
+        if (p < sh.ovf_cap) out[p] = r;       // beyond: records were dropped, error raised
     }
     __syncthreads();
     for (unsigned j = threadIdx.x; j < m; j += blockDim.x) sh.ovf_fill[rec[j].x] = 0;
@@ -731,6 +740,7 @@ __global__ void __launch_bounds__(512)
 k_deliver(const cc_shard sh) {
     cc_ctl* ctl = sh.ctl;
     const long long t = *(volatile long long*)&ctl->t;
+    if (*(volatile unsigned*)&ctl->error_bits) return;      // failed run: stop working
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         sh.log_ctr[pos_mod(t, sh.log_slots)] = 0ull;   // the slot k_neuron(t) fills
         ctl->scratch_used = 0ull;

@@ -25,7 +25,12 @@ for r in [float(x) for x in a.rates.split(",")]:
     if a.jinh is not None:
         cfg = replace(cfg, genspec=replace(cfg.genspec, j_inh_exc=a.jinh, j_inh_inh=a.jinh))
     t = time.time()
-    res = run_b200(cfg, 1)
+    try:
+        res = run_b200(cfg, 1)
+    except Exception as err:             # capacity errors = runaway activity
+        print(json.dumps(dict(config=a.config, drive=r, jinh=cfg.genspec.j_inh_exc,
+                              error=str(err)[:200])), flush=True)
+        continue
     n = cfg.grid.n_neurons
     g = res.raster_gids.astype(int)
     exc = (g % 1240) < 992
