@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 11
+#define CC_ABI_VERSION 12
 
 /* error bits raised by kernels into cc_ctl.error_bits */
 #define CC_ERR_SPIKE_LOG      0x01u  /* more spikes in one step than log capacity   */
@@ -75,7 +75,7 @@ typedef struct cc_shard {
     int32_t n_col;          /* neurons per column                              */
     int32_t n_exc_col;      /* excitatory slots per column                     */
     int32_t d_max;          /* delay ring slots (SimConfig.d_max)              */
-    int32_t bin_cap;        /* K records per (slot, neuron) in the dense bins  */
+    int32_t bin_cap;        /* records per (slot, 32-neuron group) list        */
     int32_t log_slots;      /* d_max + 1                                       */
     int32_t spk_cap;        /* spike-log entries per step                      */
     int32_t piece_len;      /* synapses per delivery work piece                */
@@ -108,14 +108,19 @@ typedef struct cc_shard {
     const float* syn_w;     /* [S] weight, mV                                  */
     const uint8_t* syn_d;   /* [S] delay, steps                                */
 
-    /* delay ring of event records (DelayRing, engine.py:124-163) */
-    uint32_t* bin_cnt;      /* [d_max][n_local]                                */
-    uint64_t* bin_rec;      /* [d_max][bin_cap][n_local] spike_ref | w_bits << 32 */
-    uint32_t* ovf_rec;      /* [d_max][ovf_cap][4] {tgt, spike_ref, w_bits, 0}  */
+    /* delay ring of event records (DelayRing, engine.py:124-163): one append
+     * list per (arrival slot, group of 32 consecutive neurons); a record is
+     * (spike_ref << 5 | lane) | w_bits << 32 */
+    int32_t n_groups;       /* ceil(n_local / 32)                              */
+    int32_t pad_g;
+    uint32_t* bin_cnt;      /* [d_max][n_groups] list fill                      */
+    uint64_t* bin_rec;      /* [d_max][n_groups][bin_cap]                      */
+    uint32_t* grp_n;        /* [n_groups] inputs of the current slot per group  */
+    uint32_t* ovf_rec;      /* [d_max][ovf_cap][4] {group, lane, spike_ref, w_bits} */
     uint32_t* ovf_cnt;      /* [d_max]                                         */
-    uint32_t* ovf_sorted;   /* [ovf_cap][4] overflow of the current slot, grouped by target */
-    int32_t* ovf_off;       /* [n_local] start of a neuron's group in ovf_sorted */
-    int32_t* ovf_fill;      /* [n_local] grouping cursors (all zero between steps) */
+    uint32_t* ovf_sorted;   /* [ovf_cap][4] overflow of the current slot, grouped by group */
+    int32_t* ovf_off;       /* [n_groups] start of a group's run in ovf_sorted  */
+    int32_t* ovf_fill;      /* [n_groups] grouping cursors (zero between steps) */
 
     /* spike log (AER payloads, network.py:60-63) and delivery work list */
     double* log_t;          /* [log_slots][spk_cap]                            */

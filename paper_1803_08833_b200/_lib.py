@@ -14,7 +14,7 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BIT
            "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 11
+ABI_VERSION = 12
 
 ERR_BITS = {
     0x01: "spike log full (more spikes in one step than planned)",
@@ -67,7 +67,8 @@ class Shard(C.Structure):
         ("pop", Pop * 2),
         ("gid", _P), ("state", _P),
         ("row_off", _P), ("syn_tgt", _P), ("syn_w", _P), ("syn_d", _P),
-        ("bin_cnt", _P), ("bin_rec", _P), ("ovf_rec", _P), ("ovf_cnt", _P),
+        ("n_groups", C.c_int32), ("pad_g", C.c_int32),
+        ("bin_cnt", _P), ("bin_rec", _P), ("grp_n", _P), ("ovf_rec", _P), ("ovf_cnt", _P),
         ("ovf_sorted", _P), ("ovf_off", _P), ("ovf_fill", _P),
         ("log_t", _P), ("log_gid", _P), ("log_ctr", _P), ("pieces", _P),
         ("raster_gid", _P), ("raster_t", _P), ("out_gid", _P), ("out_t", _P),

@@ -127,7 +127,7 @@ __device__ __forceinline__ void log_spike(const cc_shard& sh, long long t, uint3
 }
 
 __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, int t_mod_l) {
-    const uint32_t ref = (uint32_t)rec;
+    const uint32_t ref = (uint32_t)rec >> 5;                 // low 5 bits: lane in group
     const int e = (int)(ref / (uint32_t)sh.spk_cap);
     int d = t_mod_l - e;
     if (d <= 0) d += sh.log_slots;
@@ -250,10 +250,30 @@ k_plan(const cc_shard sh) {
     if (group * 32 >= sh.n_local) return;
     const bool active = li < sh.n_local;
     const int slot = (int)pos_mod(t, sh.d_max);
+    // inputs from the ring: count this slot's records of the group per lane
+    __shared__ uint32_t lane_cnt[4][32];
+    const int wib = threadIdx.x >> 5;
+    lane_cnt[wib][lane] = 0u;
+    const uint32_t K = (uint32_t)sh.bin_cap;
+    uint32_t* gc = sh.bin_cnt + (size_t)slot * sh.n_groups + group;
+    const uint32_t c_all = *gc;
+    const uint32_t c_list = min(c_all, K);
+    const long long o0 = sh.ovf_off[group];
+    const uint32_t c_ovf = c_all > K ? (uint32_t)max(0ll, min((long long)(c_all - K), sh.ovf_cap - o0)) : 0u;
+    __syncwarp();
+    const uint64_t* lst = sh.bin_rec + ((size_t)slot * sh.n_groups + group) * K;
+    for (uint32_t r = lane; r < c_list; r += 32) atomicAdd(&lane_cnt[wib][(uint32_t)lst[r] & 31u], 1u);
+    const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + o0;
+    for (uint32_t r = lane; r < c_ovf; r += 32) atomicAdd(&lane_cnt[wib][ov[r].y], 1u);
+    __syncwarp();
+    if (lane == 0) {
+        sh.grp_n[group] = c_list + c_ovf;
+        *gc = 0u;                                  // drain the ring slot (read back via grp_n)
+    }
     uint32_t n_r = 0, n_e = 0;
     if (active) {
         const uint32_t gid = sh.gid[li];
-        n_r = sh.bin_cnt[(size_t)slot * sh.n_local + li];
+        n_r = lane_cnt[wib][lane];
         if (sh.ext_budget > 0) {
             // Poisson count by product of uniforms (engine.py:172-188): the
             // prefix product never increases, so stopping at the first
@@ -289,7 +309,6 @@ k_plan(const cc_shard sh) {
     // walks the 32 counts (cheap, through shared memory)
     const unsigned has = __ballot_sync(0xffffffffu, ok && n > 0);
     __shared__ uint32_t cnts[4][32];
-    const int wib = threadIdx.x >> 5;
     cnts[wib][lane] = (ok && active) ? n : 0u;
     __syncwarp();
     if (lane == 0 && has) {
@@ -404,63 +423,44 @@ k_stage(const cc_shard sh) {
             Eo = reinterpret_cast<uint8_t*>(Ep + cap);
         }
         __syncwarp();
-        // ---- 1a gather recurrent records (owner-major flattened)
+        // ---- 1a gather this slot's records of the group (contiguous list, then
+        //      the group's run of the grouped overflow), keep the item's lanes
         {
-            const uint64_t* bins = sh.bin_rec + (size_t)slot * K * sh.n_local + li0;
-            const uint32_t nbr = go ? nb : 0u;
-            uint32_t R;
-            const uint32_t pr = warp_excl_scan(nbr, R);
-            B.tab[lane] = pr + nbr;                   // record ends
-            B.tab[32 + lane] = pr;                    // record starts
+            const uint32_t c_all = sh.grp_n[group];
+            const uint32_t c_list = min(c_all, K);
+            const uint64_t* lst = sh.bin_rec + ((size_t)slot * sh.n_groups + group) * K;
+            const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + sh.ovf_off[group];
+            B.tab[lane] = 0u;                           // per-lane fill cursors
             __syncwarp();
-            for (uint32_t r0 = 0; r0 < R; r0 += 128) {
+            for (uint32_t r0 = 0; r0 < c_all; r0 += 128) {
                 uint64_t rec[4];
-                int dst[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t r = r0 + u * 32 + lane;
-                    dst[u] = -1;
-                    if (r < R) {
-                        int lo = 0, hi = 31;              // first lane whose records end after r
-                        while (lo < hi) {
-                            const int mid = (lo + hi) >> 1;
-                            if (B.tab[mid] > r) hi = mid; else lo = mid + 1;
-                        }
-                        const uint32_t k = r - B.tab[32 + lo];
-                        rec[u] = bins[(size_t)k * sh.n_local + lo];
-                        dst[u] = B.seg[lo] + (int)k;
-                        Eo[dst[u]] = (uint8_t)lo;
+                    rec[u] = ~0ull;
+                    if (r < c_list) {
+                        rec[u] = lst[r];
+                    } else if (r < c_all) {
+                        const uint4 q = ov[r - c_list];
+                        rec[u] = (uint64_t)((q.z << 5) | q.y) | ((uint64_t)q.w << 32);
                     }
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    if (dst[u] >= 0) {
-                        const Ev ev = make_rec_event(sh, rec[u], t_mod_l);
-                        Et[dst[u]] = ev.t; Es[dst[u]] = ev.src; Ew[dst[u]] = ev.w;
-                    }
+                    if (rec[u] == ~0ull) continue;
+                    const int L = (int)((uint32_t)rec[u] & 31u);
+                    if (L < l0 || L >= l1) continue;
+                    const int dst = B.seg[L] + (int)atomicAdd(&B.tab[L], 1u);
+                    const Ev ev = make_rec_event(sh, rec[u], t_mod_l);
+                    Et[dst] = ev.t; Es[dst] = ev.src; Ew[dst] = ev.w;
+                    Eo[dst] = (uint8_t)L;
                 }
             }
+            __syncwarp();
         }
-        CC_DBG(1, gtimer());
         // ---- 1b overflow surplus (grouped by k_deliver) and external drive
         if (go) {
             const int b0 = (int)roff;
-            if (n_r > nb) {
-                const long long o0 = sh.ovf_off[li];
-                const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + o0;
-                const uint32_t nv = (uint32_t)max(0ll, min((long long)(n_r - nb), sh.ovf_cap - o0));
-                for (uint32_t k = 0; k < n_r - nb; ++k) {
-                    if (k >= nv) {                // dropped by a full overflow list (error raised)
-                        Et[b0 + nb + k] = 1e300; Es[b0 + nb + k] = 0; Ew[b0 + nb + k] = 0.0f;
-                        Eo[b0 + nb + k] = (uint8_t)lane;
-                        continue;
-                    }
-                    const uint4 r = ov[k];
-                    const Ev ev = make_rec_event(sh, (uint64_t)r.y | ((uint64_t)r.z << 32), t_mod_l);
-                    Et[b0 + nb + k] = ev.t; Es[b0 + nb + k] = ev.src; Ew[b0 + nb + k] = ev.w;
-                    Eo[b0 + nb + k] = (uint8_t)lane;
-                }
-            }
             if (n_e) {
                 // event times (t_step + u) * dt, u = counter_uniforms(EXTERNAL_TIME, gid, t, j)
                 const uint64_t h4 = cc_splitmix64(cc_splitmix64(sh.h2_time ^ (uint64_t)gid)
@@ -632,7 +632,6 @@ k_stage(const cc_shard sh) {
             reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
         }
         __syncwarp();
-        if (in) sh.bin_cnt[(size_t)slot * sh.n_local + li] = 0;   // drain the ring slot
         {
             unsigned smid_;
             asm volatile("mov.u32 %0, %smid;" : "=r"(smid_));
@@ -690,7 +689,7 @@ __global__ void k_probe(const cc_shard sh) {
 __device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
     __shared__ uint32_t wsum[32];
     __shared__ uint32_t carry;
-    const int n = sh.n_local;
+    const int n = sh.n_groups;
     const uint32_t K = (uint32_t)sh.bin_cap;
     const uint32_t* cnt = sh.bin_cnt + (size_t)s * n;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
@@ -719,7 +718,7 @@ __device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
         }
         __syncthreads();
         const uint32_t before = carry + (warp ? wsum[warp - 1] : 0u) + x - v;
-        if (v) sh.ovf_off[i] = (int32_t)before;
+        if (i < n) sh.ovf_off[i] = (int32_t)before;
         __syncthreads();
         if (threadIdx.x == 0) carry += wsum[nwarp - 1];
         __syncthreads();
@@ -736,8 +735,9 @@ __device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
 }
 
 // One warp per delivery piece (<= piece_len synapses of one spiking source).
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(512, 2)
 k_deliver(const cc_shard sh) {
+    const unsigned long long dbg_t0 = gtimer();
     cc_ctl* ctl = sh.ctl;
     const long long t = *(volatile long long*)&ctl->t;
     if (*(volatile unsigned*)&ctl->error_bits) return;      // failed run: stop working
@@ -756,23 +756,25 @@ k_deliver(const cc_shard sh) {
     const uint4* pcs = reinterpret_cast<const uint4*>(sh.pieces) + (size_t)((t - 1) & 1) * sh.piece_cap;
     const int D = sh.d_max;
     const int base = (int)pos_mod(t - 1, D);
-    const int n = sh.n_local;
+    const int NG = sh.n_groups;
     const int K = sh.bin_cap;
     const int32_t* __restrict__ tgt_a = sh.syn_tgt;
     const float* __restrict__ w_a = sh.syn_w;
     const uint8_t* __restrict__ d_a = sh.syn_d;
     unsigned long long events = 0;
+    const unsigned long long dbg_t1 = gtimer();
     for (long long p = wid; p < (long long)n_pieces; p += nw) {
         const uint4 pc = pcs[p];
         const size_t s0 = (size_t)pc.x | ((size_t)pc.y << 32);
         const uint32_t ref = pc.z;
         const int cnt = (int)pc.w;
         events += (unsigned long long)cnt;
-        for (int j0 = 0; j0 < cnt; j0 += 128) {
-            int tg[4], sl[4];
-            float w[4];
+        constexpr int U = 8;                    // a whole 256-synapse piece in one round trip
+        for (int j0 = 0; j0 < cnt; j0 += 32 * U) {
+            int tg[U], sl[U];
+            float w[U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const int j = j0 + u * 32 + lane;
                 sl[u] = -1;
                 if (j < cnt) {
@@ -783,28 +785,48 @@ k_deliver(const cc_shard sh) {
                     sl[u] = s >= D ? s - D : s;
                 }
             }
-            unsigned pos[4];
+            // one atomic per (slot, group) run of lanes: warp-aggregated reservation
+            unsigned key[U], peers[U], pos[U];
+            unsigned got[U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (sl[u] >= 0) pos[u] = atomicAdd(&sh.bin_cnt[(size_t)sl[u] * n + tg[u]], 1u);
+            for (int u = 0; u < U; ++u) {
+                key[u] = sl[u] >= 0 ? (unsigned)(sl[u] * NG + (tg[u] >> 5)) : 0xffffffffu;
+                peers[u] = __match_any_sync(0xffffffffu, key[u]);
+                got[u] = 0u;
+                if (sl[u] >= 0 && lane == __ffs(peers[u]) - 1)
+                    got[u] = atomicAdd(&sh.bin_cnt[key[u]], (unsigned)__popc(peers[u]));
+            }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < U; ++u) {
+                pos[u] = __shfl_sync(0xffffffffu, got[u], __ffs(peers[u]) - 1)
+                         + __popc(peers[u] & ((1u << lane) - 1u));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
                 if (sl[u] < 0) continue;
-                const uint64_t rec = (uint64_t)ref | ((uint64_t)__float_as_uint(w[u]) << 32);
+                const uint32_t lig = (uint32_t)tg[u] & 31u;
                 if (pos[u] < (unsigned)K) {
-                    sh.bin_rec[((size_t)sl[u] * K + pos[u]) * n + tg[u]] = rec;
+                    sh.bin_rec[(size_t)key[u] * K + pos[u]] =
+                        (uint64_t)((ref << 5) | lig) | ((uint64_t)__float_as_uint(w[u]) << 32);
                 } else {
                     const unsigned o = atomicAdd(&sh.ovf_cnt[sl[u]], 1u);
                     atomicAdd(&ctl->ovf_total, 1ull);
                     if (o < (unsigned)sh.ovf_cap) {
                         reinterpret_cast<uint4*>(sh.ovf_rec)[(size_t)sl[u] * sh.ovf_cap + o] =
-                            make_uint4((uint32_t)tg[u], ref, __float_as_uint(w[u]), 0u);
+                            make_uint4((uint32_t)tg[u] >> 5, lig, ref, __float_as_uint(w[u]));
                     } else {
                         cc_raise(ctl, CC_ERR_OVERFLOW_BIN, t);
                     }
                 }
             }
         }
+    }
+    if ((sh.debug_skip & 256) && lane == 0) {
+        unsigned long long* d_ = reinterpret_cast<unsigned long long*>(sh.scratch)
+                                 + (size_t)sh.scratch_cap * 7 - 65536ull * 8 - (size_t)(wid + 1) * 4;
+        unsigned smid_;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid_));
+        d_[0] = dbg_t0; d_[1] = dbg_t1; d_[2] = gtimer(); d_[3] = (unsigned long long)smid_ | ((unsigned long long)n_pieces << 32);
     }
     __shared__ unsigned long long blk_ev;
     if (threadIdx.x == 0) blk_ev = 0;
@@ -822,6 +844,11 @@ k_deliver(const cc_shard sh) {
         am_last = atomicAdd(&ctl->done_deliver, 1u) == gridDim.x - 1;
     }
     __syncthreads();
+    if ((sh.debug_skip & 256) && threadIdx.x == 0) {
+        unsigned long long* d_ = reinterpret_cast<unsigned long long*>(sh.scratch)
+                                 + (size_t)sh.scratch_cap * 7 - 65536ull * 8 - 65536ull * 4 - (size_t)(blockIdx.x + 1);
+        d_[0] = gtimer();
+    }
     if (!am_last) return;
     __threadfence();
     const int s = (int)pos_mod(t, D);

@@ -109,12 +109,12 @@ def _pop(p) -> _lib.Pop:
 
 
 def default_bin_cap(cfg) -> int:
-    """Dense records per (slot, neuron): ~3x the mean recurrent input per step
-    at 20 Hz plus headroom, a power of two in [64, 512]; the surplus of rarer
-    bursts goes through the grouped overflow list."""
+    """Records per (slot, 32-neuron group) list: 32 x (~3x the inputs an
+    interior neuron receives per step at 20 Hz plus headroom), a power of two
+    in [2048, 16384]; rarer bursts go through the grouped overflow list."""
     from .geometry import expected_fanout
-    want = 3.0 * expected_fanout(cfg.kernel, cfg.grid) * 0.02 * cfg.timestep_ms + 32
-    return int(min(512, max(64, 1 << int(math.ceil(math.log2(want))))))
+    want = 32 * (3.0 * expected_fanout(cfg.kernel, cfg.grid) * 0.02 * cfg.timestep_ms + 32)
+    return int(min(16384, max(2048, 1 << int(math.ceil(math.log2(want))))))
 
 
 def _spikes_per_step_bound(cfg) -> int:
@@ -147,6 +147,7 @@ class Simulator:
         bound = _spikes_per_step_bound(cfg)
         if bin_cap is None:
             bin_cap = default_bin_cap(cfg)
+        n_groups = (n_local + 31) // 32
         self.chunk = max(1, int(chunk))
         self.use_graphs = use_graphs
         direct = (net.size == 1) if direct_log is None else direct_log
@@ -157,18 +158,21 @@ class Simulator:
             raise MemoryBudgetError("spike log references exceed 32 bits")
         piece_cap = max(1, net.pieces_upper_bound(piece_len) * bound)
         ovf_cap = max(4096, n_local * 8)
+        if spk_cap * (D + 1) >= 2 ** 27:
+            raise MemoryBudgetError("spike log references exceed the 27 bits of a ring record")
         raster_cap = max(1024, n_local * bound * max(self.chunk, raster_steps or 0))
         scratch_cap = max(1 << 16, n_local * 16)
         self.buf = dict(
             gid=T.from_numpy(gids.astype(np.uint32).view(np.int32)).to(dev),
             state=T.zeros((n_local, 4), dtype=f64, device=dev),
-            bin_cnt=T.zeros((D, n_local), dtype=i32, device=dev),
-            bin_rec=T.empty((D, bin_cap, n_local), dtype=i64, device=dev),
+            bin_cnt=T.zeros((D, n_groups), dtype=i32, device=dev),
+            bin_rec=T.empty((D, n_groups, bin_cap), dtype=i64, device=dev),
+            grp_n=T.zeros(n_groups, dtype=i32, device=dev),
             ovf_rec=T.empty((D, ovf_cap, 4), dtype=i32, device=dev),
             ovf_cnt=T.zeros(D, dtype=i32, device=dev),
             ovf_sorted=T.empty((ovf_cap, 4), dtype=i32, device=dev),
-            ovf_off=T.empty(n_local, dtype=i32, device=dev),
-            ovf_fill=T.zeros(n_local, dtype=i32, device=dev),
+            ovf_off=T.zeros(n_groups, dtype=i32, device=dev),
+            ovf_fill=T.zeros(n_groups, dtype=i32, device=dev),
             log_t=T.empty((D + 1, spk_cap), dtype=f64, device=dev),
             log_gid=T.empty((D + 1, spk_cap), dtype=i32, device=dev),
             log_ctr=T.zeros(D + 1, dtype=i64, device=dev),
@@ -197,6 +201,7 @@ class Simulator:
         sh = _lib.Shard()
         sh.n_local, sh.n_col, sh.n_exc_col = n_local, n, grid.n_excitatory_per_column
         sh.d_max, sh.bin_cap, sh.log_slots = D, bin_cap, D + 1
+        sh.n_groups = n_groups
         sh.spk_cap, sh.piece_len = spk_cap, piece_len
         sh.ovf_cap, sh.piece_cap, sh.raster_cap = ovf_cap, piece_cap, raster_cap
         sh.scratch_cap, sh.n_rows = scratch_cap, grid.n_neurons
@@ -220,7 +225,7 @@ class Simulator:
         sh.gid, sh.state = b["gid"].data_ptr(), b["state"].data_ptr()
         sh.row_off, sh.syn_tgt = net.row_off.data_ptr(), net.syn_tgt.data_ptr()
         sh.syn_w, sh.syn_d = net.syn_w.data_ptr(), net.syn_d.data_ptr()
-        for k in ("bin_cnt", "bin_rec", "ovf_rec", "ovf_cnt", "ovf_sorted", "ovf_off",
+        for k in ("bin_cnt", "bin_rec", "grp_n", "ovf_rec", "ovf_cnt", "ovf_sorted", "ovf_off",
                   "ovf_fill", "log_t", "log_gid", "log_ctr",
                   "pieces", "raster_gid", "raster_t", "out_gid", "out_t", "scratch",
                   "ev_n", "ev_nr", "rounds",

@@ -20,7 +20,7 @@ sim.advance(int(os.environ.get("T0", "400")))
 L = sim.L
 st = torch.cuda.current_stream().cuda_stream
 snap = {k: v.clone() for k, v in sim.buf.items()}
-variants = {"full": 0, "skip_update": 8}
+variants = {"full": 0, "deliver: loads only": 64, "deliver: loads+store": 64 | 128}
 # neuron = k_stage + k_update (two launches) timed together
 e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
 res = {k: [] for k in variants}
