@@ -113,3 +113,19 @@ def test_partition_tiling_matches_reference_rule():
     assert sorted(owned.tolist()) == list(range(66))
     with pytest.raises(ValueError):
         map_columns_to_workers(GridSpec(nx=2, ny=2, neurons_per_column=4), 5)
+
+
+def test_multiprocess_oracle_runner_event_totals():
+    """oracle/mp_runner.py (the bench's CPU reference arm) on 4 processes
+    reproduces the reference's event totals on shared connectivity."""
+    from oracle import corticarc_oracle as O
+    from oracle.mp_runner import run_oracle_mp
+    cfg, meta, arr = golden_run("tiny_gauss")
+    net = O.build_shard(cfg.grid, cfg.kernel, cfg.genspec, cfg.seed)
+    counts = np.zeros(cfg.grid.n_neurons, np.int64)
+    counts[net.sources.astype(np.int64)] = np.diff(net.offsets)
+    row_off = np.concatenate([[0], np.cumsum(counts)])
+    r = run_oracle_mp(cfg, row_off, net.target_local.astype(np.int64), net.delay, net.weight,
+                      4, cfg.n_steps, 1e9)
+    assert r["steps"] == cfg.n_steps
+    assert r["events"] == meta["recurrent_events"] + meta["external_events"]
