@@ -11,4 +11,4 @@ $CMD > gpurun_out/${TAG}_plain.json 2> gpurun_out/${TAG}_plain.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 2200 --csv \
     --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launches.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_deliver|k_plan|k_stage|k_update" \
-    -s 1350 -c 4 -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
+    -s 1000 -c 3 -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
