@@ -77,7 +77,7 @@ typedef struct cc_shard {
     int32_t d_max;          /* delay ring slots (SimConfig.d_max)              */
     int32_t bin_cap;        /* records per (slot, 32-neuron group) list        */
     int32_t log_slots;      /* d_max + 1                                       */
-    int32_t spk_cap;        /* spike-log entries per step                      */
+    int32_t spk_cap;        /* spike-log entries per step (a power of two)     */
     int32_t piece_len;      /* synapses per delivery work piece                */
     int64_t ovf_cap;        /* overflow records per slot                       */
     int64_t piece_cap;      /* delivery pieces per step                        */

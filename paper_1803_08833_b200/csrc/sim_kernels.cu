@@ -128,7 +128,7 @@ __device__ __forceinline__ void log_spike(const cc_shard& sh, long long t, uint3
 
 __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, int t_mod_l) {
     const uint32_t ref = (uint32_t)rec >> 5;                 // low 5 bits: lane in group
-    const int e = (int)(ref / (uint32_t)sh.spk_cap);
+    const int e = (int)(ref >> (31 - __clz(sh.spk_cap)));      // spk_cap is a power of two
     int d = t_mod_l - e;
     if (d <= 0) d += sh.log_slots;
     Ev ev;
@@ -160,14 +160,14 @@ constexpr int STAGE_WARPS = 2;
 
 struct StageBuf {
     double* t; double* em; double* ec; double* f;
-    uint32_t* src; float* w; uint16_t* perm; uint8_t* own;
+    uint32_t* src; float* w; uint16_t* perm; uint8_t* own; uint8_t* owns;
     uint32_t* keep; uint32_t* tab; uint32_t* hist; int* seg;
     double* o_last; double* o_ru; uint32_t* o_flag;
 };
 
 __host__ __device__ constexpr size_t stage_warp_bytes() {
-    return (size_t)NEURON_WCAP * (8 * 4 + 4 + 4 + 4 + 2 + 1) + 64 * 4 + 32 * NBUCKET * 4 + 34 * 4
-           + 32 * (8 + 8 + 4) + 32;
+    return (size_t)NEURON_WCAP * (8 * 4 + 4 + 4 + 4 + 2 + 1 + 1) + 64 * 4 + 32 * NBUCKET * 4
+           + 34 * 4 + 32 * (8 + 8 + 4) + 32;
 }
 
 __device__ __forceinline__ StageBuf carve(char* p) {
@@ -186,7 +186,8 @@ __device__ __forceinline__ StageBuf carve(char* p) {
     b.seg = (int*)p; p += 34 * 4;
     b.o_flag = (uint32_t*)p; p += 32 * 4;
     b.perm = (uint16_t*)p; p += NEURON_WCAP * 2;
-    b.own = (uint8_t*)p;
+    b.own = (uint8_t*)p; p += NEURON_WCAP;
+    b.owns = (uint8_t*)p;
     return b;
 }
 
@@ -233,6 +234,39 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __device__ __forceinline__ int neuron_pop(const cc_shard& sh, uint32_t gid) {
     return ((int)(gid % (uint32_t)sh.n_col) < sh.n_exc_col) ? 0 : 1;
+}
+
+// General (rare) step of the in-order update: refractory window involved or
+// factors invalidated by an earlier spike in this step.  Out of line to keep
+// the hot loop small.  Returns true when the strict threshold is crossed.
+__device__ __forceinline__ bool slow_step(NState& s, const cc_pop& P, double tj, bool stale,
+                                       bool cflag, double em0, double ec0, double f0, double w) {
+    const double ff = fmin(fmax(s.last, s.ru), tj);
+    double cs = s.c;
+    if (ff != s.last && cs != 0.0)                    // leaving / inside a refractory window
+        cs = cs * exp(-(ff - s.last) / P.tau_c);
+    double emj = em0, ecj = ec0, fj = f0;
+    if (stale) decay_factors(P, tj - ff, cs != 0.0, emj, ecj, fj);
+    else if (!cflag) { ecj = 1.0; fj = 0.0; }
+    // model.py:116-143 and 272-287, reference op order
+    const double Vs = (s.last < s.ru) ? P.V_r : s.V;
+    double Vt = P.E + (Vs - P.E) * emj;
+    double ct = cs;
+    if (cs != 0.0) {
+        Vt = Vt - P.sfa * cs * fj;
+        ct = cs * ecj;
+    }
+    s.V = (tj < s.ru) ? P.V_r : Vt;
+    s.c = ct;
+    s.last = tj;
+    if (tj >= s.ru) {
+        const double V = s.V + w;
+        if (V > P.V_theta) return true;
+        s.V = V;
+    } else {
+        s.V = P.V_r;                                  // refractory: input discarded
+    }
+    return false;
 }
 
 // Planning pass of phase A: per group of 32 neurons, the input counts
@@ -396,6 +430,7 @@ k_stage(const cc_shard sh) {
         double* Et = B.t; uint32_t* Es = B.src; float* Ew = B.w; uint16_t* Ep = B.perm;
         uint32_t* Ek = B.keep;
         uint8_t* Eo = B.own;
+        uint8_t* Eq = B.owns;
         unsigned long long spill_at = 0;
         if (rtot > (uint32_t)NEURON_WCAP) {
             // a single neuron larger than the shared buffer: stage in global scratch
@@ -421,6 +456,7 @@ k_stage(const cc_shard sh) {
             Ek = reinterpret_cast<uint32_t*>(base + 2 * cap);
             Ep = reinterpret_cast<uint16_t*>(Ek + cap);
             Eo = reinterpret_cast<uint8_t*>(Ep + cap);
+            Eq = Eo + cap;
         }
         __syncwarp();
         // ---- 1a gather this slot's records of the group (contiguous list, then
@@ -498,10 +534,11 @@ k_stage(const cc_shard sh) {
         for (uint32_t e = lane; e < rtot; e += 32) {
             const uint32_t kp = Ek[e];
             const uint32_t key = kp >> 16;
-            Ep[B.hist[key] + (kp & 0xffffu)] = (uint16_t)(e - (uint32_t)B.seg[key / NBUCKET]);
+            const uint32_t pos = B.hist[key] + (kp & 0xffffu);
+            Ep[pos] = (uint16_t)(e - (uint32_t)B.seg[key / NBUCKET]);
+            Eq[pos] = (uint8_t)(key / NBUCKET);          // owner of each sorted slot
         }
         __syncwarp();
-        for (int i = B.seg[lane]; i < B.seg[lane + 1]; ++i) Eo[i] = (uint8_t)lane;
         for (int run = lane; run < 32 * NBUCKET; run += 32) {
             const int o = run / NBUCKET;
             const int a = B.seg[o];
@@ -536,7 +573,7 @@ k_stage(const cc_shard sh) {
 #pragma unroll 2
             for (uint32_t p = lane; p < rtot; p += 32) {
                 {
-                    const int o = Eo[p];
+                    const int o = Eq[p];
                     const int a = B.seg[o];
                     const double te = Et[a + Ep[p]];
                     const double last = (int)p == a ? B.o_last[o] : Et[a + Ep[p - 1]];
@@ -577,34 +614,9 @@ k_stage(const cc_shard sh) {
                     const double V = Vt + ((Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e]);
                     if (V > P.V_theta) spike = true; else s.V = V;
                 } else {
-                    const double ff = fmin(fmax(s.last, s.ru), tj);
-                    double cs = s.c;
-                    if (ff != s.last && cs != 0.0)   // leaving / inside a refractory window
-                        cs = cs * exp(-(ff - s.last) / P.tau_c);
-                    double emj, ecj = 1.0, fj = 0.0;
-                    if (stale) {
-                        decay_factors(P, tj - ff, cs != 0.0, emj, ecj, fj);
-                    } else {
-                        emj = Fm[a + i];
-                        if (cflag) { ecj = Fc[a + i]; fj = Ff[a + i]; }
-                    }
-                    // model.py:116-143 and 272-287, reference op order
-                    const double Vs = (s.last < s.ru) ? P.V_r : s.V;
-                    double Vt = P.E + (Vs - P.E) * emj;
-                    double ct = cs;
-                    if (cs != 0.0) {
-                        Vt = Vt - P.sfa * cs * fj;
-                        ct = cs * ecj;
-                    }
-                    s.V = (tj < s.ru) ? P.V_r : Vt;
-                    s.c = ct;
-                    s.last = tj;
-                    if (tj >= s.ru) {
-                        const double V = s.V + ((Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e]);
-                        if (V > P.V_theta) spike = true; else s.V = V;
-                    } else {
-                        s.V = P.V_r;                     // refractory: input discarded
-                    }
+                    const double wv = (Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
+                    spike = slow_step(s, P, tj, stale, cflag, Fm[a + i],
+                                      cflag ? Fc[a + i] : 1.0, cflag ? Ff[a + i] : 0.0, wv);
                 }
                 if (spike) {                             // strict threshold crossed
                     s.V = P.V_r;

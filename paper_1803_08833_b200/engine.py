@@ -154,6 +154,7 @@ class Simulator:
         T = torch
         i32, i64, f64 = T.int32, T.int64, T.float64
         spk_cap = max(1, min(net.nonempty_rows(), grid.n_neurons) * bound)
+        spk_cap = 1 << (spk_cap - 1).bit_length()     # power of two: ref -> slot is a shift
         if spk_cap * (D + 1) >= 2 ** 32:
             raise MemoryBudgetError("spike log references exceed 32 bits")
         piece_cap = max(1, net.pieces_upper_bound(piece_len) * bound)
