@@ -13,7 +13,8 @@ import os
 __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BITS",
            "LIB_PATH"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
+LIB_PATH = os.environ.get("CC_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
 ABI_VERSION = 12
 
 ERR_BITS = {

@@ -36,8 +36,12 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile the library; `out`/`defines` build tuning variants (tools/)."""
+    target = out or LIB
+    os.makedirs(os.path.dirname(os.path.abspath(target)), exist_ok=True)
+    if out is None and not force and not _stale():
         return LIB
     sys.path.insert(0, CSRC)
     try:
@@ -45,17 +49,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     finally:
         sys.path.pop(0)
     gen_ziggurat.emit(os.path.join(GEN, "cc_ziggurat_tables.h"))
-    cmd = [NVCC, *FLAGS, "-shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           "-I", GEN, *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-shared",
+           "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+           "-I", GEN, *[os.path.join(CSRC, s) for s in SOURCES], "-o", target + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     with open(os.path.join(GEN, "ptxas.log"), "w") as fh:
         fh.write(res.stdout + res.stderr)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stderr[-6000:])
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(target + ".tmp", target)
     if verbose:
         print(res.stderr)
-    return LIB
+    return target
 
 
 if __name__ == "__main__":

@@ -154,9 +154,21 @@ __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, i
 //   4 update   per lane, in order: affine update, jump, strict threshold,
 //              reset, refractory discard, spike emission; after a spike the
 //              neuron's remaining factors are recomputed in line.
-constexpr int NEURON_WCAP = 256;           // events per round (8 per lane)
-constexpr int NBUCKET = 8;                 // time buckets per neuron
-constexpr int STAGE_WARPS = 2;
+// Staging constants; overridable with -D for parameter sweeps (build(defines=...)).
+// A sweep at config 1 (w 128..384, buckets 4..16, warps 2..4) put all variants
+// within 12% of each other, the default among the best.
+#ifndef CC_NEURON_WCAP
+#define CC_NEURON_WCAP 256
+#endif
+#ifndef CC_NBUCKET
+#define CC_NBUCKET 8
+#endif
+#ifndef CC_STAGE_WARPS
+#define CC_STAGE_WARPS 2
+#endif
+constexpr int NEURON_WCAP = CC_NEURON_WCAP;   // events per round (8 per lane)
+constexpr int NBUCKET = CC_NBUCKET;           // time buckets per neuron
+constexpr int STAGE_WARPS = CC_STAGE_WARPS;
 
 struct StageBuf {
     double* t; double* em; double* ec; double* f;
