@@ -22,7 +22,10 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 12
+#define CC_ABI_VERSION 13
+
+/* Work items are queued in this many size classes, largest first. */
+#define CC_ITEM_CLASSES 8
 
 /* error bits raised by kernels into cc_ctl.error_bits */
 #define CC_ERR_SPIKE_LOG      0x01u  /* more spikes in one step than log capacity   */
@@ -66,6 +69,7 @@ typedef struct cc_ctl {
     unsigned int n_rounds;                /* staging work items planned this step */
     unsigned int round_next;              /* next work item to claim          */
     unsigned int pad1;
+    unsigned int cls_n[CC_ITEM_CLASSES];  /* work items queued per size class  */
 } cc_ctl;
 
 /* One shard's device state.  Layout documented in DESIGN.md section 3. */
@@ -136,7 +140,8 @@ typedef struct cc_shard {
     float* scratch;         /* [scratch_cap][14] spill staging (56 B per event) */
     int32_t* ev_n;          /* [n_local] events staged for each neuron          */
     int32_t* ev_nr;         /* [n_local] of which recurrent                     */
-    uint32_t* rounds;       /* [round_cap][2] work items: {group, l0 | l1 << 8}   */
+    uint32_t* rounds;       /* [CC_ITEM_CLASSES][round_cap][2] work items {group, l0 | l1 << 8},
+                               by size class (class 0 = largest)                */
     int64_t round_cap;
     const int32_t* probe_map; /* [n_local] probe slot or -1                    */
     double* probe_out;      /* [steps][n_probe][5] V c last refr V_end         */

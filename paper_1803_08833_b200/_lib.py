@@ -15,7 +15,8 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BIT
 
 LIB_PATH = os.environ.get("CC_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 12
+ABI_VERSION = 13
+ITEM_CLASSES = 8
 
 ERR_BITS = {
     0x01: "spike log full (more spikes in one step than planned)",
@@ -47,7 +48,7 @@ class Ctl(C.Structure):
         ("out_n", C.c_uint), ("pad0", C.c_uint), ("spilled_total", C.c_ulonglong),
         ("ovf_total", C.c_ulonglong), ("done_deliver", C.c_uint), ("ovf_grouped", C.c_uint),
         ("stream_used", C.c_ulonglong), ("done_stage", C.c_uint), ("n_rounds", C.c_uint),
-        ("round_next", C.c_uint), ("pad1", C.c_uint),
+        ("round_next", C.c_uint), ("pad1", C.c_uint), ("cls_n", C.c_uint * 8),
     ]
 
 

@@ -352,36 +352,47 @@ k_plan(const cc_shard sh) {
         sh.ev_nr[li] = (int32_t)n_r;
     }
     // greedy split of lanes 0..31 into rounds of <= NEURON_WCAP inputs; lane 0
-    // walks the 32 counts (cheap, through shared memory)
+    // walks the 32 counts (cheap, through shared memory).  Items are queued by
+    // size class, largest first, so that the last items claimed are short.
     const unsigned has = __ballot_sync(0xffffffffu, ok && n > 0);
     __shared__ uint32_t cnts[4][32];
+    __shared__ uint32_t itm[4][32], itt[4][32];
     cnts[wib][lane] = (ok && active) ? n : 0u;
     __syncwarp();
+    int ni = 0;
     if (lane == 0 && has) {
-        uint32_t items[64];
-        int ni = 0;
         int l0 = -1;
         uint32_t tot = 0;
         for (int l = 0; l < 32; ++l) {
             const uint32_t nl = cnts[wib][l];
             if (nl == 0) continue;
             if (l0 >= 0 && tot + nl > (uint32_t)NEURON_WCAP) {
-                items[ni++] = (uint32_t)l0 | ((uint32_t)l << 8);
+                itm[wib][ni] = (uint32_t)l0 | ((uint32_t)l << 8);
+                itt[wib][ni++] = tot;
                 l0 = -1;
-                tot = 0;
             }
             if (l0 < 0) { l0 = l; tot = 0; }
             tot += nl;
         }
-        if (l0 >= 0) items[ni++] = (uint32_t)l0 | (32u << 8);
-        const unsigned at = atomicAdd(&ctl->n_rounds, (unsigned)ni);
-        if (at + ni > (unsigned)sh.round_cap) {
+        if (l0 >= 0) {
+            itm[wib][ni] = (uint32_t)l0 | (32u << 8);
+            itt[wib][ni++] = tot;
+        }
+        atomicAdd(&ctl->n_rounds, (unsigned)ni);
+    }
+    ni = __shfl_sync(0xffffffffu, ni, 0);
+    __syncwarp();
+    if (lane < ni) {
+        const uint32_t tot = itt[wib][lane];
+        const int c = tot >= (uint32_t)NEURON_WCAP
+                          ? 0 : CC_ITEM_CLASSES - 1 - (int)(tot * CC_ITEM_CLASSES / NEURON_WCAP);
+        const unsigned at = atomicAdd(&ctl->cls_n[c], 1u);
+        if (at >= (unsigned)sh.round_cap) {
             cc_raise(ctl, CC_ERR_SCRATCH, t);
         } else {
-            for (int k = 0; k < ni; ++k) {
-                sh.rounds[2 * (size_t)(at + k)] = (uint32_t)group;
-                sh.rounds[2 * (size_t)(at + k) + 1] = items[k];
-            }
+            uint32_t* r = sh.rounds + 2 * ((size_t)c * sh.round_cap + at);
+            r[0] = (uint32_t)group;
+            r[1] = itm[wib][lane];
         }
     }
     if (lane == 0) {
@@ -406,17 +417,28 @@ k_stage(const cc_shard sh) {
     const uint32_t K = (uint32_t)sh.bin_cap;
     const double t0 = (double)t * sh.dt;
     const double bscale = (double)NBUCKET / sh.dt;
-    const unsigned n_items = *(volatile unsigned*)&ctl->error_bits ? 0u
-                             : *(volatile unsigned*)&ctl->n_rounds;
+    // queued items per size class (k_plan is complete); claimed largest first
+    __shared__ unsigned cls_n[CC_ITEM_CLASSES];
+    if (threadIdx.x < CC_ITEM_CLASSES)
+        cls_n[threadIdx.x] = min(*(volatile unsigned*)&ctl->cls_n[threadIdx.x],
+                                 (unsigned)sh.round_cap);
+    __syncthreads();
+    unsigned n_items = 0;
+    for (int c = 0; c < CC_ITEM_CLASSES; ++c) n_items += cls_n[c];
+    if (*(volatile unsigned*)&ctl->error_bits) n_items = 0u;
     uint32_t my_spikes = 0;
     for (;;) {
         unsigned item = 0;
         if (lane == 0) item = atomicAdd(&ctl->round_next, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
-        if (item >= n_items || item >= (unsigned)sh.round_cap) break;
+        if (item >= n_items) break;
         CC_DBG(0, gtimer());
-        const int group = (int)sh.rounds[2 * (size_t)item];
-        const uint32_t lr = sh.rounds[2 * (size_t)item + 1];
+        unsigned r = item;                        // class c, position r in it
+        int c = 0;
+        while (r >= cls_n[c]) r -= cls_n[c++];    // terminates: item < n_items
+        const size_t q = (size_t)c * sh.round_cap + r;
+        const int group = (int)sh.rounds[2 * q];
+        const uint32_t lr = sh.rounds[2 * q + 1];
         const int l0 = (int)(lr & 0xff), l1 = (int)(lr >> 8);
         const int li0 = group * 32;
         const int li = li0 + lane;
@@ -771,6 +793,8 @@ k_deliver(const cc_shard sh) {
         ctl->stream_used = 0ull;
         ctl->n_rounds = 0u;
         ctl->round_next = 0u;
+#pragma unroll
+        for (int c = 0; c < CC_ITEM_CLASSES; ++c) ctl->cls_n[c] = 0u;
     }
     const int ep = (int)pos_mod(t - 1, sh.log_slots);
     const unsigned long long n_pieces = sh.log_ctr[ep] >> 32;

@@ -186,7 +186,8 @@ class Simulator:
             probe_map=T.full((n_local,), -1, dtype=i32, device=dev),
             ev_n=T.zeros(n_local, dtype=i32, device=dev),
             ev_nr=T.zeros(n_local, dtype=i32, device=dev),
-            rounds=T.zeros(((n_local + 31) // 32) * 32 * 2, dtype=i32, device=dev),
+            rounds=T.zeros(_lib.ITEM_CLASSES * ((n_local + 31) // 32) * 32 * 2, dtype=i32,
+                           device=dev),
 
             ctl=T.zeros(C.sizeof(_lib.Ctl) // 8, dtype=i64, device=dev),
         )

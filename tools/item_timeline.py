@@ -46,3 +46,14 @@ for rep in range(2):
     sm = tail[:, 5]
     busy = np.bincount(sm, weights=dur)
     print(f"  per-SM summed item-us: min {busy[busy>0].min():.0f} max {busy.max():.0f} mean {busy[busy>0].mean():.0f}")
+    # tail: when does each warp finish its last item, and how big were late items
+    last = {}
+    for w_, e_ in zip(warps, rel[:, 4]):
+        last[w_] = max(last.get(w_, 0.0), e_)
+    lw = np.sort(np.array(list(last.values())))
+    print("  warp finish quantiles (us):", [round(float(np.percentile(lw, q)), 1) for q in (0, 10, 50, 90, 100)])
+    late = rel[:, 0] > np.percentile(rel[:, 0], 90)
+    print(f"  items claimed in the last 10% of claim times: mean rtot {tail[late, 6].mean():.1f}, "
+          f"mean dur {dur[late].mean():.1f} us (all: {tail[:, 6].mean():.1f}, {dur.mean():.1f})")
+    idle = (rel[:, 4].max() - lw).sum() / (len(lw) * rel[:, 4].max())
+    print(f"  warp-time idle after own last item: {100 * idle:.1f}%")
