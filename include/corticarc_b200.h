@@ -64,7 +64,7 @@ typedef struct cc_ctl {
     unsigned long long ovf_total;         /* records that went to overflow    */
     unsigned int done_deliver;            /* last-block detection (deliver k.) */
     unsigned int ovf_grouped;             /* records grouped for this step    */
-    unsigned long long stream_used;       /* staged-event slots used this step */
+    unsigned long long stream_used;       /* event records used this step      */
     unsigned int done_stage;              /* last-block detection (stage k.)  */
     unsigned int n_rounds;                /* staging work items planned this step */
     unsigned int round_next;              /* next work item to claim          */
@@ -140,6 +140,13 @@ typedef struct cc_shard {
     float* scratch;         /* [scratch_cap][14] spill staging (56 B per event) */
     int32_t* ev_n;          /* [n_local] events staged for each neuron          */
     int32_t* ev_nr;         /* [n_local] of which recurrent                     */
+    /* ordered inputs of the step, one 48 B record {t, w, em, ec, f, 0} each,
+     * written by the staging warps and consumed by the group's in-order update */
+    double* evrec;          /* [evrec_cap][6]                                    */
+    int64_t evrec_cap;
+    int32_t* ev_off;        /* [n_local] first record of each neuron this step  */
+    uint32_t* grp_items;    /* [n_groups] work items planned for each group     */
+    uint32_t* grp_done;     /* [n_groups] items finished (zero between steps)   */
     uint32_t* rounds;       /* [CC_ITEM_CLASSES][round_cap][2] work items {group, l0 | l1 << 8},
                                by size class (class 0 = largest)                */
     int64_t round_cap;

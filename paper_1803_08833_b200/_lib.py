@@ -74,7 +74,9 @@ class Shard(C.Structure):
         ("ovf_sorted", _P), ("ovf_off", _P), ("ovf_fill", _P),
         ("log_t", _P), ("log_gid", _P), ("log_ctr", _P), ("pieces", _P),
         ("raster_gid", _P), ("raster_t", _P), ("out_gid", _P), ("out_t", _P),
-        ("scratch", _P), ("ev_n", _P), ("ev_nr", _P), ("rounds", _P), ("round_cap", C.c_int64),
+        ("scratch", _P), ("ev_n", _P), ("ev_nr", _P),
+        ("evrec", _P), ("evrec_cap", C.c_int64), ("ev_off", _P), ("grp_items", _P),
+        ("grp_done", _P), ("rounds", _P), ("round_cap", C.c_int64),
         ("probe_map", _P), ("probe_out", _P),
         ("probe_steps", C.c_int64), ("ctl", _P),
     ]

@@ -63,5 +63,18 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     return target
 
 
+# A 4-input staging window: most neuron-steps overflow the shared-memory
+# window and take the global-scratch path (tests/test_gpu_parity.py).
+SPILL_VARIANT = os.path.join(PKG, "libcorticarc_b200_w4.so")
+
+
+def build_test_variants(force: bool = False) -> None:
+    if force or not os.path.exists(SPILL_VARIANT) or \
+            os.path.getmtime(SPILL_VARIANT) < os.path.getmtime(LIB):
+        build(force=True, out=SPILL_VARIANT, defines=("CC_NEURON_WCAP=4",))
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--variants" in sys.argv:
+        build_test_variants(force=True)

@@ -146,8 +146,8 @@ __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, i
 //   1 gather   recurrent records (owner-major, 4 loads in flight per lane),
 //              overflow surplus, external Poisson events
 //   2 sort     per neuron: counting sort on a monotone time bucket
-//              b(t) = clamp(floor((t - t0) * NB / dt)) then an insertion pass
-//              fixing order inside buckets: exact (t, src) order
+//              b(t) = clamp(floor((t - t0) * NB_L / dt)), NB_L ~ 2 inputs,
+//              then the exact (t, src) rank of each input inside its bucket
 //   3 factors  em = exp(-dt/tau_m), ec, f (model.py:116-143) of every input,
 //              flattened, assuming the step-start refractory window and
 //              fatigue flag: exactly the values the serial update computes
@@ -155,49 +155,49 @@ __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, i
 //              reset, refractory discard, spike emission; after a spike the
 //              neuron's remaining factors are recomputed in line.
 // Staging constants; overridable with -D for parameter sweeps (build(defines=...)).
-// A sweep at config 1 (w 128..384, buckets 4..16, warps 2..4) put all variants
+// A sweep at config 1 (w 128..384, 4..16 fixed buckets, warps 2..4) put all variants
 // within 12% of each other, the default among the best.
 #ifndef CC_NEURON_WCAP
 #define CC_NEURON_WCAP 256
-#endif
-#ifndef CC_NBUCKET
-#define CC_NBUCKET 8
 #endif
 #ifndef CC_STAGE_WARPS
 #define CC_STAGE_WARPS 2
 #endif
 constexpr int NEURON_WCAP = CC_NEURON_WCAP;   // events per round (8 per lane)
-constexpr int NBUCKET = CC_NBUCKET;           // time buckets per neuron
 constexpr int STAGE_WARPS = CC_STAGE_WARPS;
 
+// Sort buckets per work item: neuron L gets NB_L = min(2 n_L, 352 n_L / rtot + 1)
+// buckets (0 if it has no input), so sum NB_L <= HCAP and a bucket holds ~0.5
+// inputs on average.
+constexpr int HCAP = 384;
+
 struct StageBuf {
-    double* t; double* em; double* ec; double* f;
-    uint32_t* src; float* w; uint16_t* perm; uint8_t* own; uint8_t* owns;
-    uint32_t* keep; uint32_t* tab; uint32_t* hist; int* seg;
-    double* o_last; double* o_ru; uint32_t* o_flag;
+    double* t; double* o_last; double* o_ru; double* bsc;
+    uint32_t* src; float* w; uint32_t* keep; uint32_t* hist; int* seg; uint32_t* o_flag;
+    uint32_t* cbk;
+    uint16_t* perm; uint16_t* prov; uint8_t* own; uint8_t* owns;
 };
 
 __host__ __device__ constexpr size_t stage_warp_bytes() {
-    return (size_t)NEURON_WCAP * (8 * 4 + 4 + 4 + 4 + 2 + 1 + 1) + 64 * 4 + 32 * NBUCKET * 4
-           + 34 * 4 + 32 * (8 + 8 + 4) + 32;
+    return (size_t)NEURON_WCAP * (8 + 4 + 4 + 4 + 2 + 2 + 1 + 1) + HCAP * 4 + 34 * 4
+           + 32 * (8 + 8 + 8 + 4 + 4) + 32;
 }
 
 __device__ __forceinline__ StageBuf carve(char* p) {
     StageBuf b;
     b.t = (double*)p; p += NEURON_WCAP * 8;
-    b.em = (double*)p; p += NEURON_WCAP * 8;
-    b.ec = (double*)p; p += NEURON_WCAP * 8;
-    b.f = (double*)p; p += NEURON_WCAP * 8;
     b.o_last = (double*)p; p += 32 * 8;
     b.o_ru = (double*)p; p += 32 * 8;
+    b.bsc = (double*)p; p += 32 * 8;
     b.src = (uint32_t*)p; p += NEURON_WCAP * 4;
     b.w = (float*)p; p += NEURON_WCAP * 4;
     b.keep = (uint32_t*)p; p += NEURON_WCAP * 4;
-    b.tab = (uint32_t*)p; p += 64 * 4;
-    b.hist = (uint32_t*)p; p += 32 * NBUCKET * 4;
+    b.hist = (uint32_t*)p; p += HCAP * 4;
     b.seg = (int*)p; p += 34 * 4;
     b.o_flag = (uint32_t*)p; p += 32 * 4;
+    b.cbk = (uint32_t*)p; p += 32 * 4;
     b.perm = (uint16_t*)p; p += NEURON_WCAP * 2;
+    b.prov = (uint16_t*)p; p += NEURON_WCAP * 2;
     b.own = (uint8_t*)p; p += NEURON_WCAP;
     b.owns = (uint8_t*)p;
     return b;
@@ -279,6 +279,87 @@ __device__ __forceinline__ bool slow_step(NState& s, const cc_pop& P, double tj,
         s.V = P.V_r;                                  // refractory: input discarded
     }
     return false;
+}
+
+// Ordered inputs of one neuron: the 48 B records {t, w}, {em, ec}, {f, 0}
+// written by the staging warps; the next record is loaded while the current
+// one is applied.
+struct Recs {
+    const double2* R;
+    uint32_t n;
+    double2 r0, r1, r2;
+    __device__ __forceinline__ Recs(const double2* R_, uint32_t n_) : R(R_), n(n_) {
+        r0 = __ldcg(R); r1 = __ldcg(R + 1); r2 = __ldcg(R + 2);
+    }
+    __device__ __forceinline__ void fetch(uint32_t i, double& tj, double& wv, double& em,
+                                          double& ec, double& f) {
+        tj = r0.x; wv = r0.y; em = r1.x; ec = r1.y; f = r2.x;
+        if (i + 1 < n) {
+            r0 = __ldcg(R + 3 * (i + 1));
+            r1 = __ldcg(R + 3 * (i + 1) + 1);
+            r2 = __ldcg(R + 3 * (i + 1) + 2);
+        }
+    }
+};
+
+// In-order update of one neuron (NeuronBlock.integrate_sorted, model.py:289-337):
+// affine update, jump, strict threshold, reset, refractory discard, spike
+// emission.  The factors assume the step-start refractory window; after a
+// spike they are recomputed in line (slow_step).
+__device__ __forceinline__ void update_neuron(const cc_shard& sh, int li, uint32_t n,
+                                              long long t, Recs& src, uint32_t& my_spikes) {
+    cc_ctl* ctl = sh.ctl;
+    const uint32_t gid = sh.gid[li];
+    const cc_pop& P = sh.pop[neuron_pop(sh, gid)];
+    double* st = sh.state + (size_t)li * 4;
+    const double2 a0 = reinterpret_cast<const double2*>(st)[0];
+    const double2 a1 = reinterpret_cast<const double2*>(st)[1];
+    NState s{a0.x, a0.y, a1.x, a1.y};
+    const bool cflag = s.c != 0.0;
+    bool stale = false;                      // spiked: factors need recomputing
+    for (uint32_t i = 0; i < n; ++i) {
+        double tj, wv, em, ec, f;
+        src.fetch(i, tj, wv, em, ec, f);
+        bool spike = false;
+        if (!stale && s.ru <= s.last) {
+            // fast path (no refractory window involved, factors valid):
+            // free_from == last, V_s == V, not refractory; ec = 1, f = 0 when
+            // the neuron started the step without fatigue (c stays 0 then)
+            double Vt = P.E + (s.V - P.E) * em;
+            if (s.c != 0.0) {
+                Vt = Vt - P.sfa * s.c * f;
+                s.c = s.c * ec;
+            }
+            s.last = tj;
+            const double V = Vt + wv;
+            if (V > P.V_theta) spike = true; else s.V = V;
+        } else {
+            spike = slow_step(s, P, tj, stale, cflag, em, ec, f, wv);
+        }
+        if (spike) {                             // strict threshold crossed
+            s.V = P.V_r;
+            s.c = s.c + P.alpha_c;
+            s.ru = tj + P.tau_arp;
+            stale = true;
+            ++my_spikes;
+            if (sh.direct_log) {
+                log_spike(sh, t, gid, tj);
+            } else {
+                const unsigned o = atomicAdd(&ctl->out_n, 1u);
+                if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = tj; }
+                else cc_raise(ctl, CC_ERR_OUTLIST, t);
+            }
+            const unsigned long long r = atomicAdd(&ctl->raster_n, 1ull);
+            if (r < (unsigned long long)sh.raster_cap) {
+                sh.raster_gid[r] = gid;
+                sh.raster_t[r] = tj;
+            } else {
+                cc_raise(ctl, CC_ERR_RASTER, t);
+            }
+        }
+    }
+    reinterpret_cast<double2*>(st)[0] = make_double2(s.V, s.c);
+    reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
 }
 
 // Planning pass of phase A: per group of 32 neurons, the input counts
@@ -381,6 +462,7 @@ k_plan(const cc_shard sh) {
         atomicAdd(&ctl->n_rounds, (unsigned)ni);
     }
     ni = __shfl_sync(0xffffffffu, ni, 0);
+    if (lane == 0) sh.grp_items[group] = (uint32_t)ni;
     __syncwarp();
     if (lane < ni) {
         const uint32_t tot = itt[wib][lane];
@@ -403,7 +485,10 @@ k_plan(const cc_shard sh) {
 }
 
 // Phase A proper: persistent warps claim work items from the queue.
-__global__ void __launch_bounds__(32 * STAGE_WARPS)
+#ifndef CC_STAGE_MINB
+#define CC_STAGE_MINB 10
+#endif
+__global__ void __launch_bounds__(32 * STAGE_WARPS, CC_STAGE_MINB)
 k_stage(const cc_shard sh) {
     extern __shared__ __align__(16) char nsm[];
     cc_ctl* ctl = sh.ctl;
@@ -416,7 +501,6 @@ k_stage(const cc_shard sh) {
     const int t_mod_l = (int)pos_mod(t, sh.log_slots);
     const uint32_t K = (uint32_t)sh.bin_cap;
     const double t0 = (double)t * sh.dt;
-    const double bscale = (double)NBUCKET / sh.dt;
     // queued items per size class (k_plan is complete); claimed largest first
     __shared__ unsigned cls_n[CC_ITEM_CLASSES];
     if (threadIdx.x < CC_ITEM_CLASSES)
@@ -463,6 +547,7 @@ k_stage(const cc_shard sh) {
         if (lane == 31) B.seg[32] = (int)rtot;
         double* Et = B.t; uint32_t* Es = B.src; float* Ew = B.w; uint16_t* Ep = B.perm;
         uint32_t* Ek = B.keep;
+        uint16_t* Epv = B.prov;
         uint8_t* Eo = B.own;
         uint8_t* Eq = B.owns;
         unsigned long long spill_at = 0;
@@ -491,6 +576,8 @@ k_stage(const cc_shard sh) {
             Ep = reinterpret_cast<uint16_t*>(Ek + cap);
             Eo = reinterpret_cast<uint8_t*>(Ep + cap);
             Eq = Eo + cap;
+            Epv = reinterpret_cast<uint16_t*>(reinterpret_cast<double*>(sh.scratch)
+                                              + 6ull * sh.scratch_cap + at);
         }
         __syncwarp();
         // ---- 1a gather this slot's records of the group (contiguous list, then
@@ -500,7 +587,7 @@ k_stage(const cc_shard sh) {
             const uint32_t c_list = min(c_all, K);
             const uint64_t* lst = sh.bin_rec + ((size_t)slot * sh.n_groups + group) * K;
             const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + sh.ovf_off[group];
-            B.tab[lane] = 0u;                           // per-lane fill cursors
+            B.hist[lane] = 0u;                          // per-lane fill cursors
             __syncwarp();
             for (uint32_t r0 = 0; r0 < c_all; r0 += 128) {
                 uint64_t rec[4];
@@ -520,7 +607,7 @@ k_stage(const cc_shard sh) {
                     if (rec[u] == ~0ull) continue;
                     const int L = (int)((uint32_t)rec[u] & 31u);
                     if (L < l0 || L >= l1) continue;
-                    const int dst = B.seg[L] + (int)atomicAdd(&B.tab[L], 1u);
+                    const int dst = B.seg[L] + (int)atomicAdd(&B.hist[L], 1u);
                     const Ev ev = make_rec_event(sh, rec[u], t_mod_l);
                     Et[dst] = ev.t; Es[dst] = ev.src; Ew[dst] = ev.w;
                     Eo[dst] = (uint8_t)L;
@@ -543,141 +630,128 @@ k_stage(const cc_shard sh) {
                 }
             }
         }
-#pragma unroll
-        for (int b = 0; b < NBUCKET; ++b) B.hist[lane * NBUCKET + b] = 0u;
-        __syncwarp();
-        // ---- 2 counting sort on a monotone time bucket (flattened over the
-        //      warp), then exact (t, src) order inside each bucket run
-        for (uint32_t e = lane; e < rtot; e += 32) {
-            double x = (Et[e] - t0) * bscale;
-            x = fmin(fmax(x, 0.0), (double)(NBUCKET - 1));
-            const uint32_t key = (uint32_t)Eo[e] * NBUCKET + (uint32_t)x;
-            Ek[e] = (key << 16) | atomicAdd(&B.hist[key], 1u);
-        }
-        __syncwarp();
-        {                                               // bucket starts of neuron `lane`
-            uint32_t acc = (uint32_t)B.seg[lane];
-#pragma unroll
-            for (int b = 0; b < NBUCKET; ++b) {
-                const uint32_t c = B.hist[lane * NBUCKET + b];
-                B.hist[lane * NBUCKET + b] = acc;
-                acc += c;
+        // ---- 2 order each neuron's inputs by (t, src): counting sort on a
+        //      monotone time bucket (adaptive count per neuron, flattened over
+        //      the warp), then the exact rank of each input inside its bucket
+        {
+            const uint32_t nbl = go ? min(2u * n, 352u * n / rtot + 1u) : 0u;
+            uint32_t nbt;
+            const uint32_t cb = warp_excl_scan(nbl, nbt);
+            B.cbk[lane] = cb | (nbl << 16);
+            B.bsc[lane] = (double)nbl / sh.dt;
+            __syncwarp();
+            for (uint32_t i = lane; i < nbt; i += 32) B.hist[i] = 0u;
+            __syncwarp();
+            for (uint32_t e = lane; e < rtot; e += 32) {
+                const uint32_t o = Eo[e];
+                const uint32_t ck = B.cbk[o];
+                double x = (Et[e] - t0) * B.bsc[o];
+                x = fmin(fmax(x, 0.0), (double)((ck >> 16) - 1u));
+                const uint32_t key = (ck & 0xffffu) + (uint32_t)x;
+                Ek[e] = (key << 16) | atomicAdd(&B.hist[key], 1u);
             }
-        }
-        __syncwarp();
-        for (uint32_t e = lane; e < rtot; e += 32) {
-            const uint32_t kp = Ek[e];
-            const uint32_t key = kp >> 16;
-            const uint32_t pos = B.hist[key] + (kp & 0xffffu);
-            Ep[pos] = (uint16_t)(e - (uint32_t)B.seg[key / NBUCKET]);
-            Eq[pos] = (uint8_t)(key / NBUCKET);          // owner of each sorted slot
-        }
-        __syncwarp();
-        for (int run = lane; run < 32 * NBUCKET; run += 32) {
-            const int o = run / NBUCKET;
-            const int a = B.seg[o];
-            const int r0 = (int)B.hist[run];
-            const int r1 = (run % NBUCKET == NBUCKET - 1) ? B.seg[o + 1] : (int)B.hist[run + 1];
-            for (int i = r0 + 1; i < r1; ++i) {
-                const uint16_t pi = Ep[i];
-                const double ti = Et[a + pi];
-                const uint32_t si = Es[a + pi];
-                int j = i;
-                while (j > r0) {
-                    const uint16_t pj = Ep[j - 1];
-                    const double tj = Et[a + pj];
-                    if (!(ti < tj || (ti == tj && si < Es[a + pj]))) break;
-                    Ep[j] = pj;
-                    --j;
+            __syncwarp();
+            // exclusive scan of the flattened counters: bucket starts, which
+            // are already segmented by neuron (lane-major order); packed
+            // start | count << 16
+            const uint32_t per = (nbt + 31u) / 32u;
+            const uint32_t i0 = min(lane * per, nbt), i1 = min(i0 + per, nbt);
+            uint32_t sum = 0;
+            for (uint32_t i = i0; i < i1; ++i) sum += B.hist[i];
+            uint32_t tot2;
+            uint32_t base = warp_excl_scan(sum, tot2);
+            for (uint32_t i = i0; i < i1; ++i) {
+                const uint32_t c = B.hist[i];
+                B.hist[i] = base | (c << 16);
+                base += c;
+            }
+            __syncwarp();
+            // scatter: singleton buckets are final, others provisional
+            for (uint32_t e = lane; e < rtot; e += 32) {
+                const uint32_t kp = Ek[e];
+                const uint32_t h = B.hist[kp >> 16];
+                const uint32_t o = Eo[e];
+                const uint32_t rel = e - (uint32_t)B.seg[o];
+                const uint32_t pos = (h & 0xffffu) + (kp & 0xffffu);
+                if ((h >> 16) == 1u) Ep[pos] = (uint16_t)rel;
+                else Epv[pos] = (uint16_t)rel;
+                Eq[pos] = (uint8_t)o;                   // owner of each sorted slot
+            }
+            __syncwarp();
+            // exact order inside shared buckets: rank among the bucket's inputs
+            // by (t, src), ties by staging index (identical inputs commute)
+            for (uint32_t e = lane; e < rtot; e += 32) {
+                const uint32_t kp = Ek[e];
+                const uint32_t h = B.hist[kp >> 16];
+                const uint32_t c = h >> 16;
+                if (c == 1u) continue;
+                const uint32_t s0 = h & 0xffffu;
+                const uint32_t o = Eo[e];
+                const int a = B.seg[o];
+                const uint32_t rel = e - (uint32_t)a;
+                const double te = Et[e];
+                const uint32_t se = Es[e];
+                uint32_t rank = 0;
+                for (uint32_t q = s0; q < s0 + c; ++q) {
+                    const uint32_t pq = Epv[q];
+                    const double tq = Et[a + pq];
+                    const uint32_t sq = Es[a + pq];
+                    rank += (tq < te || (tq == te && (sq < se || (sq == se && pq < rel)))) ? 1u : 0u;
                 }
-                Ep[j] = pi;
+                Ep[s0 + rank] = (uint16_t)rel;
             }
         }
         __syncwarp();
         CC_DBG(2, gtimer());
         // ---- 3 decay factors of every input (flattened over the warp), valid
-        //      under the step-start refractory window and fatigue flag
-        double* Fm = B.em; double* Fc = B.ec; double* Ff = B.f;
-        if (rtot > (uint32_t)NEURON_WCAP) {     // spilled round: factors in scratch too
-            double* base = reinterpret_cast<double*>(sh.scratch) + 3ull * sh.scratch_cap
-                           + 3ull * spill_at;
-            Fm = base; Fc = base + rtot; Ff = base + 2 * rtot;
+        //      under the step-start refractory window and fatigue flag, written
+        //      with t and w as one ordered record per input
+        unsigned long long rbase = 0;
+        if (lane == 0 && rtot) {
+            rbase = atomicAdd(&ctl->stream_used, (unsigned long long)rtot);
+            // cannot happen: evrec_cap covers a full ring slot + overflow + drive
+            if (rbase + rtot > (unsigned long long)sh.evrec_cap) cc_raise(ctl, CC_ERR_SCRATCH, t);
         }
+        rbase = __shfl_sync(0xffffffffu, rbase, 0);
+        if (rbase + rtot > (unsigned long long)sh.evrec_cap) continue;
         {
-#pragma unroll 2
+            double2* R = reinterpret_cast<double2*>(sh.evrec) + 3 * rbase;
             for (uint32_t p = lane; p < rtot; p += 32) {
-                {
-                    const int o = Eq[p];
-                    const int a = B.seg[o];
-                    const double te = Et[a + Ep[p]];
-                    const double last = (int)p == a ? B.o_last[o] : Et[a + Ep[p - 1]];
-                    const double ru = B.o_ru[o];
-                    const uint32_t fl = B.o_flag[o];
-                    const double ff = fmin(fmax(last, ru), te);
-                    double em, ec, f;
-                    decay_factors(sh.pop[fl & 1u], te - ff, (fl & 2u) != 0, em, ec, f);
-                    Fm[p] = em; Fc[p] = ec; Ff[p] = f;
-                }
+                const int o = Eq[p];
+                const int a = B.seg[o];
+                const int e = a + Ep[p];
+                const double te = Et[e];
+                const double last = (int)p == a ? B.o_last[o] : Et[a + Ep[p - 1]];
+                const double ru = B.o_ru[o];
+                const uint32_t fl = B.o_flag[o];
+                const double ff = fmin(fmax(last, ru), te);
+                double em, ec, f;
+                decay_factors(sh.pop[fl & 1u], te - ff, (fl & 2u) != 0, em, ec, f);
+                const double wv = (Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
+                R[3 * p] = make_double2(te, wv);
+                R[3 * p + 1] = make_double2(em, ec);
+                R[3 * p + 2] = make_double2(f, 0.0);
             }
         }
-        __syncwarp();
+        if (go) sh.ev_off[li] = (int32_t)(rbase + roff);
         CC_DBG(3, gtimer());
-        // ---- 4 in-order update of each neuron (NeuronBlock.integrate_sorted,
-        //      model.py:289-337): affine update, jump, strict threshold, reset
-        if (go) {
-            const cc_pop& P = sh.pop[neuron_pop(sh, gid)];
-            double* st = sh.state + (size_t)li * 4;
-            const double2 a0 = reinterpret_cast<const double2*>(st)[0];
-            NState s{a0.x, a0.y, B.o_last[lane], B.o_ru[lane]};
-            const bool cflag = s.c != 0.0;
-            const int a = (int)roff;
-            bool stale = false;                      // spiked: factors need recomputing
-            for (uint32_t i = 0; i < n; ++i) {
-                const int e = a + Ep[a + i];
-                const double tj = Et[e];
-                bool spike = false;
-                if (!stale && s.ru <= s.last) {
-                    // fast path (no refractory window involved, factors valid):
-                    // free_from == last, V_s == V, not refractory
-                    double Vt = P.E + (s.V - P.E) * Fm[a + i];
-                    if (s.c != 0.0) {
-                        Vt = Vt - P.sfa * s.c * (cflag ? Ff[a + i] : 0.0);
-                        s.c = s.c * (cflag ? Fc[a + i] : 1.0);
-                    }
-                    s.last = tj;
-                    const double V = Vt + ((Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e]);
-                    if (V > P.V_theta) spike = true; else s.V = V;
-                } else {
-                    const double wv = (Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
-                    spike = slow_step(s, P, tj, stale, cflag, Fm[a + i],
-                                      cflag ? Fc[a + i] : 1.0, cflag ? Ff[a + i] : 0.0, wv);
-                }
-                if (spike) {                             // strict threshold crossed
-                    s.V = P.V_r;
-                    s.c = s.c + P.alpha_c;
-                    s.ru = tj + P.tau_arp;
-                    stale = true;
-                    ++my_spikes;
-                    if (sh.direct_log) {
-                        log_spike(sh, t, gid, tj);
-                    } else {
-                        const unsigned o = atomicAdd(&ctl->out_n, 1u);
-                        if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = tj; }
-                        else cc_raise(ctl, CC_ERR_OUTLIST, t);
-                    }
-                    const unsigned long long r = atomicAdd(&ctl->raster_n, 1ull);
-                    if (r < (unsigned long long)sh.raster_cap) {
-                        sh.raster_gid[r] = gid;
-                        sh.raster_t[r] = tj;
-                    } else {
-                        cc_raise(ctl, CC_ERR_RASTER, t);
-                    }
-                }
+        // ---- 4 publish; the warp finishing a group's last item runs the
+        //      group's in-order update (one lane per neuron)
+        __threadfence();
+        unsigned prev = 0;
+        if (lane == 0) prev = atomicAdd(&sh.grp_done[group], 1u);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev + 1u == sh.grp_items[group]) {
+            __threadfence();
+            if (lane == 0) sh.grp_done[group] = 0u;
+            const int lg = li0 + lane;
+            const uint32_t ng = lg < sh.n_local ? (uint32_t)sh.ev_n[lg] : 0u;
+            if (ng) {
+                Recs src(reinterpret_cast<const double2*>(sh.evrec)
+                         + 3 * (size_t)__ldcg(&sh.ev_off[lg]), ng);
+                update_neuron(sh, lg, ng, t, src, my_spikes);
             }
-            reinterpret_cast<double2*>(st)[0] = make_double2(s.V, s.c);
-            reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
         }
-        __syncwarp();
         {
             unsigned smid_;
             asm volatile("mov.u32 %0, %smid;" : "=r"(smid_));

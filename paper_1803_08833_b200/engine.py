@@ -163,6 +163,11 @@ class Simulator:
             raise MemoryBudgetError("spike log references exceed the 27 bits of a ring record")
         raster_cap = max(1024, n_local * bound * max(self.chunk, raster_steps or 0))
         scratch_cap = max(1 << 16, n_local * 16)
+        # ordered-input records of one step: at most a full ring slot, its
+        # overflow list and every neuron's Poisson budget
+        lam = cfg.external.mean_per_step(cfg.timestep_ms)
+        ext_m = int(math.ceil(lam + 12.0 * math.sqrt(lam))) + 20 if lam > 0 else 0
+        evrec_cap = n_groups * bin_cap + ovf_cap + n_local * ext_m
         self.buf = dict(
             gid=T.from_numpy(gids.astype(np.uint32).view(np.int32)).to(dev),
             state=T.zeros((n_local, 4), dtype=f64, device=dev),
@@ -186,6 +191,10 @@ class Simulator:
             probe_map=T.full((n_local,), -1, dtype=i32, device=dev),
             ev_n=T.zeros(n_local, dtype=i32, device=dev),
             ev_nr=T.zeros(n_local, dtype=i32, device=dev),
+            evrec=T.empty((evrec_cap, 6), dtype=f64, device=dev),          # 48 B/input
+            ev_off=T.zeros(n_local, dtype=i32, device=dev),
+            grp_items=T.zeros(n_groups, dtype=i32, device=dev),
+            grp_done=T.zeros(n_groups, dtype=i32, device=dev),
             rounds=T.zeros(_lib.ITEM_CLASSES * ((n_local + 31) // 32) * 32 * 2, dtype=i32,
                            device=dev),
 
@@ -207,6 +216,7 @@ class Simulator:
         sh.spk_cap, sh.piece_len = spk_cap, piece_len
         sh.ovf_cap, sh.piece_cap, sh.raster_cap = ovf_cap, piece_cap, raster_cap
         sh.scratch_cap, sh.n_rows = scratch_cap, grid.n_neurons
+        sh.evrec_cap = evrec_cap
         sh.round_cap = ((n_local + 31) // 32) * 32
         sh.out_cap = b["out_gid"].numel()
         lam = cfg.external.mean_per_step(cfg.timestep_ms)
@@ -230,7 +240,7 @@ class Simulator:
         for k in ("bin_cnt", "bin_rec", "grp_n", "ovf_rec", "ovf_cnt", "ovf_sorted", "ovf_off",
                   "ovf_fill", "log_t", "log_gid", "log_ctr",
                   "pieces", "raster_gid", "raster_t", "out_gid", "out_t", "scratch",
-                  "ev_n", "ev_nr", "rounds",
+                  "ev_n", "ev_nr", "rounds", "evrec", "ev_off", "grp_items", "grp_done",
                   "probe_map", "probe_out", "ctl"):
             setattr(sh, k, b[k].data_ptr())
         sh.probe_steps = b["probe_out"].shape[0] if n_probe else 0

@@ -158,6 +158,47 @@ def test_overflow_path_same_raster(cuda):
     _assert_same_run(res, meta, arr)
 
 
+_SPILL_CHECK = """
+import json, sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, {root!r} + "/tests")
+import numpy as np
+from conftest import golden_run
+from paper_1803_08833_b200 import _lib
+from paper_1803_08833_b200.engine import run_b200
+assert _lib.LIB_PATH.endswith("_w4.so")
+out = {{}}
+for name in ("tiny_gauss_long", "tiny_exp"):
+    cfg, meta, arr = golden_run(name)
+    r = run_b200(cfg, 1)
+    out[name] = dict(spilled=r.device_stats["spilled"],
+                     same=bool(np.array_equal(r.raster_gids, arr["raster_gids"].astype(np.uint64))
+                               and r.raster_checksum == meta["raster_checksum"]
+                               and r.recurrent_events == meta["recurrent_events"]))
+print(json.dumps(out))
+"""
+
+
+def test_spill_path_small_window(cuda):
+    """A 16-input staging window (libcorticarc_b200_w4.so, built by build())
+    sends most neuron-steps through the global-scratch path; rasters stay
+    identical to the reference's."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    lib = os.path.join(ROOT, "paper_1803_08833_b200", "libcorticarc_b200_w4.so")
+    assert os.path.exists(lib), "run __graft_entry__.build() (builds the test variant)"
+    r = subprocess.run([sys.executable, "-c", _SPILL_CHECK.format(root=ROOT)],
+                       env={**os.environ, "CC_LIB_PATH": lib}, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    for name, v in out.items():
+        assert v["same"], name
+        assert v["spilled"] > 0, name
+
+
 def test_eager_equals_graph(cuda):
     from paper_1803_08833_b200.engine import run_b200
     cfg, meta, arr = golden_run("tiny_gauss_long")
