@@ -679,7 +679,8 @@ k_stage(const cc_shard sh) {
             }
             __syncwarp();
             // exact order inside shared buckets: rank among the bucket's inputs
-            // by (t, src), ties by staging index (identical inputs commute)
+            // by (t, src, w) like lexsort((w, src, tm, tgt)) (engine.py:386);
+            // ties by staging index (identical inputs commute)
             for (uint32_t e = lane; e < rtot; e += 32) {
                 const uint32_t kp = Ek[e];
                 const uint32_t h = B.hist[kp >> 16];
@@ -691,12 +692,18 @@ k_stage(const cc_shard sh) {
                 const uint32_t rel = e - (uint32_t)a;
                 const double te = Et[e];
                 const uint32_t se = Es[e];
+                const float we = Ew[e];
                 uint32_t rank = 0;
                 for (uint32_t q = s0; q < s0 + c; ++q) {
                     const uint32_t pq = Epv[q];
                     const double tq = Et[a + pq];
                     const uint32_t sq = Es[a + pq];
-                    rank += (tq < te || (tq == te && (sq < se || (sq == se && pq < rel)))) ? 1u : 0u;
+                    bool lt = tq < te;
+                    if (tq == te) {
+                        const float wq = Ew[a + pq];
+                        lt = sq < se || (sq == se && (wq < we || (wq == we && pq < rel)));
+                    }
+                    rank += lt ? 1u : 0u;
                 }
                 Ep[s0 + rank] = (uint16_t)rel;
             }

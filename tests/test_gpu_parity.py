@@ -226,6 +226,36 @@ def test_import_path_matches(cuda):
     assert a.raster_checksum == b.raster_checksum and a.n_spikes > 0
 
 
+def test_multapse_ties_follow_weight_order(cuda):
+    """Inputs equal in (t, src) - a duplicated synapse with the same delay and
+    a different weight - are applied in weight order like the reference's
+    lexsort((w, src, tm, tgt)); the two orders give different rasters here
+    (a large negative and a large positive weight)."""
+    from oracle import corticarc_oracle as O
+    from paper_1803_08833_b200.engine import run_b200
+    from paper_1803_08833_b200.network import import_csr
+    cfg = tiny_config(duration_s=0.15)
+    net = O.build_shard(cfg.grid, cfg.kernel, cfg.genspec, cfg.seed)
+    rows = np.repeat(np.arange(len(net.sources)), np.diff(net.offsets))
+    dup = np.arange(0, len(rows), 7)                  # every 7th synapse gets a twin
+    idx = np.sort(np.concatenate([np.arange(len(rows)), dup]), kind="stable")
+    is_twin = np.zeros(len(idx), bool)
+    is_twin[np.searchsorted(idx, dup, side="right") - 1] = True
+    w = net.weight[idx].copy()
+    w[is_twin] = np.float32(6.0)                      # twin: strong excitation
+    w[np.roll(is_twin, -1)] = np.float32(-6.0)        # original: strong inhibition
+    counts = np.bincount(rows[idx], minlength=len(net.sources))
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    mnet = O.ShardNet(net.sources, offs, net.target_local[idx], net.delay[idx], w, 0, len(idx))
+    ref = O.run_oracle(cfg, net=mnet)
+    dnet = import_csr(cfg, net.sources, offs, net.target_local[idx], net.delay[idx], w)
+    res = run_b200(cfg, 1, net=dnet)
+    assert ref.n_spikes > 0
+    assert np.array_equal(res.raster_gids, ref.raster_gids)
+    assert np.array_equal(res.raster_times.view(np.uint64), ref.raster_times.view(np.uint64))
+    assert res.recurrent_events == ref.recurrent_events
+
+
 def test_zero_duration_is_construction_only(cuda):
     from paper_1803_08833_b200.engine import run_b200
     res = run_b200(tiny_config(duration_s=0.0), 1)
