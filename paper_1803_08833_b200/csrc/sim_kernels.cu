@@ -389,7 +389,17 @@ k_plan(const cc_shard sh) {
     const uint32_t c_ovf = c_all > K ? (uint32_t)max(0ll, min((long long)(c_all - K), sh.ovf_cap - o0)) : 0u;
     __syncwarp();
     const uint64_t* lst = sh.bin_rec + ((size_t)slot * sh.n_groups + group) * K;
-    for (uint32_t r = lane; r < c_list; r += 32) atomicAdd(&lane_cnt[wib][(uint32_t)lst[r] & 31u], 1u);
+    for (uint32_t r0 = 0; r0 < c_list; r0 += 32 * 8) {
+        uint32_t v[8];                             // 8 loads in flight per lane
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t r = r0 + u * 32 + lane;
+            v[u] = r < c_list ? (uint32_t)lst[r] : 0xffffffffu;   // ref < 2^27: never all-ones
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (v[u] != 0xffffffffu) atomicAdd(&lane_cnt[wib][v[u] & 31u], 1u);
+    }
     const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + o0;
     for (uint32_t r = lane; r < c_ovf; r += 32) atomicAdd(&lane_cnt[wib][ov[r].y], 1u);
     __syncwarp();
@@ -501,6 +511,7 @@ k_stage(const cc_shard sh) {
     const int t_mod_l = (int)pos_mod(t, sh.log_slots);
     const uint32_t K = (uint32_t)sh.bin_cap;
     const double t0 = (double)t * sh.dt;
+    const double inv_dt = 1.0 / sh.dt;
     // queued items per size class (k_plan is complete); claimed largest first
     __shared__ unsigned cls_n[CC_ITEM_CLASSES];
     if (threadIdx.x < CC_ITEM_CLASSES)
@@ -638,16 +649,16 @@ k_stage(const cc_shard sh) {
             uint32_t nbt;
             const uint32_t cb = warp_excl_scan(nbl, nbt);
             B.cbk[lane] = cb | (nbl << 16);
-            B.bsc[lane] = (double)nbl / sh.dt;
+            B.bsc[lane] = (double)nbl * inv_dt;      // any monotone map of t will do
             __syncwarp();
             for (uint32_t i = lane; i < nbt; i += 32) B.hist[i] = 0u;
             __syncwarp();
             for (uint32_t e = lane; e < rtot; e += 32) {
                 const uint32_t o = Eo[e];
                 const uint32_t ck = B.cbk[o];
-                double x = (Et[e] - t0) * B.bsc[o];
-                x = fmin(fmax(x, 0.0), (double)((ck >> 16) - 1u));
-                const uint32_t key = (ck & 0xffffu) + (uint32_t)x;
+                const int b = min(max(__double2int_rz((Et[e] - t0) * B.bsc[o]), 0),
+                                  (int)(ck >> 16) - 1);
+                const uint32_t key = (ck & 0xffffu) + (uint32_t)b;
                 Ek[e] = (key << 16) | atomicAdd(&B.hist[key], 1u);
             }
             __syncwarp();
@@ -697,13 +708,13 @@ k_stage(const cc_shard sh) {
                 for (uint32_t q = s0; q < s0 + c; ++q) {
                     const uint32_t pq = Epv[q];
                     const double tq = Et[a + pq];
-                    const uint32_t sq = Es[a + pq];
-                    bool lt = tq < te;
-                    if (tq == te) {
+                    rank += tq < te ? 1u : 0u;
+                    if (tq == te && pq != rel) {        // rare: equal times
+                        const uint32_t sq = Es[a + pq];
                         const float wq = Ew[a + pq];
-                        lt = sq < se || (sq == se && (wq < we || (wq == we && pq < rel)));
+                        rank += (sq < se || (sq == se && (wq < we || (wq == we && pq < rel))))
+                                    ? 1u : 0u;
                     }
-                    rank += lt ? 1u : 0u;
                 }
                 Ep[s0 + rank] = (uint16_t)rel;
             }
