@@ -368,14 +368,21 @@ __device__ __forceinline__ void update_neuron(const cc_shard& sh, int li, uint32
 // to a global queue so that heavy groups are spread over many warps.
 __global__ void __launch_bounds__(128)
 k_plan(const cc_shard sh) {
+    const unsigned long long pt0 = gtimer();
     cc_ctl* ctl = sh.ctl;
     const long long t = *(volatile long long*)&ctl->t;
-    if (*(volatile unsigned*)&ctl->error_bits) return;      // failed run: stop working
+    // whole blocks stop once the run has failed (the block barriers below
+    // need every warp of a block, so no per-warp early exit)
+    __shared__ unsigned blk_err;
+    if (threadIdx.x == 0) blk_err = *(volatile unsigned*)&ctl->error_bits;
+    __syncthreads();
+    if (blk_err) return;
     const int lane = threadIdx.x & 31;
-    const int group = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int group0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const bool gvalid = group0 * 32 < sh.n_local;   // warps past the last group idle
+    const int group = gvalid ? group0 : 0;
     const int li = group * 32 + lane;
-    if (group * 32 >= sh.n_local) return;
-    const bool active = li < sh.n_local;
+    const bool active = gvalid && li < sh.n_local;
     const int slot = (int)pos_mod(t, sh.d_max);
     // inputs from the ring: count this slot's records of the group per lane
     __shared__ uint32_t lane_cnt[4][32];
@@ -383,7 +390,7 @@ k_plan(const cc_shard sh) {
     lane_cnt[wib][lane] = 0u;
     const uint32_t K = (uint32_t)sh.bin_cap;
     uint32_t* gc = sh.bin_cnt + (size_t)slot * sh.n_groups + group;
-    const uint32_t c_all = *gc;
+    const uint32_t c_all = gvalid ? *gc : 0u;
     const uint32_t c_list = min(c_all, K);
     const long long o0 = sh.ovf_off[group];
     const uint32_t c_ovf = c_all > K ? (uint32_t)max(0ll, min((long long)(c_all - K), sh.ovf_cap - o0)) : 0u;
@@ -403,10 +410,11 @@ k_plan(const cc_shard sh) {
     const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + o0;
     for (uint32_t r = lane; r < c_ovf; r += 32) atomicAdd(&lane_cnt[wib][ov[r].y], 1u);
     __syncwarp();
-    if (lane == 0) {
+    if (lane == 0 && gvalid) {
         sh.grp_n[group] = c_list + c_ovf;
         *gc = 0u;                                  // drain the ring slot (read back via grp_n)
     }
+    const unsigned long long pt1 = gtimer();
     uint32_t n_r = 0, n_e = 0;
     if (active) {
         const uint32_t gid = sh.gid[li];
@@ -417,17 +425,28 @@ k_plan(const cc_shard sh) {
             // product <= exp(-lambda) counts exactly the same terms.
             const uint64_t h4 = cc_splitmix64(cc_splitmix64(sh.h2_ext ^ (uint64_t)gid)
                                               ^ (uint64_t)t);
+            // uniforms 4 at a time (independent hashes), products in order
             double prod = 1.0;
-            int k = 0;
-            for (; k < sh.ext_budget; ++k) {
-                prod = prod * cc_u53(cc_splitmix64(h4 ^ (uint64_t)k));
-                if (!(prod > sh.ext_thresh)) break;
+            int k = sh.ext_budget;
+            for (int k0 = 0; k0 < sh.ext_budget; k0 += 4) {
+                double u[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) u[j] = cc_u53(cc_splitmix64(h4 ^ (uint64_t)(k0 + j)));
+                bool done = false;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (done || k0 + j >= sh.ext_budget) continue;
+                    prod = prod * u[j];
+                    if (!(prod > sh.ext_thresh)) { k = k0 + j; done = true; }
+                }
+                if (done) break;
             }
             if (k >= sh.ext_budget) cc_raise(ctl, CC_ERR_POISSON, t);
             n_e = (uint32_t)k;
         }
     }
     const uint32_t n = n_r + n_e;
+    const unsigned long long pt2 = gtimer();
     uint32_t nmax = n;
     unsigned long long es = n_e;
     uint32_t mb = n_r;
@@ -442,55 +461,85 @@ k_plan(const cc_shard sh) {
         sh.ev_n[li] = (int32_t)n;
         sh.ev_nr[li] = (int32_t)n_r;
     }
-    // greedy split of lanes 0..31 into rounds of <= NEURON_WCAP inputs; lane 0
-    // walks the 32 counts (cheap, through shared memory).  Items are queued by
-    // size class, largest first, so that the last items claimed are short.
-    const unsigned has = __ballot_sync(0xffffffffu, ok && n > 0);
-    __shared__ uint32_t cnts[4][32];
-    __shared__ uint32_t itm[4][32], itt[4][32];
-    cnts[wib][lane] = (ok && active) ? n : 0u;
-    __syncwarp();
-    int ni = 0;
-    if (lane == 0 && has) {
-        int l0 = -1;
-        uint32_t tot = 0;
-        for (int l = 0; l < 32; ++l) {
-            const uint32_t nl = cnts[wib][l];
-            if (nl == 0) continue;
-            if (l0 >= 0 && tot + nl > (uint32_t)NEURON_WCAP) {
-                itm[wib][ni] = (uint32_t)l0 | ((uint32_t)l << 8);
-                itt[wib][ni++] = tot;
-                l0 = -1;
-            }
-            if (l0 < 0) { l0 = l; tot = 0; }
-            tot += nl;
+    // greedy split of lanes 0..31 into items of <= NEURON_WCAP inputs (a lane
+    // with more forms an item alone), warp-parallel: lane s finds by binary
+    // search the first lane e > s whose inclusive prefix exceeds
+    // prefix(s - 1) + NEURON_WCAP; the items are the chain first, e(first), ...
+    // Items are queued by size class, largest first, so that the last items
+    // claimed are short.
+    const uint32_t nn = active ? n : 0u;
+    uint32_t gtot;
+    const uint32_t excl = warp_excl_scan(nn, gtot);
+    const uint32_t incl = excl + nn;
+    const uint32_t thr = excl + (uint32_t)NEURON_WCAP;
+    int lo = lane + 1, hi = 32;
+#pragma unroll
+    for (int it = 0; it < 6; ++it) {
+        const int mid = (lo + hi) >> 1;
+        const uint32_t pm = __shfl_sync(0xffffffffu, incl, mid & 31);
+        if (lo < hi) {
+            if (pm > thr) hi = mid; else lo = mid + 1;
         }
-        if (l0 >= 0) {
-            itm[wib][ni] = (uint32_t)l0 | (32u << 8);
-            itt[wib][ni++] = tot;
-        }
-        atomicAdd(&ctl->n_rounds, (unsigned)ni);
     }
-    ni = __shfl_sync(0xffffffffu, ni, 0);
-    if (lane == 0) sh.grp_items[group] = (uint32_t)ni;
-    __syncwarp();
+    const unsigned has = __ballot_sync(0xffffffffu, nn > 0);
+    int ni = 0;
+    uint32_t my_item = 0, my_tot = 0;
+    for (int st = has ? __ffs(has) - 1 : 32; st < 32; ++ni) {
+        const int en = __shfl_sync(0xffffffffu, lo, st);
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, en - 1)
+                             - __shfl_sync(0xffffffffu, excl, st);
+        if (lane == ni) { my_item = (uint32_t)st | ((uint32_t)en << 8); my_tot = tot; }
+        st = en;
+    }
+    const unsigned long long pt3 = gtimer();
+    if (lane == 0 && gvalid) sh.grp_items[group] = (uint32_t)ni;
+    // queue positions: per-block counts per class, one global atomic per class
+    __shared__ unsigned blk_cls[CC_ITEM_CLASSES], blk_base[CC_ITEM_CLASSES];
+    __shared__ unsigned long long blk_es;
+    __shared__ unsigned blk_ni, blk_mb, blk_nmax;
+    if (threadIdx.x < CC_ITEM_CLASSES) blk_cls[threadIdx.x] = 0u;
+    if (threadIdx.x == 0) { blk_es = 0ull; blk_ni = 0u; blk_mb = 0u; blk_nmax = 0u; }
+    __syncthreads();
+    int cls = 0;
+    unsigned local = 0;
     if (lane < ni) {
-        const uint32_t tot = itt[wib][lane];
-        const int c = tot >= (uint32_t)NEURON_WCAP
-                          ? 0 : CC_ITEM_CLASSES - 1 - (int)(tot * CC_ITEM_CLASSES / NEURON_WCAP);
-        const unsigned at = atomicAdd(&ctl->cls_n[c], 1u);
+        cls = my_tot >= (uint32_t)NEURON_WCAP
+                  ? 0 : CC_ITEM_CLASSES - 1 - (int)(my_tot * CC_ITEM_CLASSES / NEURON_WCAP);
+        local = atomicAdd(&blk_cls[cls], 1u);
+    }
+    if (lane == 0) {
+        if (ni) atomicAdd(&blk_ni, (unsigned)ni);
+        if (es) atomicAdd(&blk_es, es);
+        if (mb) atomicMax(&blk_mb, mb);
+        if (nmax) atomicMax(&blk_nmax, nmax);
+    }
+    __syncthreads();
+    if (threadIdx.x < CC_ITEM_CLASSES && blk_cls[threadIdx.x])
+        blk_base[threadIdx.x] = atomicAdd(&ctl->cls_n[threadIdx.x], blk_cls[threadIdx.x]);
+    if (threadIdx.x == 0) {
+        if (blk_ni) atomicAdd(&ctl->n_rounds, blk_ni);
+        if (blk_es) atomicAdd(&ctl->ext_events, blk_es);
+        if (blk_mb) atomicMax(&ctl->max_bin, blk_mb);
+        if (blk_nmax) atomicMax(&ctl->max_events, blk_nmax);
+    }
+    __syncthreads();
+    if (lane < ni) {
+        const unsigned at = blk_base[cls] + local;
         if (at >= (unsigned)sh.round_cap) {
             cc_raise(ctl, CC_ERR_SCRATCH, t);
         } else {
-            uint32_t* r = sh.rounds + 2 * ((size_t)c * sh.round_cap + at);
+            uint32_t* r = sh.rounds + 2 * ((size_t)cls * sh.round_cap + at);
             r[0] = (uint32_t)group;
-            r[1] = itm[wib][lane];
+            r[1] = my_item;
         }
     }
-    if (lane == 0) {
-        if (es) atomicAdd(&ctl->ext_events, es);
-        if (mb) atomicMax(&ctl->max_bin, mb);
-        if (nmax) atomicMax(&ctl->max_events, nmax);
+    if ((sh.debug_skip & 512) && lane == 0 && gvalid) {
+        unsigned long long* d_ = reinterpret_cast<unsigned long long*>(sh.scratch)
+                                 + (size_t)sh.scratch_cap * 7 - (size_t)(group + 1) * 8;
+        unsigned smid_;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid_));
+        d_[0] = pt0; d_[1] = pt1; d_[2] = pt2; d_[3] = pt3; d_[4] = gtimer();
+        d_[5] = smid_; d_[6] = c_all; d_[7] = (unsigned long long)ni;
     }
 }
 
