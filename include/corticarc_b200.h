@@ -140,7 +140,7 @@ typedef struct cc_shard {
     float* scratch;         /* [scratch_cap][14] spill staging (56 B per event) */
     int32_t* ev_n;          /* [n_local] events staged for each neuron          */
     int32_t* ev_nr;         /* [n_local] of which recurrent                     */
-    /* ordered inputs of the step, one 48 B record {t, w, em, ec, f, 0} each,
+    /* ordered inputs of the step, one 48 B record {t, w, em, ec, f, ecr} each,
      * written by the staging warps and consumed by the group's in-order update */
     double* evrec;          /* [evrec_cap][6]                                    */
     int64_t evrec_cap;

@@ -249,14 +249,16 @@ __device__ __forceinline__ int neuron_pop(const cc_shard& sh, uint32_t gid) {
 }
 
 // General (rare) step of the in-order update: refractory window involved or
-// factors invalidated by an earlier spike in this step.  Out of line to keep
-// the hot loop small.  Returns true when the strict threshold is crossed.
+// factors invalidated by an earlier spike in this step.  Returns true when the
+// strict threshold is crossed.  ecr0 = exp(-(ff - last) / tau_c) as staged
+// (valid unless stale, like em0, ec0, f0).
 __device__ __forceinline__ bool slow_step(NState& s, const cc_pop& P, double tj, bool stale,
-                                       bool cflag, double em0, double ec0, double f0, double w) {
+                                       bool cflag, double em0, double ec0, double f0,
+                                       double ecr0, double w) {
     const double ff = fmin(fmax(s.last, s.ru), tj);
     double cs = s.c;
     if (ff != s.last && cs != 0.0)                    // leaving / inside a refractory window
-        cs = cs * exp(-(ff - s.last) / P.tau_c);
+        cs = cs * (stale ? exp(-(ff - s.last) / P.tau_c) : ecr0);
     double emj = em0, ecj = ec0, fj = f0;
     if (stale) decay_factors(P, tj - ff, cs != 0.0, emj, ecj, fj);
     else if (!cflag) { ecj = 1.0; fj = 0.0; }
@@ -292,8 +294,8 @@ struct Recs {
         r0 = __ldcg(R); r1 = __ldcg(R + 1); r2 = __ldcg(R + 2);
     }
     __device__ __forceinline__ void fetch(uint32_t i, double& tj, double& wv, double& em,
-                                          double& ec, double& f) {
-        tj = r0.x; wv = r0.y; em = r1.x; ec = r1.y; f = r2.x;
+                                          double& ec, double& f, double& ecr) {
+        tj = r0.x; wv = r0.y; em = r1.x; ec = r1.y; f = r2.x; ecr = r2.y;
         if (i + 1 < n) {
             r0 = __ldcg(R + 3 * (i + 1));
             r1 = __ldcg(R + 3 * (i + 1) + 1);
@@ -318,8 +320,8 @@ __device__ __forceinline__ void update_neuron(const cc_shard& sh, int li, uint32
     const bool cflag = s.c != 0.0;
     bool stale = false;                      // spiked: factors need recomputing
     for (uint32_t i = 0; i < n; ++i) {
-        double tj, wv, em, ec, f;
-        src.fetch(i, tj, wv, em, ec, f);
+        double tj, wv, em, ec, f, ecr;
+        src.fetch(i, tj, wv, em, ec, f, ecr);
         bool spike = false;
         if (!stale && s.ru <= s.last) {
             // fast path (no refractory window involved, factors valid):
@@ -334,7 +336,7 @@ __device__ __forceinline__ void update_neuron(const cc_shard& sh, int li, uint32
             const double V = Vt + wv;
             if (V > P.V_theta) spike = true; else s.V = V;
         } else {
-            spike = slow_step(s, P, tj, stale, cflag, em, ec, f, wv);
+            spike = slow_step(s, P, tj, stale, cflag, em, ec, f, ecr, wv);
         }
         if (spike) {                             // strict threshold crossed
             s.V = P.V_r;
@@ -793,11 +795,14 @@ k_stage(const cc_shard sh) {
                 const uint32_t fl = B.o_flag[o];
                 const double ff = fmin(fmax(last, ru), te);
                 double em, ec, f;
-                decay_factors(sh.pop[fl & 1u], te - ff, (fl & 2u) != 0, em, ec, f);
+                const cc_pop& P = sh.pop[fl & 1u];
+                decay_factors(P, te - ff, (fl & 2u) != 0, em, ec, f);
+                // fatigue decay over the refractory part of the gap (slow_step)
+                const double ecr = (ff != last && (fl & 2u)) ? exp(-(ff - last) / P.tau_c) : 1.0;
                 const double wv = (Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
                 R[3 * p] = make_double2(te, wv);
                 R[3 * p + 1] = make_double2(em, ec);
-                R[3 * p + 2] = make_double2(f, 0.0);
+                R[3 * p + 2] = make_double2(f, ecr);
             }
         }
         if (go) sh.ev_off[li] = (int32_t)(rbase + roff);
