@@ -467,8 +467,8 @@ k_plan(const cc_shard sh) {
     // with more forms an item alone), warp-parallel: lane s finds by binary
     // search the first lane e > s whose inclusive prefix exceeds
     // prefix(s - 1) + NEURON_WCAP; the items are the chain first, e(first), ...
-    // Items are queued by size class, largest first, so that the last items
-    // claimed are short.
+    // Items are queued by the size class of their group, heaviest first, so
+    // that the last items claimed (and group updates run) are short.
     const uint32_t nn = active ? n : 0u;
     uint32_t gtot;
     const uint32_t excl = warp_excl_scan(nn, gtot);
@@ -505,8 +505,10 @@ k_plan(const cc_shard sh) {
     int cls = 0;
     unsigned local = 0;
     if (lane < ni) {
-        cls = my_tot >= (uint32_t)NEURON_WCAP
-                  ? 0 : CC_ITEM_CLASSES - 1 - (int)(my_tot * CC_ITEM_CLASSES / NEURON_WCAP);
+        // class by the GROUP's input total: all items of a heavy group are
+        // claimed early, so its (long) in-order update does not start last
+        cls = CC_ITEM_CLASSES - 1 - (int)min(gtot / (uint32_t)NEURON_WCAP,
+                                             (uint32_t)(CC_ITEM_CLASSES - 1));
         local = atomicAdd(&blk_cls[cls], 1u);
     }
     if (lane == 0) {
