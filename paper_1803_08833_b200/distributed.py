@@ -29,7 +29,7 @@ from typing import List, Optional, Tuple
 import numpy as np
 
 __all__ = ["SpikeExchange", "dest_masks_from_rows", "DistributedSimulator",
-           "run_multi_gpu", "bench_distributed", "ProtocolViolation"]
+           "run_multi_gpu", "bench_distributed", "ProtocolViolation", "run_local_shards"]
 
 
 class ProtocolViolation(RuntimeError):
@@ -168,6 +168,86 @@ class DistributedSimulator:
             self.step()
             if (i + 1) % check_every == 0 or i == n_steps - 1:
                 self.sim.check()
+
+
+def run_local_shards(config, size: int, device=None):
+    """All `size` shards of a multi-GPU run, stepped in turn on ONE device.
+
+    Same shard code as run_multi_gpu - per-rank generator (build_b200 rank /
+    size), exchange-mode neuron step (out-list), cc_ingest - with the AER
+    exchange done in-process: destination d receives, in source-rank order,
+    the spikes whose source has a row on d (SpikeExchange semantics).  No
+    kernel waits on another shard's kernel.  Used to test partition invariance
+    of the CUDA path on a single B200 (tests/test_gpu_parity.py)."""
+    import torch
+    from . import _lib
+    from .engine import RunResult, Simulator, raster_checksum
+    from .network import build_b200
+    dev = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+    nets = [build_b200(config, rank=r, size=size, device=dev) for r in range(size)]
+    sims = [Simulator(config, nets[r], direct_log=False, use_graphs=False, device=dev)
+            for r in range(size)]
+    has = [((n.row_off[1:] - n.row_off[:-1]) > 0).cpu().numpy() for n in nets]
+    n_col = config.grid.neurons_per_column
+    masks, luts = [], []
+    for r in range(size):
+        masks.append(torch.as_tensor(dest_masks_from_rows(has, sims[r].gids), device=dev))
+        lut = np.full(config.grid.n_columns, -1, np.int64)
+        lut[nets[r].owned_columns] = np.arange(len(nets[r].owned_columns))
+        luts.append(torch.as_tensor(lut, device=dev))
+    n_in = torch.zeros(1, dtype=torch.int32, device=dev)
+    off = _lib.Ctl.out_n.offset
+    stream = torch.cuda.current_stream(dev)
+    t0 = time.perf_counter()
+    for step in range(config.n_steps):
+        out = []
+        for r, sim in enumerate(sims):
+            sim._launch_step(stream.cuda_stream)
+        torch.cuda.synchronize(dev)
+        for r, sim in enumerate(sims):
+            k = int(sim.ctl().out_n)
+            g = sim.buf["out_gid"][:k].long() & 0xFFFFFFFF
+            li = luts[r][g // n_col] * n_col + g % n_col
+            out.append((g, sim.buf["out_t"][:k].clone(), masks[r][li] if k else g))
+            sim.buf["ctl"].view(torch.uint8)[off:off + 4].zero_()
+        for d, sim in enumerate(sims):
+            gs, ts = [], []
+            for g, tm, m in out:
+                if g.numel():
+                    sel = ((m >> d) & 1).bool()
+                    gs.append(g[sel])
+                    ts.append(tm[sel])
+            in_g = torch.cat(gs).to(torch.int32) if gs else torch.zeros(0, dtype=torch.int32,
+                                                                        device=dev)
+            in_t = torch.cat(ts) if ts else torch.zeros(0, dtype=torch.float64, device=dev)
+            n_in.fill_(int(in_g.numel()))
+            _lib.check(sim.L.cc_ingest(C.byref(sim.shard), in_g.data_ptr() if in_g.numel() else 0,
+                                       in_t.data_ptr() if in_t.numel() else 0, n_in.data_ptr(),
+                                       stream.cuda_stream), "cc_ingest")
+            torch.cuda.synchronize(dev)
+        if (step + 1) % 100 == 0 or step == config.n_steps - 1:
+            for sim in sims:
+                sim.check()
+    wall = time.perf_counter() - t0
+    ctls = [sim.ctl() for sim in sims]
+    parts = [sim.raster() for sim in sims]
+    g = np.concatenate([p[0] for p in parts]) if parts else np.empty(0, np.uint64)
+    t = np.concatenate([p[1] for p in parts]) if parts else np.empty(0)
+    o = np.lexsort((g, t))
+    g, t = g[o], t[o]
+    return RunResult(
+        config=config, worker_count=size, raster_gids=g, raster_times=t,
+        n_spikes=sum(int(c.n_spikes) for c in ctls),
+        recurrent_events=sum(int(c.rec_events) for c in ctls),
+        external_events=sum(int(c.ext_events) for c in ctls),
+        recurrent_synapses=sum(n.n_synapses for n in nets),
+        construction_checksum=sum(n.checksum for n in nets) % 2 ** 64,
+        raster_checksum=raster_checksum(g, t),
+        construction_seconds=max(n.construction_seconds for n in nets),
+        sim_seconds_wall=wall,
+        substep_seconds={"deliver": 0.0, "expand": 0.0, "external": 0.0, "integrate": wall},
+        steady_bytes_per_worker=[n.steady_bytes for n in nets],
+        peak_bytes_per_worker=[n.peak_bytes for n in nets])
 
 
 def _init_dist():

@@ -276,6 +276,18 @@ def test_event_bookkeeping_matches_fanout(cuda):
     assert res.recurrent_events == int((row_off[g + 1] - row_off[g]).sum())
 
 
+@pytest.mark.parametrize("name,size", [("tiny_gauss", 2), ("tiny_gauss", 4), ("tiny_exp", 2),
+                                       ("config0_cal_0p1", 4)])
+def test_partition_invariance_on_one_gpu(cuda, name, size):
+    """W shards (per-rank generator, exchange-mode neuron step, AER exchange,
+    cc_ingest) stepped on one B200 give the reference raster (acceptance #4,
+    SURVEY 8(e))."""
+    from paper_1803_08833_b200.distributed import run_local_shards
+    cfg, meta, arr = golden_run(name)
+    res = run_local_shards(cfg, size)
+    _assert_same_run(res, meta, arr)
+
+
 def test_exchange_mode_single_rank_matches_reference(cuda):
     """The multi-GPU code path (spike out-list -> NCCL all-to-all-v ->
     cc_ingest) on a one-rank NCCL group reproduces the reference raster."""
