@@ -182,6 +182,11 @@ int cc_init_state(const cc_shard* sh, void* stream);
  * (engine.py:138-149). */
 int cc_deliver(const cc_shard* sh, void* stream);
 
+/* One-time launch configuration of the step kernels (shared-memory opt-in,
+ * persistent grid size).  Call once before capturing steps into a CUDA graph;
+ * cc_neuron_step calls it itself otherwise. */
+int cc_prepare(void);
+
 /* Step phases (4)-(6): drain the ring slot of step t, generate the external
  * Poisson events, order each neuron's inputs by (time, source, weight) and
  * integrate them exactly; emit spikes.  Increments ctl->t.

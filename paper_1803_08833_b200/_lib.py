@@ -108,6 +108,7 @@ _SIGS = {
     "cc_timer_destroy": (C.c_int, [C.c_void_p]),
     "cc_init_state": (C.c_int, [C.POINTER(Shard), _P]),
     "cc_deliver": (C.c_int, [C.POINTER(Shard), _P]),
+    "cc_prepare": (C.c_int, []),
     "cc_neuron_step": (C.c_int, [C.POINTER(Shard), _P]),
     "cc_ingest": (C.c_int, [C.POINTER(Shard), _P, _P, _P, _P]),
     "cc_pack_outgoing": (C.c_int, [C.POINTER(Shard), _P, C.c_int32, C.c_int32, _P, _P, _P,

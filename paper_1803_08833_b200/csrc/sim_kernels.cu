@@ -1129,6 +1129,22 @@ extern "C" int cc_deliver(const cc_shard* sh, void* stream) {
     return cc_check_launch("k_deliver");
 }
 
+// One-time kernel attributes and the persistent grid size (not capturable in
+// a CUDA graph, so done here or on the first eager cc_neuron_step).
+static int stage_blocks = 0;
+
+extern "C" int cc_prepare(void) {
+    if (stage_blocks) return 0;
+    const size_t smem = stage_warp_bytes() * STAGE_WARPS;
+    if (cudaFuncSetAttribute(k_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+        != cudaSuccess)
+        return cc_set_error("cc_prepare: %s", cudaGetErrorString(cudaGetLastError()));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage, 32 * STAGE_WARPS, smem);
+    stage_blocks = sm_count() * (per_sm > 0 ? per_sm : 1);
+    return 0;
+}
+
 extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_neuron_step: null shard");
     if (sh->n_local <= 0) return cc_set_error("cc_neuron_step: empty shard");
@@ -1136,13 +1152,7 @@ extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
     k_plan<<<(groups + 3) / 4, 128, 0, (cudaStream_t)stream>>>(*sh);
     if (const int rc = cc_check_launch("k_plan")) return rc;
     const size_t smem = stage_warp_bytes() * STAGE_WARPS;
-    static int stage_blocks = 0;
-    if (!stage_blocks) {
-        cudaFuncSetAttribute(k_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage, 32 * STAGE_WARPS, smem);
-        stage_blocks = sm_count() * (per_sm > 0 ? per_sm : 1);
-    }
+    if (const int rc = cc_prepare()) return rc;
     k_stage<<<stage_blocks, 32 * STAGE_WARPS, smem, (cudaStream_t)stream>>>(*sh);
     if (const int rc = cc_check_launch("k_stage")) return rc;
     if (sh->n_probe > 0) {

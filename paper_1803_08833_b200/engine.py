@@ -130,7 +130,7 @@ class Simulator:
     def __init__(self, cfg, net: DeviceNetwork, *, probes=None, probe_steps: int = 0,
                  bin_cap: Optional[int] = None, piece_len: int = 256, chunk: int = 100,
                  use_graphs: bool = True, direct_log: Optional[bool] = None,
-                 raster_steps: Optional[int] = None, device=None):
+                 raster_steps: Optional[int] = None, substeps: bool = False, device=None):
         import torch
         self.L = _lib.lib()
         self.torch = torch
@@ -248,12 +248,19 @@ class Simulator:
         self.n_local = n_local
         self._graph = None
         self._graph_steps = 0
+        # per-kernel device time of graph-replayed chunks (RunResult.substep_seconds)
+        self.substeps = substeps
+        self._timer = None
+        self.kernel_ms = dict(deliver=0.0, neuron=0.0, steps=0)
         self.t = 0
         self.raster_g: List[np.ndarray] = []
         self.raster_t: List[np.ndarray] = []
         self.device_bytes = sum(x.numel() * x.element_size() for x in b.values())
         stream = torch.cuda.current_stream(dev).cuda_stream
         _lib.check(self.L.cc_init_state(C.byref(sh), stream), "cc_init_state")
+        _lib.check(self.L.cc_prepare(), "cc_prepare")
+        if use_graphs:                     # capture once, outside any timed region
+            self._capture(self.chunk, torch.cuda.Stream(dev))
 
     # ------------------------------------------------------------------ steps
     def _launch_step(self, stream) -> None:
@@ -280,13 +287,41 @@ class Simulator:
         return c
 
     def _capture(self, steps: int, stream_obj) -> None:
+        """The chunk graph; with substep timing, event-record nodes before and
+        after each step's delivery (2 per step + 1 at the end)."""
         torch = self.torch
+        if self.substeps and self._timer is None:
+            self._timer = C.c_void_p()
+            _lib.check(self.L.cc_timer_create(2 * steps + 1, C.byref(self._timer)))
+        tm = self._timer if self.substeps else None
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream_obj):
             s = torch.cuda.current_stream(self.dev).cuda_stream
-            for _ in range(steps):
-                self._launch_step(s)
+            for i in range(steps):
+                if tm is not None:
+                    _lib.check(self.L.cc_timer_record(tm, 2 * i, s))
+                _lib.check(self.L.cc_deliver(C.byref(self.shard), s), "cc_deliver")
+                if tm is not None:
+                    _lib.check(self.L.cc_timer_record(tm, 2 * i + 1, s))
+                _lib.check(self.L.cc_neuron_step(C.byref(self.shard), s), "cc_neuron_step")
+            if tm is not None:
+                _lib.check(self.L.cc_timer_record(tm, 2 * steps, s))
         self._graph, self._graph_steps = g, steps
+
+    def _read_substeps(self, steps: int) -> None:
+        el = self.L.cc_timer_elapsed_ms
+        d = sum(el(self._timer, 2 * i, 2 * i + 1) for i in range(steps))
+        n = sum(el(self._timer, 2 * i + 1, 2 * i + 2) for i in range(steps))
+        self.kernel_ms["deliver"] += d
+        self.kernel_ms["neuron"] += n
+        self.kernel_ms["steps"] += steps
+
+    def __del__(self):
+        try:
+            if self._timer is not None:
+                self.L.cc_timer_destroy(self._timer)
+        except Exception:
+            pass
 
     def capture(self, steps: int, timer=None, timer_base: int = 0):
         """A CUDA graph of `steps` steps; with a timer (cc_timer_create handle)
@@ -313,17 +348,21 @@ class Simulator:
         done = 0
         while done < n_steps:
             k = min(self.chunk, n_steps - done)
-            if self.use_graphs and k == self.chunk and self.t > 0:
+            if self.use_graphs and k == self.chunk:
                 if self._graph is None or self._graph_steps != k:
                     self._capture(k, torch.cuda.Stream(self.dev))
                 self._graph.replay()
+                timed = self.substeps
             else:
                 s = torch.cuda.current_stream(self.dev).cuda_stream
                 for _ in range(k):
                     self._launch_step(s)
+                timed = False
             self.t += k
             done += k
             self.check(collect_raster)
+            if timed:
+                self._read_substeps(k)
 
     def raster(self):
         g = np.concatenate(self.raster_g) if self.raster_g else np.empty(0, np.uint64)
@@ -336,6 +375,20 @@ class Simulator:
             return None, None
         p = self.buf["probe_out"][:steps].cpu().numpy()
         return p[:, :, :4].copy(), p[:, :, 4].copy()
+
+
+def _substeps(sim, n_steps: int, wall: float) -> dict:
+    """RunResult.substep_seconds (engine.py:251-275 keys): expand = delivery
+    kernel, integrate = neuron step (Poisson drive, sort and update are one
+    kernel pair, so external is folded into it), deliver = spike exchange
+    (none on one GPU).  Device time of the graph-replayed chunks (CUDA event
+    nodes), scaled to all steps; without any, the wall goes to integrate."""
+    km = sim.kernel_ms
+    if not km["steps"]:
+        return {"deliver": 0.0, "expand": 0.0, "external": 0.0, "integrate": wall}
+    scale = n_steps / km["steps"] / 1e3
+    return {"deliver": 0.0, "expand": km["deliver"] * scale, "external": 0.0,
+            "integrate": km["neuron"] * scale}
 
 
 def run_b200(config, workers: int = 1, *, net: Optional[DeviceNetwork] = None, probes=None,
@@ -358,7 +411,7 @@ def run_b200(config, workers: int = 1, *, net: Optional[DeviceNetwork] = None, p
         net = build_b200(config, device=device)
     n_steps = config.n_steps if steps is None else steps
     sim = Simulator(config, net, probes=probes, probe_steps=n_steps, bin_cap=bin_cap,
-                    chunk=chunk, use_graphs=use_graphs, device=device)
+                    chunk=chunk, use_graphs=use_graphs, substeps=True, device=device)
     torch.cuda.synchronize(sim.dev)
     t0 = time.perf_counter()
     sim.advance(n_steps)
@@ -372,7 +425,7 @@ def run_b200(config, workers: int = 1, *, net: Optional[DeviceNetwork] = None, p
         external_events=int(c.ext_events), recurrent_synapses=net.n_synapses,
         construction_checksum=net.checksum, raster_checksum=raster_checksum(g, t),
         construction_seconds=net.construction_seconds, sim_seconds_wall=wall,
-        substep_seconds={"deliver": 0.0, "expand": 0.0, "external": 0.0, "integrate": wall},
+        substep_seconds=_substeps(sim, n_steps, wall),
         steady_bytes_per_worker=[net.steady_bytes], peak_bytes_per_worker=[net.peak_bytes],
         probe_state=ps, probe_v_end=pv,
         device_stats=dict(max_bin=int(c.max_bin), max_events=int(c.max_events),

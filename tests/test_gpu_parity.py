@@ -147,6 +147,11 @@ def test_config0_one_second_matches_reference(cuda, name):
     cfg, meta, arr = golden_run(name)
     res = run_b200(cfg, 1)
     _assert_same_run(res, meta, arr)
+    # substep keys of the reference (test_engine.py:230-234), device-timed here
+    sub = res.substep_seconds
+    assert set(sub) >= {"deliver", "expand", "external", "integrate"}
+    assert sub["expand"] > 0 and sub["integrate"] > 0
+    assert sub["expand"] + sub["integrate"] < 2 * res.sim_seconds_wall
 
 
 def test_overflow_path_same_raster(cuda):
