@@ -929,7 +929,13 @@ __device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
 }
 
 // One warp per delivery piece (<= piece_len synapses of one spiking source).
-__global__ void __launch_bounds__(512, 2)
+#ifndef CC_DEL_THREADS
+#define CC_DEL_THREADS 256
+#endif
+#ifndef CC_DEL_MINB
+#define CC_DEL_MINB 3
+#endif
+__global__ void __launch_bounds__(CC_DEL_THREADS, CC_DEL_MINB)
 k_deliver(const cc_shard sh) {
     const unsigned long long dbg_t0 = gtimer();
     cc_ctl* ctl = sh.ctl;
@@ -959,63 +965,91 @@ k_deliver(const cc_shard sh) {
     const uint8_t* __restrict__ d_a = sh.syn_d;
     unsigned long long events = 0;
     const unsigned long long dbg_t1 = gtimer();
-    for (long long p = wid; p < (long long)n_pieces; p += nw) {
-        const uint4 pc = pcs[p];
-        const size_t s0 = (size_t)pc.x | ((size_t)pc.y << 32);
+    // Software pipeline over 128-synapse units of this warp's pieces (p = wid,
+    // wid + nw, ...): the next unit's descriptor and CSR loads are issued
+    // before the current unit's reservations and deposits.
+    constexpr int U = 4;
+    const long long np_ = (long long)n_pieces;
+    long long p = wid;
+    uint4 pc = p < np_ ? pcs[p] : make_uint4(0, 0, 0, 0);
+    long long pn = p + nw;
+    uint4 pcn = pn < np_ ? pcs[pn] : make_uint4(0, 0, 0, 0);
+    int j0 = 0;
+    int tg[U], sl[U];
+    float w[U];
+    auto load_unit = [&](const uint4& q, int jb, int* tg_, int* sl_, float* w_) {
+        const size_t b0 = (size_t)q.x | ((size_t)q.y << 32);
+        const int cnt = (int)q.w;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = jb + u * 32 + lane;
+            sl_[u] = -1;
+            if (j < cnt) {
+                const size_t si = b0 + j;
+                tg_[u] = __ldg(tgt_a + si);
+                w_[u] = __ldg(w_a + si);
+                const int s = base + (int)__ldg(d_a + si);
+                sl_[u] = s >= D ? s - D : s;
+            }
+        }
+    };
+    if (p < np_) load_unit(pc, 0, tg, sl, w);
+    while (p < np_) {
+        // next unit: rest of this piece, else the next piece of this warp
+        long long p2 = p;
+        uint4 pc2 = pc;
+        int j2 = j0 + 32 * U;
+        const bool adv = j2 >= (int)pc.w;
+        if (adv) { p2 = pn; pc2 = pcn; j2 = 0; }
+        int tg2[U], sl2[U];
+        float w2[U];
+        if (p2 < np_) load_unit(pc2, j2, tg2, sl2, w2);
+        else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) sl2[u] = -1;
+        }
+        if (adv) {
+            pn = p2 + nw;
+            if (pn < np_) pcn = pcs[pn];
+        }
+        if (j0 == 0) events += (unsigned long long)pc.w;
         const uint32_t ref = pc.z;
-        const int cnt = (int)pc.w;
-        events += (unsigned long long)cnt;
-        constexpr int U = 8;                    // a whole 256-synapse piece in one round trip
-        for (int j0 = 0; j0 < cnt; j0 += 32 * U) {
-            int tg[U], sl[U];
-            float w[U];
+        // one atomic per (slot, group) run of lanes: warp-aggregated reservation
+        unsigned key[U], peers[U], pos[U], got[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int j = j0 + u * 32 + lane;
-                sl[u] = -1;
-                if (j < cnt) {
-                    const size_t si = s0 + j;
-                    tg[u] = __ldg(tgt_a + si);
-                    w[u] = __ldg(w_a + si);
-                    int s = base + (int)__ldg(d_a + si);
-                    sl[u] = s >= D ? s - D : s;
-                }
-            }
-            // one atomic per (slot, group) run of lanes: warp-aggregated reservation
-            unsigned key[U], peers[U], pos[U];
-            unsigned got[U];
+        for (int u = 0; u < U; ++u) {
+            key[u] = sl[u] >= 0 ? (unsigned)(sl[u] * NG + (tg[u] >> 5)) : 0xffffffffu;
+            peers[u] = __match_any_sync(0xffffffffu, key[u]);
+            got[u] = 0u;
+            if (sl[u] >= 0 && lane == __ffs(peers[u]) - 1)
+                got[u] = atomicAdd(&sh.bin_cnt[key[u]], (unsigned)__popc(peers[u]));
+        }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                key[u] = sl[u] >= 0 ? (unsigned)(sl[u] * NG + (tg[u] >> 5)) : 0xffffffffu;
-                peers[u] = __match_any_sync(0xffffffffu, key[u]);
-                got[u] = 0u;
-                if (sl[u] >= 0 && lane == __ffs(peers[u]) - 1)
-                    got[u] = atomicAdd(&sh.bin_cnt[key[u]], (unsigned)__popc(peers[u]));
-            }
+        for (int u = 0; u < U; ++u) {
+            pos[u] = __shfl_sync(0xffffffffu, got[u], __ffs(peers[u]) - 1)
+                     + __popc(peers[u] & ((1u << lane) - 1u));
+        }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                pos[u] = __shfl_sync(0xffffffffu, got[u], __ffs(peers[u]) - 1)
-                         + __popc(peers[u] & ((1u << lane) - 1u));
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (sl[u] < 0) continue;
-                const uint32_t lig = (uint32_t)tg[u] & 31u;
-                if (pos[u] < (unsigned)K) {
-                    sh.bin_rec[(size_t)key[u] * K + pos[u]] =
-                        (uint64_t)((ref << 5) | lig) | ((uint64_t)__float_as_uint(w[u]) << 32);
+        for (int u = 0; u < U; ++u) {
+            if (sl[u] < 0) continue;
+            const uint32_t lig = (uint32_t)tg[u] & 31u;
+            if (pos[u] < (unsigned)K) {
+                sh.bin_rec[(size_t)key[u] * K + pos[u]] =
+                    (uint64_t)((ref << 5) | lig) | ((uint64_t)__float_as_uint(w[u]) << 32);
+            } else {
+                const unsigned o = atomicAdd(&sh.ovf_cnt[sl[u]], 1u);
+                atomicAdd(&ctl->ovf_total, 1ull);
+                if (o < (unsigned)sh.ovf_cap) {
+                    reinterpret_cast<uint4*>(sh.ovf_rec)[(size_t)sl[u] * sh.ovf_cap + o] =
+                        make_uint4((uint32_t)tg[u] >> 5, lig, ref, __float_as_uint(w[u]));
                 } else {
-                    const unsigned o = atomicAdd(&sh.ovf_cnt[sl[u]], 1u);
-                    atomicAdd(&ctl->ovf_total, 1ull);
-                    if (o < (unsigned)sh.ovf_cap) {
-                        reinterpret_cast<uint4*>(sh.ovf_rec)[(size_t)sl[u] * sh.ovf_cap + o] =
-                            make_uint4((uint32_t)tg[u] >> 5, lig, ref, __float_as_uint(w[u]));
-                    } else {
-                        cc_raise(ctl, CC_ERR_OVERFLOW_BIN, t);
-                    }
+                    cc_raise(ctl, CC_ERR_OVERFLOW_BIN, t);
                 }
             }
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u) { tg[u] = tg2[u]; sl[u] = sl2[u]; w[u] = w2[u]; }
+        p = p2; pc = pc2; j0 = j2;
     }
     if ((sh.debug_skip & 256) && lane == 0) {
         unsigned long long* d_ = reinterpret_cast<unsigned long long*>(sh.scratch)
@@ -1125,7 +1159,7 @@ extern "C" int cc_init_state(const cc_shard* sh, void* stream) {
 
 extern "C" int cc_deliver(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_deliver: null shard");
-    k_deliver<<<sm_count() * 2, 512, 0, (cudaStream_t)stream>>>(*sh);
+    k_deliver<<<sm_count() * CC_DEL_MINB, CC_DEL_THREADS, 0, (cudaStream_t)stream>>>(*sh);
     return cc_check_launch("k_deliver");
 }
 
