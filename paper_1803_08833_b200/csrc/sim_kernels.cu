@@ -1014,21 +1014,29 @@ k_deliver(const cc_shard sh) {
         }
         if (j0 == 0) events += (unsigned long long)pc.w;
         const uint32_t ref = pc.z;
-        // one atomic per (slot, group) run of lanes: warp-aggregated reservation
-        unsigned key[U], peers[U], pos[U], got[U];
+        // one atomic per run of consecutive lanes with the same (slot, group)
+        // key: rows are sorted by (delay, target), so a warp's 32 synapses form
+        // 1-3 runs; runs are found with a shuffle and a ballot (any split into
+        // equal-key runs is a valid reservation; __match_any_sync costs ~56 SM
+        // cycles with many distinct keys, tools/micro/match.cu)
+        unsigned key[U], pos[U], got[U];
+        int lead[U];
+        const unsigned upto = 0xffffffffu >> (31 - lane);      // bits 0..lane
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             key[u] = sl[u] >= 0 ? (unsigned)(sl[u] * NG + (tg[u] >> 5)) : 0xffffffffu;
-            peers[u] = __match_any_sync(0xffffffffu, key[u]);
+            const unsigned prev = __shfl_up_sync(0xffffffffu, key[u], 1);
+            const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || key[u] != prev);
+            lead[u] = 31 - __clz(heads & upto);
+            const unsigned after = heads & ~upto;
+            const int end = after ? __ffs(after) - 1 : 32;
             got[u] = 0u;
-            if (sl[u] >= 0 && lane == __ffs(peers[u]) - 1)
-                got[u] = atomicAdd(&sh.bin_cnt[key[u]], (unsigned)__popc(peers[u]));
+            if (sl[u] >= 0 && lane == lead[u])
+                got[u] = atomicAdd(&sh.bin_cnt[key[u]], (unsigned)(end - lead[u]));
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            pos[u] = __shfl_sync(0xffffffffu, got[u], __ffs(peers[u]) - 1)
-                     + __popc(peers[u] & ((1u << lane) - 1u));
-        }
+        for (int u = 0; u < U; ++u)
+            pos[u] = __shfl_sync(0xffffffffu, got[u], lead[u]) + (unsigned)(lane - lead[u]);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (sl[u] < 0) continue;
