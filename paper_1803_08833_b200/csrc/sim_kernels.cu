@@ -933,7 +933,10 @@ __device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
 #define CC_DEL_THREADS 256
 #endif
 #ifndef CC_DEL_MINB
-#define CC_DEL_MINB 3
+#define CC_DEL_MINB 2
+#endif
+#ifndef CC_DEL_U
+#define CC_DEL_U 8          // synapses per lane per pipelined unit
 #endif
 __global__ void __launch_bounds__(CC_DEL_THREADS, CC_DEL_MINB)
 k_deliver(const cc_shard sh) {
@@ -968,7 +971,7 @@ k_deliver(const cc_shard sh) {
     // Software pipeline over 128-synapse units of this warp's pieces (p = wid,
     // wid + nw, ...): the next unit's descriptor and CSR loads are issued
     // before the current unit's reservations and deposits.
-    constexpr int U = 4;
+    constexpr int U = CC_DEL_U;
     const long long np_ = (long long)n_pieces;
     long long p = wid;
     uint4 pc = p < np_ ? pcs[p] : make_uint4(0, 0, 0, 0);

@@ -18,7 +18,7 @@ sim = Simulator(cfg, net, chunk=100)
 sim.advance(400)
 L = sim.L
 st = torch.cuda.current_stream().cuda_stream
-nw = 148 * 3 * 8
+nw = 148 * 2 * 8
 for rep in range(3):
     sim.shard.debug_skip = 256
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -40,6 +40,6 @@ for rep in range(3):
     print(f"rep {rep}: event-timed {e0.elapsed_time(e1)*1e3:.1f} us, pieces {npieces}, span {((tail[:,2]-t0)/1e3).max():.1f} us")
     print(f"  warp start: p50 {np.median(start):.2f} max {start.max():.2f}; setup p50 {np.median(setup):.2f} max {setup.max():.2f}")
     print(f"  loop (busy warps): p50 {np.median(loop[busy]):.2f} p90 {np.percentile(loop[busy],90):.2f} max {loop[busy].max():.2f}")
-    nb = 148 * 3
+    nb = 148 * 2
     ends = raw[base - 65536 * 4 - nb: base - 65536 * 4].cpu().numpy().astype(np.int64)
     print(f"  block ends after loop: max {(ends.max()-t0)/1e3:.2f} us; last loop end {(tail[:,2].max()-t0)/1e3:.2f} us")
