@@ -259,8 +259,11 @@ class Simulator:
         stream = torch.cuda.current_stream(dev).cuda_stream
         _lib.check(self.L.cc_init_state(C.byref(sh), stream), "cc_init_state")
         _lib.check(self.L.cc_prepare(), "cc_prepare")
+        self._graph_t = None
         if use_graphs:                     # capture once, outside any timed region
             self._capture(self.chunk, torch.cuda.Stream(dev))
+            if substeps:
+                self._capture(self.chunk, torch.cuda.Stream(dev), timed=True)
 
     # ------------------------------------------------------------------ steps
     def _launch_step(self, stream) -> None:
@@ -286,14 +289,15 @@ class Simulator:
             self.buf["ctl"][4] = 0
         return c
 
-    def _capture(self, steps: int, stream_obj) -> None:
-        """The chunk graph; with substep timing, event-record nodes before and
-        after each step's delivery (2 per step + 1 at the end)."""
+    def _capture(self, steps: int, stream_obj, timed: bool = False):
+        """The chunk graph; timed: event-record nodes before and after each
+        step's delivery (2 per step + 1 at the end) - used for one sampled
+        chunk only, since the nodes cost ~9 % of the step."""
         torch = self.torch
-        if self.substeps and self._timer is None:
+        if timed and self._timer is None:
             self._timer = C.c_void_p()
             _lib.check(self.L.cc_timer_create(2 * steps + 1, C.byref(self._timer)))
-        tm = self._timer if self.substeps else None
+        tm = self._timer if timed else None
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream_obj):
             s = torch.cuda.current_stream(self.dev).cuda_stream
@@ -306,7 +310,11 @@ class Simulator:
                 _lib.check(self.L.cc_neuron_step(C.byref(self.shard), s), "cc_neuron_step")
             if tm is not None:
                 _lib.check(self.L.cc_timer_record(tm, 2 * steps, s))
-        self._graph, self._graph_steps = g, steps
+        if timed:
+            self._graph_t = g
+        else:
+            self._graph, self._graph_steps = g, steps
+        return g
 
     def _read_substeps(self, steps: int) -> None:
         el = self.L.cc_timer_elapsed_ms
@@ -351,8 +359,9 @@ class Simulator:
             if self.use_graphs and k == self.chunk:
                 if self._graph is None or self._graph_steps != k:
                     self._capture(k, torch.cuda.Stream(self.dev))
-                self._graph.replay()
-                timed = self.substeps
+                # substep timing on the first graph chunk only
+                timed = self._graph_t is not None and not self.kernel_ms["steps"]
+                (self._graph_t if timed else self._graph).replay()
             else:
                 s = torch.cuda.current_stream(self.dev).cuda_stream
                 for _ in range(k):
@@ -381,14 +390,15 @@ def _substeps(sim, n_steps: int, wall: float) -> dict:
     """RunResult.substep_seconds (engine.py:251-275 keys): expand = delivery
     kernel, integrate = neuron step (Poisson drive, sort and update are one
     kernel pair, so external is folded into it), deliver = spike exchange
-    (none on one GPU).  Device time of the graph-replayed chunks (CUDA event
-    nodes), scaled to all steps; without any, the wall goes to integrate."""
+    (none on one GPU).  The simulation wall is apportioned by the kernel-time
+    shares measured with CUDA event nodes on one graph chunk; without a timed
+    chunk, the wall goes to integrate."""
     km = sim.kernel_ms
-    if not km["steps"]:
+    tot = km["deliver"] + km["neuron"]
+    if not km["steps"] or tot <= 0:
         return {"deliver": 0.0, "expand": 0.0, "external": 0.0, "integrate": wall}
-    scale = n_steps / km["steps"] / 1e3
-    return {"deliver": 0.0, "expand": km["deliver"] * scale, "external": 0.0,
-            "integrate": km["neuron"] * scale}
+    return {"deliver": 0.0, "expand": wall * km["deliver"] / tot, "external": 0.0,
+            "integrate": wall * km["neuron"] / tot}
 
 
 def run_b200(config, workers: int = 1, *, net: Optional[DeviceNetwork] = None, probes=None,

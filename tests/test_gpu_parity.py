@@ -151,7 +151,7 @@ def test_config0_one_second_matches_reference(cuda, name):
     sub = res.substep_seconds
     assert set(sub) >= {"deliver", "expand", "external", "integrate"}
     assert sub["expand"] > 0 and sub["integrate"] > 0
-    assert sub["expand"] + sub["integrate"] < 2 * res.sim_seconds_wall
+    assert sub["expand"] + sub["integrate"] <= res.sim_seconds_wall * (1 + 1e-9)
 
 
 def test_overflow_path_same_raster(cuda):
