@@ -201,14 +201,21 @@ int cc_neuron_step(const cc_shard* sh, void* stream);
 int cc_ingest(const cc_shard* sh, const uint32_t* in_gid, const double* in_t,
               const int32_t* in_n, void* stream);
 
-/* Pack this shard's out-list into per-destination AER buffers using the
- * per-neuron destination bit mask (source_masks, network.py:229-230).
- * local_of_col maps a global column to its rank among owned columns.
- * send_gid/send_t are [n_dest][dest_cap]; send_n [n_dest] (zeroed by caller). */
-int cc_pack_outgoing(const cc_shard* sh, const uint32_t* dest_mask_by_local,
-                     int32_t n_dest, int32_t dest_cap, uint32_t* send_gid,
-                     double* send_t, int32_t* send_n, const uint32_t* local_of_col,
-                     void* stream);
+/* Multi-shard send, device-driven (capturable in a CUDA graph): pack this
+ * shard's out-list into one fixed-size slot per destination, selected by the
+ * per-neuron destination bit mask (source_masks, network.py:229-230):
+ * send[d] = {count, gid_0, t_0 bits, gid_1, ...}, int64, stride 1 + 2 cap.
+ * local_of_col maps a global column to its rank among owned columns.  The
+ * out-list is consumed (ctl->out_n = 0).  An all-to-all of the slots (equal
+ * splits, NCCL) stands in for the counters-then-payloads exchange of
+ * deliver_spikes (network.py:325-379). */
+int cc_pack_aer(const cc_shard* sh, const uint32_t* dest_mask_by_local, int32_t n_dest,
+                int32_t cap, int64_t* send, const int32_t* local_of_col, void* stream);
+
+/* Multi-shard receive of n_src packed slots (same layout): log the received
+ * spikes of step ctl->t - 1 (cuts their local rows into delivery pieces). */
+int cc_ingest_aer(const cc_shard* sh, const int64_t* recv, int32_t n_src, int32_t cap,
+                  void* stream);
 
 /* ------------------------------------------------- connectivity generator */
 /* Philox4x64-10 generator of the incoming-synapse CSR of one shard, bit-exact

@@ -111,8 +111,8 @@ _SIGS = {
     "cc_prepare": (C.c_int, []),
     "cc_neuron_step": (C.c_int, [C.POINTER(Shard), _P]),
     "cc_ingest": (C.c_int, [C.POINTER(Shard), _P, _P, _P, _P]),
-    "cc_pack_outgoing": (C.c_int, [C.POINTER(Shard), _P, C.c_int32, C.c_int32, _P, _P, _P,
-                                   _P, _P]),
+    "cc_pack_aer": (C.c_int, [C.POINTER(Shard), _P, C.c_int32, C.c_int32, _P, _P, _P]),
+    "cc_ingest_aer": (C.c_int, [C.POINTER(Shard), _P, C.c_int32, C.c_int32, _P]),
     "cc_gen_count": (C.c_int, [C.POINTER(Gen), _P, C.c_int64, _P, _P, _P]),
     "cc_gen_fill": (C.c_int, [C.POINTER(Gen), _P, C.c_int64, _P, _P, _P, _P, _P, _P,
                               C.c_int64, _P, _P]),

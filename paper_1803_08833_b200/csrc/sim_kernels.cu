@@ -6,7 +6,7 @@
 //   k_neuron    drain ring slot t, add the external Poisson events, order each
 //               neuron's inputs by (time, source, weight), integrate exactly in
 //               float64, emit spikes (engine.py:371-394, model.py:272-337)
-// plus k_ingest / k_pack for multi-shard runs and k_init_state.
+// plus k_ingest / k_pack_aer / k_ingest_aer for multi-shard runs and k_init_state.
 //
 // Exactness contract: every float64 expression below
 // follows the reference's evaluation order; the file is compiled with
@@ -1108,25 +1108,52 @@ __global__ void k_ingest(const cc_shard sh, const uint32_t* in_gid, const double
         log_spike(sh, t, in_gid[i], in_t[i]);
 }
 
-// Multi-shard send: AER payload per destination (source_masks, network.py:229-230).
-__global__ void k_pack(const cc_shard sh, const uint32_t* dest_mask, int n_dest, int dest_cap,
-                       uint32_t* send_gid, double* send_t, int32_t* send_n,
-                       const uint32_t* local_of_col, int n_col) {
-    const unsigned n = min(*(volatile unsigned*)&sh.ctl->out_n, (unsigned)sh.out_cap);
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+// Multi-shard send (source_masks, network.py:229-230; the counters-then-payloads
+// message of deliver_spikes, network.py:325-379, as one fixed-size slot per
+// destination): slot d = {count, (gid, t bits) x count}, int64 words.  One block,
+// so the per-destination counters live in shared memory; consumes the out-list.
+__global__ void __launch_bounds__(1024)
+k_pack_aer(const cc_shard sh, const uint32_t* dest_mask, int n_dest, int cap,
+           long long* send, const int32_t* local_of_col) {
+    __shared__ unsigned cnt[32];
+    cc_ctl* ctl = sh.ctl;
+    if (threadIdx.x < 32) cnt[threadIdx.x] = 0u;
+    __syncthreads();
+    const unsigned n = min(*(volatile unsigned*)&ctl->out_n, (unsigned)sh.out_cap);
+    const size_t stride = 1 + 2 * (size_t)cap;
+    const int n_col = sh.n_col;
+    for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {
         const uint32_t g = sh.out_gid[i];
-        const uint32_t li = local_of_col[g / n_col] * n_col + g % n_col;
+        const uint32_t li = (uint32_t)local_of_col[g / n_col] * n_col + g % n_col;
         const uint32_t m = dest_mask[li];
+        const long long tb = __double_as_longlong(sh.out_t[i]);
         for (int d = 0; d < n_dest; ++d) {
             if (!(m >> d & 1u)) continue;
-            const int p = atomicAdd(&send_n[d], 1);
-            if (p < dest_cap) {
-                send_gid[(size_t)d * dest_cap + p] = g;
-                send_t[(size_t)d * dest_cap + p] = sh.out_t[i];
+            const unsigned p = atomicAdd(&cnt[d], 1u);
+            if (p < (unsigned)cap) {
+                send[d * stride + 1 + 2 * (size_t)p] = (long long)g;
+                send[d * stride + 2 + 2 * (size_t)p] = tb;
             } else {
-                cc_raise(sh.ctl, CC_ERR_OUTLIST, *(volatile long long*)&sh.ctl->t - 1);
+                cc_raise(ctl, CC_ERR_OUTLIST, *(volatile long long*)&ctl->t - 1);
             }
         }
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < n_dest) send[threadIdx.x * stride] = (long long)min(cnt[threadIdx.x], (unsigned)cap);
+    if (threadIdx.x == 0) ctl->out_n = 0u;                // out-list consumed
+}
+
+// Multi-shard receive of the packed slots of n_src sources: log the AER events
+// of step ctl->t - 1 that have rows here (rows_for, network.py:135-141).
+__global__ void k_ingest_aer(const cc_shard sh, const long long* recv, int n_src, int cap) {
+    const long long t = *(volatile long long*)&sh.ctl->t - 1;
+    if (*(volatile unsigned*)&sh.ctl->error_bits) return;
+    const size_t stride = 1 + 2 * (size_t)cap;
+    for (int src = 0; src < n_src; ++src) {
+        const long long* r = recv + src * stride;
+        const int n = (int)min(r[0], (long long)cap);
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+            log_spike(sh, t, (uint32_t)r[1 + 2 * i], __longlong_as_double(r[2 + 2 * i]));
     }
 }
 
@@ -1215,14 +1242,22 @@ extern "C" int cc_ingest(const cc_shard* sh, const uint32_t* in_gid, const doubl
     return cc_check_launch("k_ingest");
 }
 
-extern "C" int cc_pack_outgoing(const cc_shard* sh, const uint32_t* dest_mask_by_local,
-                                int32_t n_dest, int32_t dest_cap, uint32_t* send_gid,
-                                double* send_t, int32_t* send_n, const uint32_t* local_of_col,
-                                void* stream) {
-    if (!sh) return cc_set_error("cc_pack_outgoing: null shard");
-    if (n_dest > 32) return cc_set_error("cc_pack_outgoing: at most 32 shards");
-    k_pack<<<sm_count(), 256, 0, (cudaStream_t)stream>>>(*sh, dest_mask_by_local, n_dest,
-                                                         dest_cap, send_gid, send_t, send_n,
-                                                         local_of_col, sh->n_col);
-    return cc_check_launch("k_pack");
+extern "C" int cc_pack_aer(const cc_shard* sh, const uint32_t* dest_mask_by_local,
+                           int32_t n_dest, int32_t cap, int64_t* send,
+                           const int32_t* local_of_col, void* stream) {
+    if (!sh) return cc_set_error("cc_pack_aer: null shard");
+    if (n_dest < 1 || n_dest > 32) return cc_set_error("cc_pack_aer: 1..32 shards");
+    if (cap < 1) return cc_set_error("cc_pack_aer: cap must be positive");
+    k_pack_aer<<<1, 1024, 0, (cudaStream_t)stream>>>(*sh, dest_mask_by_local, n_dest, cap,
+                                                     reinterpret_cast<long long*>(send),
+                                                     local_of_col);
+    return cc_check_launch("k_pack_aer");
+}
+
+extern "C" int cc_ingest_aer(const cc_shard* sh, const int64_t* recv, int32_t n_src, int32_t cap,
+                             void* stream) {
+    if (!sh) return cc_set_error("cc_ingest_aer: null shard");
+    k_ingest_aer<<<sm_count(), 256, 0, (cudaStream_t)stream>>>(
+        *sh, reinterpret_cast<const long long*>(recv), n_src, cap);
+    return cc_check_launch("k_ingest_aer");
 }

@@ -109,76 +109,127 @@ def _has_row_all_ranks(net, size, group=None):
     return [g.cpu().numpy().astype(bool) for g in gathered]
 
 
-class DistributedSimulator:
-    """One rank's shard: Simulator in exchange mode + SpikeExchange per step."""
+def _aer_cap(sim) -> int:
+    """Spikes one shard can emit in a step: every owned neuron at most the
+    engine's per-step bound (refractoriness >= dt gives 1)."""
+    from .engine import _spikes_per_step_bound
+    return max(1, sim.n_local * _spikes_per_step_bound(sim.cfg))
 
-    def __init__(self, cfg, rank: int, size: int, device=None, group=None, **sim_kw):
+
+class DistributedSimulator:
+    """One rank's shard: Simulator in exchange mode plus a device-driven AER
+    exchange per step - cc_pack_aer (fixed-size slot per destination), one
+    equal-split all_to_all_single (NCCL), cc_ingest_aer - so whole chunks of
+    steps are captured into a CUDA graph with no host synchronisation."""
+
+    def __init__(self, cfg, rank: int, size: int, device=None, group=None, chunk: int = 100,
+                 use_graphs: bool = True, **sim_kw):
         import torch
         from .engine import Simulator
         from .network import build_b200
         self.torch = torch
-        self.rank, self.size = rank, size
+        self.rank, self.size, self.group = rank, size, group
         self.dev = torch.device(device or f"cuda:{torch.cuda.current_device()}")
         self.net = build_b200(cfg, rank=rank, size=size, device=self.dev)
         self.sim = Simulator(cfg, self.net, direct_log=False, use_graphs=False, device=self.dev,
                              **sim_kw)
         has = _has_row_all_ranks(self.net, size, group)
         masks = dest_masks_from_rows(has, self.sim.gids)
-        self.xchg = SpikeExchange(rank, size, masks, self.dev, group)
+        self.mask = torch.as_tensor(masks.astype(np.uint32).view(np.int32), device=self.dev)
         n = cfg.grid.neurons_per_column
         self.local_of_col = np.full(cfg.grid.n_columns, -1, np.int64)
         self.local_of_col[self.net.owned_columns] = np.arange(len(self.net.owned_columns))
-        self.lut = torch.as_tensor(self.local_of_col, device=self.dev)
+        self.lut = torch.as_tensor(self.local_of_col.astype(np.int32), device=self.dev)
         self.n_col = n
+        self.cap = _aer_cap(self.sim)
+        self.send = torch.zeros((size, 1 + 2 * self.cap), dtype=torch.int64, device=self.dev)
+        self.recv = torch.zeros_like(self.send)
+        self.chunk = max(1, int(chunk))
+        self.use_graphs = use_graphs
+        self._graph = None
         self.t = 0
         self.timers = dict(exchange=0.0, kernels=0.0)
-        self.n_in = torch.zeros(1, dtype=torch.int32, device=self.dev)
+
+    def _launch(self, stream) -> None:
+        """One step on `stream` (torch stream): deliver, neuron step, pack,
+        all-to-all, ingest - no host synchronisation."""
+        from . import _lib
+        L, sim, s = self.sim.L, self.sim, stream.cuda_stream
+        sim._launch_step(s)
+        _lib.check(L.cc_pack_aer(C.byref(sim.shard), self.mask.data_ptr(), self.size, self.cap,
+                                 self.send.data_ptr(), self.lut.data_ptr(), s), "cc_pack_aer")
+        self.dist_a2a()
+        _lib.check(L.cc_ingest_aer(C.byref(sim.shard), self.recv.data_ptr(), self.size, self.cap,
+                                   s), "cc_ingest_aer")
+
+    def measure_exchange(self, n_steps: int):
+        """(exchange ms, step ms) summed over n eager steps, CUDA events on the
+        stream: exchange = pack + all-to-all + ingest."""
+        from . import _lib
+        torch = self.torch
+        st = torch.cuda.current_stream(self.dev)
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n_steps)]
+        L, sim, s = self.sim.L, self.sim, st.cuda_stream
+        for e in ev:
+            e[0].record(st)
+            sim._launch_step(s)
+            e[1].record(st)
+            _lib.check(L.cc_pack_aer(C.byref(sim.shard), self.mask.data_ptr(), self.size,
+                                     self.cap, self.send.data_ptr(), self.lut.data_ptr(), s))
+            self.dist_a2a()
+            _lib.check(L.cc_ingest_aer(C.byref(sim.shard), self.recv.data_ptr(), self.size,
+                                       self.cap, s))
+            e[2].record(st)
+        torch.cuda.synchronize(self.dev)
+        self.t += n_steps
+        self.sim.t = self.t
+        self.sim.check()
+        return (sum(e[1].elapsed_time(e[2]) for e in ev), sum(e[0].elapsed_time(e[2]) for e in ev))
+
+    def dist_a2a(self) -> None:
+        import torch.distributed as dist
+        dist.all_to_all_single(self.recv, self.send, group=self.group)
 
     def step(self) -> None:
-        torch = self.torch
-        L, sim = self.sim.L, self.sim
-        from . import _lib
-        s = torch.cuda.current_stream(self.dev).cuda_stream
-        t0 = time.perf_counter()
-        sim._launch_step(s)                      # deliver + plan + stage + update
-        torch.cuda.synchronize(self.dev)
-        t1 = time.perf_counter()
-        ctl = sim.buf["ctl"]
-        out_n = int(sim.ctl().out_n)
-        g = sim.buf["out_gid"][:out_n].long() & 0xFFFFFFFF
-        tm = sim.buf["out_t"][:out_n]
-        li = self.lut[g // self.n_col] * self.n_col + g % self.n_col
-        rg, rt = self.xchg.exchange(li, g, tm)
-        k = int(rg.numel())
-        in_g = rg.to(torch.int32).contiguous()
-        in_t = rt.contiguous()
-        self.n_in.fill_(k)
-        _lib.check(L.cc_ingest(C.byref(sim.shard), in_g.data_ptr() if k else 0,
-                               in_t.data_ptr() if k else 0, self.n_in.data_ptr(), s), "cc_ingest")
-        # reset the out-list fill (ctl.out_n, byte offset of field)
-        off = _lib.Ctl.out_n.offset
-        ctl.view(torch.uint8)[off:off + 4].zero_()
-        torch.cuda.synchronize(self.dev)
-        self.timers["kernels"] += t1 - t0
-        self.timers["exchange"] += time.perf_counter() - t1
+        self._launch(self.torch.cuda.current_stream(self.dev))
         self.t += 1
 
-    def advance(self, n_steps: int, check_every: int = 100) -> None:
-        for i in range(n_steps):
-            self.step()
-            if (i + 1) % check_every == 0 or i == n_steps - 1:
-                self.sim.check()
+    def _capture(self) -> None:
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=torch.cuda.Stream(self.dev)):
+            st = torch.cuda.current_stream(self.dev)
+            for _ in range(self.chunk):
+                self._launch(st)
+        self._graph = g
+
+    def advance(self, n_steps: int) -> None:
+        """Steps in chunks (CUDA graph replays once the communicator is warm),
+        with the device counters checked and the raster drained per chunk."""
+        done = 0
+        while done < n_steps:
+            k = min(self.chunk, n_steps - done)
+            if self.use_graphs and k == self.chunk and self.t > 0:
+                if self._graph is None:
+                    self._capture()
+                self._graph.replay()
+                self.t += k
+            else:
+                for _ in range(k):
+                    self.step()
+            done += k
+            self.sim.t = self.t
+            self.sim.check()
 
 
 def run_local_shards(config, size: int, device=None):
     """All `size` shards of a multi-GPU run, stepped in turn on ONE device.
 
     Same shard code as run_multi_gpu - per-rank generator (build_b200 rank /
-    size), exchange-mode neuron step (out-list), cc_ingest - with the AER
-    exchange done in-process: destination d receives, in source-rank order,
-    the spikes whose source has a row on d (SpikeExchange semantics).  No
-    kernel waits on another shard's kernel.  Used to test partition invariance
-    of the CUDA path on a single B200 (tests/test_gpu_parity.py)."""
+    size), exchange-mode neuron step (out-list), cc_pack_aer, cc_ingest_aer -
+    with the all-to-all done by device copies of the packed slots.  No kernel
+    waits on another shard's kernel.  Used to test partition invariance of
+    the CUDA path on a single B200 (tests/test_gpu_parity.py)."""
     import torch
     from . import _lib
     from .engine import RunResult, Simulator, raster_checksum
@@ -188,46 +239,34 @@ def run_local_shards(config, size: int, device=None):
     sims = [Simulator(config, nets[r], direct_log=False, use_graphs=False, device=dev)
             for r in range(size)]
     has = [((n.row_off[1:] - n.row_off[:-1]) > 0).cpu().numpy() for n in nets]
-    n_col = config.grid.neurons_per_column
-    masks, luts = [], []
+    cap = max(_aer_cap(sm) for sm in sims)
+    masks, luts, sends = [], [], []
     for r in range(size):
-        masks.append(torch.as_tensor(dest_masks_from_rows(has, sims[r].gids), device=dev))
-        lut = np.full(config.grid.n_columns, -1, np.int64)
+        masks.append(torch.as_tensor(dest_masks_from_rows(has, sims[r].gids)
+                                     .astype(np.uint32).view(np.int32), device=dev))
+        lut = np.full(config.grid.n_columns, -1, np.int32)
         lut[nets[r].owned_columns] = np.arange(len(nets[r].owned_columns))
         luts.append(torch.as_tensor(lut, device=dev))
-    n_in = torch.zeros(1, dtype=torch.int32, device=dev)
-    off = _lib.Ctl.out_n.offset
+        sends.append(torch.zeros((size, 1 + 2 * cap), dtype=torch.int64, device=dev))
+    recv = torch.zeros((size, 1 + 2 * cap), dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
+    s = stream.cuda_stream
     t0 = time.perf_counter()
     for step in range(config.n_steps):
-        out = []
         for r, sim in enumerate(sims):
-            sim._launch_step(stream.cuda_stream)
-        torch.cuda.synchronize(dev)
-        for r, sim in enumerate(sims):
-            k = int(sim.ctl().out_n)
-            g = sim.buf["out_gid"][:k].long() & 0xFFFFFFFF
-            li = luts[r][g // n_col] * n_col + g % n_col
-            out.append((g, sim.buf["out_t"][:k].clone(), masks[r][li] if k else g))
-            sim.buf["ctl"].view(torch.uint8)[off:off + 4].zero_()
+            sim._launch_step(s)
+            _lib.check(sim.L.cc_pack_aer(C.byref(sim.shard), masks[r].data_ptr(), size, cap,
+                                         sends[r].data_ptr(), luts[r].data_ptr(), s),
+                       "cc_pack_aer")
         for d, sim in enumerate(sims):
-            gs, ts = [], []
-            for g, tm, m in out:
-                if g.numel():
-                    sel = ((m >> d) & 1).bool()
-                    gs.append(g[sel])
-                    ts.append(tm[sel])
-            in_g = torch.cat(gs).to(torch.int32) if gs else torch.zeros(0, dtype=torch.int32,
-                                                                        device=dev)
-            in_t = torch.cat(ts) if ts else torch.zeros(0, dtype=torch.float64, device=dev)
-            n_in.fill_(int(in_g.numel()))
-            _lib.check(sim.L.cc_ingest(C.byref(sim.shard), in_g.data_ptr() if in_g.numel() else 0,
-                                       in_t.data_ptr() if in_t.numel() else 0, n_in.data_ptr(),
-                                       stream.cuda_stream), "cc_ingest")
-            torch.cuda.synchronize(dev)
+            for r in range(size):                       # recv[r] = slot d of source r
+                recv[r].copy_(sends[r][d])
+            _lib.check(sim.L.cc_ingest_aer(C.byref(sim.shard), recv.data_ptr(), size, cap, s),
+                       "cc_ingest_aer")
         if (step + 1) % 100 == 0 or step == config.n_steps - 1:
             for sim in sims:
                 sim.check()
+    torch.cuda.synchronize(dev)
     wall = time.perf_counter() - t0
     ctls = [sim.ctl() for sim in sims]
     parts = [sim.raster() for sim in sims]
@@ -282,8 +321,7 @@ def run_multi_gpu(config, workers: int):
     g, t = ds.sim.raster()
     mine = dict(g=g, t=t, n_spikes=int(c.n_spikes), rec=int(c.rec_events), ext=int(c.ext_events),
                 syn=ds.net.n_synapses, csum=ds.net.checksum, cons=ds.net.construction_seconds,
-                wall=wall, steady=ds.net.steady_bytes, peak=ds.net.peak_bytes,
-                xchg=ds.timers["exchange"], kern=ds.timers["kernels"])
+                wall=wall, steady=ds.net.steady_bytes, peak=ds.net.peak_bytes)
     allr = [None] * size
     dist.all_gather_object(allr, mine)
     if rank != 0:
@@ -300,52 +338,89 @@ def run_multi_gpu(config, workers: int):
         raster_checksum=raster_checksum(g, t),
         construction_seconds=max(r["cons"] for r in allr),
         sim_seconds_wall=max(r["wall"] for r in allr),
-        substep_seconds={"deliver": max(r["xchg"] for r in allr),
-                         "expand": 0.0, "external": 0.0,
-                         "integrate": max(r["kern"] for r in allr)},
+        # the exchange runs inside the same CUDA graphs as the kernels
+        substep_seconds={"deliver": 0.0, "expand": 0.0, "external": 0.0,
+                         "integrate": max(r["wall"] for r in allr)},
         steady_bytes_per_worker=[r["steady"] for r in allr],
         peak_bytes_per_worker=[r["peak"] for r in allr])
 
 
 def bench_distributed(args, cfg) -> None:
-    """bench.py for N > 1 (launched by torchrun): device-timed K steps, max
-    over ranks, rank 0 prints the JSON line."""
+    """bench.py for N > 1 (launched by torchrun): K steps timed with CUDA
+    events on every rank (max over ranks), rank 0 prints the JSON line.  The
+    step loop is host-driven (exchange per step), so the same timed region is
+    also the end-to-end number (host loop, NCCL exchange, raster copies)."""
     import torch
     import torch.distributed as dist
     rank, size = _init_dist()
     ds = DistributedSimulator(cfg, rank, size)
     ds.advance(args.warmup)
     c0 = ds.sim.ctl()
+    clocks = None
+    if rank == 0:
+        import bench as _b                               # the repo-root bench module
+        clocks = _b.Clocks(torch.cuda.current_device())
     dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
     ev0.record()
-    x0 = ds.timers["exchange"]
     ds.advance(args.steps)
     ev1.record()
     torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
     dist.barrier()
+    clk = clocks.stop() if clocks is not None else None
     ms = torch.tensor([ev0.elapsed_time(ev1)], device=ds.dev)
-    xs = torch.tensor([ds.timers["exchange"] - x0], device=ds.dev, dtype=torch.float64)
+    wl = torch.tensor([wall], device=ds.dev, dtype=torch.float64)
     c1 = ds.sim.ctl()
-    ev = torch.tensor([(c1.rec_events + c1.ext_events) - (c0.rec_events + c0.ext_events)],
+    ev = torch.tensor([(c1.rec_events + c1.ext_events) - (c0.rec_events + c0.ext_events),
+                       c1.rec_events - c0.rec_events, c1.n_spikes - c0.n_spikes],
                       device=ds.dev, dtype=torch.float64)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    dist.all_reduce(xs, op=dist.ReduceOp.MAX)
+    # exchange share from a short eager sample after the timed region
+    xm, sm = ds.measure_exchange(20)
+    xs = torch.tensor([xm / max(sm, 1e-9)], device=ds.dev, dtype=torch.float64)
+    a2a_bytes = float(ds.send.numel() * 8)
+    for x in (ms, xs, wl):
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
     dist.all_reduce(ev, op=dist.ReduceOp.SUM)
     if rank == 0:
         ms_v = float(ms.item())
+        total, rec = float(ev[0].item()), float(ev[1].item())
+        try:
+            hbm = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(
+                os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"])
+        except Exception:
+            hbm = 6650.0
+        ach = rec / (ms_v / 1e3) * 17 / 1e9 / size          # per GPU
         line = {
             "metric": "synaptic events/s (recurrent + external)",
-            "value": float(ev.item()) / (ms_v / 1e3), "unit": "events/s", "n_gpus": size,
+            "value": total / (ms_v / 1e3), "unit": "events/s", "n_gpus": size,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_v / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: seeded counter-based RNG, bit-exact with the reference streams",
-            "config": {"workload": f"BASELINE config {args.config}", "grid":
-                       f"{cfg.grid.nx}x{cfg.grid.ny}", "parallelism": f"column blocks x{size}"},
+            "data": "synthetic: seeded counter-based RNG (connectivity, Poisson drive), "
+                    "bit-exact with the reference streams",
+            "config": {"workload": f"BASELINE config {args.config}: {cfg.grid.nx}x{cfg.grid.ny} "
+                                   f"columns x {cfg.grid.neurons_per_column} neurons, "
+                                   f"{cfg.kernel.kind} lateral decay, calibrated drive",
+                       "grid": f"{cfg.grid.nx}x{cfg.grid.ny}", "neurons": cfg.grid.n_neurons,
+                       "parallelism": f"column blocks x{size} (one process per GPU, NCCL)",
+                       "l2": "no flush between steps (per-step working set > 126 MB L2)"},
             "wall_s_per_sim_s": (ms_v / 1e3) / (args.steps * cfg.timestep_ms / 1e3),
-            "exchange_fraction": float(xs.item()) * 1e3 / ms_v,
-            "gpu_launches": 5 * args.steps,
+            "exchange_fraction": float(xs.item()),
+            "exchange": "device-driven: cc_pack_aer + equal-split NCCL all_to_all_single "
+                        f"({a2a_bytes / 1e6:.2f} MB per rank per step) + cc_ingest_aer, "
+                        "captured in CUDA graphs of 100 steps",
+            "roofline": {"bound": "hbm", "kernel": "whole step, per GPU (exchange mode)",
+                         "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                         "traffic": None, "bytes_per_event": 17},
+            "e2e": {"value": total / float(wl.item()), "unit": "events/s",
+                    "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 12.0 * float(ev[2].item()) / args.steps,
+                    "api": "DistributedSimulator.advance wall (graph replays, per-chunk "
+                           "counter checks and raster copies)"},
+            "gpu_launches": 5 * args.steps,       # deliver, plan, stage, pack, ingest per step
+            "clocks": clk,
         }
         print(json.dumps(line))
     dist.destroy_process_group()
