@@ -5,7 +5,8 @@ Public surface (mirrors corticarc's names where they exist):
 
     GridSpec, KernelSpec, SynapseGenSpec, NeuronParams, ExternalInputSpec,
     SimConfig, MemoryBudgetError          run description (spec.py)
-    build_b200, import_csr                network build on the GPU (network.py)
+    build_b200, import_csr, export_csr    network build on the GPU, reference-format
+                                          CSR in and out (network.py)
     run_b200, Simulator, RunResult        simulate (engine.py)
     runner                                the `runner(config, workers)` seam of
                                           metrics.scaling_harness / calibration_sweep
@@ -21,13 +22,14 @@ __version__ = "0.1.0"
 __all__ = [
     "GridSpec", "KernelSpec", "SynapseGenSpec", "NeuronParams", "ExternalInputSpec",
     "SimConfig", "MemoryBudgetError", "baseline_config", "build_b200", "import_csr",
+    "export_csr",
     "run_b200", "Simulator", "RunResult", "runner", "__version__",
 ]
 
 
 def __getattr__(name):
     # device-facing modules load lazily so that config-only use works on CPU hosts
-    if name in ("build_b200", "import_csr", "DeviceNetwork"):
+    if name in ("build_b200", "import_csr", "export_csr", "DeviceNetwork"):
         from . import network
         return getattr(network, name)
     if name in ("run_b200", "Simulator", "RunResult"):

@@ -26,7 +26,7 @@ from . import _lib
 from .geometry import layout_blocks
 from .partition import map_columns_to_workers
 
-__all__ = ["DeviceNetwork", "build_b200", "import_csr", "halo_source_columns"]
+__all__ = ["DeviceNetwork", "build_b200", "import_csr", "export_csr", "halo_source_columns"]
 
 MASK64 = (1 << 64) - 1
 
@@ -216,3 +216,18 @@ def import_csr(cfg, sources, offsets, target_local, delay, weight, rank: int = 0
                          syn_d=syn_d, n_synapses=S, checksum=int(csum.item()) & MASK64,
                          construction_seconds=time.perf_counter() - t0,
                          row_len_max=int(np.diff(offsets).max()) if len(sources) else 0)
+
+
+def export_csr(net: DeviceNetwork) -> dict:
+    """The shard's store in the reference's IncomingSynapses layout
+    (network.py:114-152): rows of the sources that have synapses here, in
+    ascending gid order, each sorted by delay (network.py:257).  Returns numpy
+    arrays sources u64, offsets i64, target_local u32, delay u16, weight f32 -
+    what import_csr takes back (round trip), plus the construction checksum."""
+    row_off, tgt, w, d = net.host_csr()
+    ln = np.diff(row_off)
+    src = np.flatnonzero(ln).astype(np.int64)
+    offsets = np.concatenate([[0], np.cumsum(ln[src])]).astype(np.int64)
+    return dict(sources=src.astype(np.uint64), offsets=offsets,
+                target_local=tgt.astype(np.uint32), delay=d.astype(np.uint16),
+                weight=w.astype(np.float32), checksum=net.checksum)

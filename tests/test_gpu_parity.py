@@ -261,6 +261,25 @@ def test_multapse_ties_follow_weight_order(cuda):
     assert res.recurrent_events == ref.recurrent_events
 
 
+def test_export_matches_reference_store_and_round_trips(cuda):
+    """export_csr gives the reference's IncomingSynapses arrays (sources,
+    offsets, targets, delays, weights identical to the golden store) and
+    import_csr(export) rebuilds the same network."""
+    from paper_1803_08833_b200.network import build_b200, export_csr, import_csr
+    meta = golden_json("connectivity.json")["gauss"]
+    arr = golden_npz("connectivity.npz")
+    cfg = _conn_config(meta)
+    ex = export_csr(build_b200(cfg))
+    assert np.array_equal(ex["sources"], arr["gauss_sources"].astype(np.uint64))
+    assert np.array_equal(ex["offsets"], arr["gauss_offsets"].astype(np.int64))
+    assert np.array_equal(ex["target_local"], arr["gauss_target"].astype(np.uint32))
+    assert np.array_equal(ex["delay"], arr["gauss_delay"].astype(np.uint16))
+    assert np.array_equal(ex["weight"].view(np.uint32), arr["gauss_weight"].view(np.uint32))
+    back = import_csr(cfg, ex["sources"], ex["offsets"], ex["target_local"], ex["delay"],
+                      ex["weight"])
+    assert back.checksum == ex["checksum"] == meta["checksum"]
+
+
 def test_zero_duration_is_construction_only(cuda):
     from paper_1803_08833_b200.engine import run_b200
     res = run_b200(tiny_config(duration_s=0.0), 1)

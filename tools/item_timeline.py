@@ -57,3 +57,9 @@ for rep in range(2):
           f"mean dur {dur[late].mean():.1f} us (all: {tail[:, 6].mean():.1f}, {dur.mean():.1f})")
     idle = (rel[:, 4].max() - lw).sum() / (len(lw) * rel[:, 4].max())
     print(f"  warp-time idle after own last item: {100 * idle:.1f}%")
+    # the last 5 % of claims: phase durations
+    lastk = np.argsort(rel[:, 0])[-max(1, len(rel) // 20):]
+    ph = np.diff(rel[lastk][:, [0, 2, 3, 4]], axis=1)
+    print(f"  last 5% claims: rtot {tail[lastk, 6].mean():.0f}, gather+sort {ph[:, 0].mean():.1f}, "
+          f"factors {ph[:, 1].mean():.1f}, publish+update {ph[:, 2].mean():.1f} us; "
+          f"end at {rel[lastk, 4].mean():.1f} (kernel end {rel[:, 4].max():.1f})")
