@@ -222,14 +222,16 @@ class DistributedSimulator:
             self.sim.check()
 
 
-def run_local_shards(config, size: int, device=None):
+def run_local_shards(config, size: int, device=None, flat_ingest: bool = False):
     """All `size` shards of a multi-GPU run, stepped in turn on ONE device.
 
     Same shard code as run_multi_gpu - per-rank generator (build_b200 rank /
     size), exchange-mode neuron step (out-list), cc_pack_aer, cc_ingest_aer -
     with the all-to-all done by device copies of the packed slots.  No kernel
     waits on another shard's kernel.  Used to test partition invariance of
-    the CUDA path on a single B200 (tests/test_gpu_parity.py)."""
+    the CUDA path on a single B200 (tests/test_gpu_parity.py).  flat_ingest:
+    receive through cc_ingest (one flat AER list per shard, the entry for
+    hosts with their own transport) instead of cc_ingest_aer."""
     import torch
     from . import _lib
     from .engine import RunResult, Simulator, raster_checksum
@@ -261,8 +263,18 @@ def run_local_shards(config, size: int, device=None):
         for d, sim in enumerate(sims):
             for r in range(size):                       # recv[r] = slot d of source r
                 recv[r].copy_(sends[r][d])
-            _lib.check(sim.L.cc_ingest_aer(C.byref(sim.shard), recv.data_ptr(), size, cap, s),
-                       "cc_ingest_aer")
+            if flat_ingest:
+                cnt = recv[:, 0].tolist()
+                ev = torch.cat([recv[r, 1:1 + 2 * c].view(-1, 2) for r, c in enumerate(cnt)])
+                g32 = ev[:, 0].to(torch.int32).contiguous()
+                tf = ev[:, 1].contiguous().view(torch.float64)
+                n_in = torch.tensor([g32.numel()], dtype=torch.int32, device=dev)
+                _lib.check(sim.L.cc_ingest(C.byref(sim.shard), g32.data_ptr(), tf.data_ptr(),
+                                           n_in.data_ptr(), s), "cc_ingest")
+                torch.cuda.synchronize(dev)             # the temporaries die here
+            else:
+                _lib.check(sim.L.cc_ingest_aer(C.byref(sim.shard), recv.data_ptr(), size, cap,
+                                               s), "cc_ingest_aer")
         if (step + 1) % 100 == 0 or step == config.n_steps - 1:
             for sim in sims:
                 sim.check()

@@ -304,11 +304,19 @@ def test_event_bookkeeping_matches_fanout(cuda):
                                        ("config0_cal_0p1", 4)])
 def test_partition_invariance_on_one_gpu(cuda, name, size):
     """W shards (per-rank generator, exchange-mode neuron step, AER exchange,
-    cc_ingest) stepped on one B200 give the reference raster (acceptance #4,
+    cc_pack_aer / cc_ingest_aer) stepped on one B200 give the reference raster (acceptance #4,
     SURVEY 8(e))."""
     from paper_1803_08833_b200.distributed import run_local_shards
     cfg, meta, arr = golden_run(name)
     res = run_local_shards(cfg, size)
+    _assert_same_run(res, meta, arr)
+
+
+def test_partition_invariance_flat_ingest(cuda):
+    """The same with the flat AER receive entry (cc_ingest)."""
+    from paper_1803_08833_b200.distributed import run_local_shards
+    cfg, meta, arr = golden_run("tiny_gauss")
+    res = run_local_shards(cfg, 2, flat_ingest=True)
     _assert_same_run(res, meta, arr)
 
 
