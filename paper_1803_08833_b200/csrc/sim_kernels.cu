@@ -257,8 +257,10 @@ __device__ __forceinline__ bool slow_step(NState& s, const cc_pop& P, double tj,
                                        double ecr0, double w) {
     const double ff = fmin(fmax(s.last, s.ru), tj);
     double cs = s.c;
-    if (ff != s.last && cs != 0.0)                    // leaving / inside a refractory window
-        cs = cs * (stale ? exp(-(ff - s.last) / P.tau_c) : ecr0);
+    if (ff != s.last && cs != 0.0) {                  // leaving / inside a refractory window
+        if (stale) cs = cs * exp(-(ff - s.last) / P.tau_c);
+        else cs = cs * ecr0;
+    }
     double emj = em0, ecj = ec0, fj = f0;
     if (stale) decay_factors(P, tj - ff, cs != 0.0, emj, ecj, fj);
     else if (!cflag) { ecj = 1.0; fj = 0.0; }
