@@ -696,6 +696,7 @@ k_stage(const cc_shard sh) {
                 }
             }
         }
+        CC_DBG(1, gtimer());
         // ---- 2 order each neuron's inputs by (t, src): counting sort on a
         //      monotone time bucket (adaptive count per neuron, flattened over
         //      the warp), then the exact rank of each input inside its bucket

@@ -34,7 +34,7 @@ for rep in range(2):
     dur = rel[:, 4] - rel[:, 0]
     print(f"rep {rep}: items {ni}, span {rel[:,4].max():.1f} us, first claim spread {np.sort(rel[:,0])[:2000].max():.1f} us")
     print(f"  item us: mean {dur.mean():.1f} p50 {np.median(dur):.1f} p90 {np.percentile(dur,90):.1f} max {dur.max():.1f}")
-    for k, name in enumerate(["gather+admit", "ext+sort", "factors", "update"]):
+    for k, name in enumerate(["gather+drive", "sort", "factors", "publish+update"]):
         d = rel[:, k + 1] - rel[:, k]
         print(f"  {name:14s} mean {d.mean():6.2f} p90 {np.percentile(d,90):6.2f} max {d.max():6.2f}")
     warps = tail[:, 7]
@@ -59,7 +59,8 @@ for rep in range(2):
     print(f"  warp-time idle after own last item: {100 * idle:.1f}%")
     # the last 5 % of claims: phase durations
     lastk = np.argsort(rel[:, 0])[-max(1, len(rel) // 20):]
-    ph = np.diff(rel[lastk][:, [0, 2, 3, 4]], axis=1)
-    print(f"  last 5% claims: rtot {tail[lastk, 6].mean():.0f}, gather+sort {ph[:, 0].mean():.1f}, "
-          f"factors {ph[:, 1].mean():.1f}, publish+update {ph[:, 2].mean():.1f} us; "
+    ph = np.diff(rel[lastk][:, [0, 1, 2, 3, 4]], axis=1)
+    print(f"  last 5% claims: rtot {tail[lastk, 6].mean():.0f}, gather+drive {ph[:, 0].mean():.1f}, "
+          f"sort {ph[:, 1].mean():.1f}, factors {ph[:, 2].mean():.1f}, "
+          f"publish+update {ph[:, 3].mean():.1f} us; "
           f"end at {rel[lastk, 4].mean():.1f} (kernel end {rel[:, 4].max():.1f})")
