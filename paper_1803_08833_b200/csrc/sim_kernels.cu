@@ -681,14 +681,37 @@ k_stage(const cc_shard sh) {
             }
             __syncwarp();
         }
-        // ---- 1b overflow surplus (grouped by k_deliver) and external drive
-        if (go) {
-            const int b0 = (int)roff;
-            if (n_e) {
-                // event times (t_step + u) * dt, u = counter_uniforms(EXTERNAL_TIME, gid, t, j)
-                const uint64_t h4 = cc_splitmix64(cc_splitmix64(sh.h2_time ^ (uint64_t)gid)
-                                                  ^ (uint64_t)t);
-                for (uint32_t k = 0; k < n_e; ++k) {
+        // ---- 1b external drive: event times (t_step + u) * dt with
+        //      u = counter_uniforms(EXTERNAL_TIME, gid, t, j) (engine.py:191-206),
+        //      flattened over the warp (lane owner map in the idle prov buffer)
+        {
+            const uint32_t ne = go ? n_e : 0u;
+            uint32_t etot;
+            const uint32_t eoff = warp_excl_scan(ne, etot);
+            const uint64_t h4 = ne ? cc_splitmix64(cc_splitmix64(sh.h2_time ^ (uint64_t)gid)
+                                                   ^ (uint64_t)t) : 0ull;
+            if (rtot <= (uint32_t)NEURON_WCAP) {
+                uint64_t* hq = reinterpret_cast<uint64_t*>(B.hist + 32);   // [32], idle here
+                uint32_t* eo = B.hist + 96;
+                uint32_t* eb = B.hist + 128;
+                uint8_t* own = reinterpret_cast<uint8_t*>(B.prov);
+                hq[lane] = h4;
+                eo[lane] = eoff;
+                eb[lane] = roff + n_r;
+                for (uint32_t k = 0; k < ne; ++k) own[eoff + k] = (uint8_t)lane;
+                __syncwarp();
+                for (uint32_t f = lane; f < etot; f += 32) {
+                    const int L = own[f];
+                    const uint32_t k = f - eo[L];
+                    const int dst = (int)(eb[L] + k);
+                    Et[dst] = ((double)t + cc_u53(cc_splitmix64(hq[L] ^ (uint64_t)k))) * sh.dt;
+                    Es[dst] = CC_EXT_SRC;
+                    Ew[dst] = 0.0f;
+                    Eo[dst] = (uint8_t)L;
+                }
+            } else {                                    // spilled item: per lane
+                const int b0 = (int)roff;
+                for (uint32_t k = 0; k < ne; ++k) {
                     Et[b0 + n_r + k] = ((double)t + cc_u53(cc_splitmix64(h4 ^ (uint64_t)k))) * sh.dt;
                     Es[b0 + n_r + k] = CC_EXT_SRC;
                     Ew[b0 + n_r + k] = 0.0f;
