@@ -375,12 +375,8 @@ k_plan(const cc_shard sh) {
     const unsigned long long pt0 = gtimer();
     cc_ctl* ctl = sh.ctl;
     const long long t = *(volatile long long*)&ctl->t;
-    // whole blocks stop once the run has failed (the block barriers below
-    // need every warp of a block, so no per-warp early exit)
-    __shared__ unsigned blk_err;
-    if (threadIdx.x == 0) blk_err = *(volatile unsigned*)&ctl->error_bits;
-    __syncthreads();
-    if (blk_err) return;
+    // (after a failed run the plan is still bounded - every write is checked -
+    // and k_stage processes nothing; the block barriers below need all warps)
     const int lane = threadIdx.x & 31;
     const int group0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const bool gvalid = group0 * 32 < sh.n_local;   // warps past the last group idle
