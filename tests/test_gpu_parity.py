@@ -280,6 +280,29 @@ def test_export_matches_reference_store_and_round_trips(cuda):
     assert back.checksum == ex["checksum"] == meta["checksum"]
 
 
+def test_capacity_violation_raises_with_step(cuda):
+    """A device-side capacity violation (here an exchange out-list of one entry)
+    stops every kernel and surfaces as EngineError naming the failing step
+    (the reference's ProtocolViolation / MemoryBudgetError contract)."""
+    from paper_1803_08833_b200 import _lib
+    from paper_1803_08833_b200.engine import Simulator
+    from paper_1803_08833_b200.network import build_b200
+    cfg, meta, arr = golden_run("tiny_gauss")
+    first_step = int(np.floor(arr["raster_times"][0] / cfg.timestep_ms))
+    sim = Simulator(cfg, build_b200(cfg), direct_log=False, use_graphs=False)
+    sim.shard.out_cap = 1
+    with pytest.raises(_lib.EngineError, match=r"step \d+: .*exchange out-list full"):
+        for _ in range(cfg.n_steps):
+            sim._launch_step(__import__("torch").cuda.current_stream().cuda_stream)
+            sim.t += 1
+            sim.check(collect_raster=False)
+    c = sim.ctl()
+    assert c.error_step >= first_step           # not before the first spike
+    rec = int(c.rec_events)
+    sim._launch_step(__import__("torch").cuda.current_stream().cuda_stream)
+    assert int(sim.ctl().rec_events) == rec     # kernels are no-ops after the error
+
+
 def test_zero_duration_is_construction_only(cuda):
     from paper_1803_08833_b200.engine import run_b200
     res = run_b200(tiny_config(duration_s=0.0), 1)
