@@ -161,7 +161,7 @@ __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, i
 #define CC_NEURON_WCAP 256
 #endif
 #ifndef CC_STAGE_WARPS
-#define CC_STAGE_WARPS 2
+#define CC_STAGE_WARPS 4
 #endif
 constexpr int NEURON_WCAP = CC_NEURON_WCAP;   // events per round (8 per lane)
 constexpr int STAGE_WARPS = CC_STAGE_WARPS;
@@ -547,7 +547,7 @@ k_plan(const cc_shard sh) {
 
 // Phase A proper: persistent warps claim work items from the queue.
 #ifndef CC_STAGE_MINB
-#define CC_STAGE_MINB 10
+#define CC_STAGE_MINB 5
 #endif
 __global__ void __launch_bounds__(32 * STAGE_WARPS, CC_STAGE_MINB)
 k_stage(const cc_shard sh) {
