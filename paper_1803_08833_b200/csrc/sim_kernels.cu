@@ -179,8 +179,8 @@ struct StageBuf {
 };
 
 __host__ __device__ constexpr size_t stage_warp_bytes() {
-    return (size_t)NEURON_WCAP * (8 + 4 + 4 + 4 + 2 + 2 + 1 + 1) + HCAP * 4 + 34 * 4
-           + 32 * (8 + 8 + 8 + 4 + 4) + 32;
+    return ((size_t)NEURON_WCAP * (8 + 4 + 4 + 4 + 2 + 2 + 1 + 1) + HCAP * 4 + 34 * 4
+            + 32 * (8 + 8 + 8 + 4 + 4) + 32 + 15) / 16 * 16;     // 16 B aligned per warp
 }
 
 __device__ __forceinline__ StageBuf carve(char* p) {
@@ -285,85 +285,113 @@ __device__ __forceinline__ bool slow_step(NState& s, const cc_pop& P, double tj,
     return false;
 }
 
-// Ordered inputs of one neuron: the 48 B records {t, w}, {em, ec}, {f, 0}
-// written by the staging warps; the next record is loaded while the current
-// one is applied.
-struct Recs {
-    const double2* R;
-    uint32_t n;
-    double2 r0, r1, r2;
-    __device__ __forceinline__ Recs(const double2* R_, uint32_t n_) : R(R_), n(n_) {
-        r0 = __ldcg(R); r1 = __ldcg(R + 1); r2 = __ldcg(R + 2);
-    }
-    __device__ __forceinline__ void fetch(uint32_t i, double& tj, double& wv, double& em,
-                                          double& ec, double& f, double& ecr) {
-        tj = r0.x; wv = r0.y; em = r1.x; ec = r1.y; f = r2.x; ecr = r2.y;
-        if (i + 1 < n) {
-            r0 = __ldcg(R + 3 * (i + 1));
-            r1 = __ldcg(R + 3 * (i + 1) + 1);
-            r2 = __ldcg(R + 3 * (i + 1) + 2);
-        }
-    }
-};
+// In-order update of the 32 neurons of one group (NeuronBlock.integrate_sorted,
+// model.py:289-337), one lane per neuron: affine update, jump, strict
+// threshold, reset, refractory discard, spike emission.  The factors assume the
+// step-start refractory window; after a spike they are recomputed in line
+// (slow_step).  The ordered 48 B records {t, w}, {em, ec}, {f, ecr} are staged
+// into the warp's (idle) shared buffer UB inputs per neuron at a time by
+// cp.async (L2 only), so a neuron's serial chain waits
+// for one L2 round trip per UB inputs instead of one per input.
+constexpr int UB = stage_warp_bytes() / (32 * 48) < 5 ? (int)(stage_warp_bytes() / (32 * 48))
+                                                        : 5;    // inputs per neuron per batch
+constexpr int UB_STRIDE = 3 * UB;        // double2 per lane: 15 = 7 mod 8, conflict-free
+static_assert(32 * UB_STRIDE * 16 <= stage_warp_bytes(), "update batch > stage buffer");
 
-// In-order update of one neuron (NeuronBlock.integrate_sorted, model.py:289-337):
-// affine update, jump, strict threshold, reset, refractory discard, spike
-// emission.  The factors assume the step-start refractory window; after a
-// spike they are recomputed in line (slow_step).
-__device__ __forceinline__ void update_neuron(const cc_shard& sh, int li, uint32_t n,
-                                              long long t, Recs& src, uint32_t& my_spikes) {
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+__device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long long t,
+                                             double2* S, uint32_t& my_spikes) {
     cc_ctl* ctl = sh.ctl;
-    const uint32_t gid = sh.gid[li];
-    const cc_pop& P = sh.pop[neuron_pop(sh, gid)];
-    double* st = sh.state + (size_t)li * 4;
-    const double2 a0 = reinterpret_cast<const double2*>(st)[0];
-    const double2 a1 = reinterpret_cast<const double2*>(st)[1];
-    NState s{a0.x, a0.y, a1.x, a1.y};
+    const int lane = threadIdx.x & 31;
+    const int li = li0 + lane;
+    const uint32_t n = li < sh.n_local ? (uint32_t)sh.ev_n[li] : 0u;
+    const uint32_t off = n ? (uint32_t)__ldcg(&sh.ev_off[li]) : 0u;
+    uint32_t nmax = n;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+    const double2* R = reinterpret_cast<const double2*>(sh.evrec);
+    uint32_t gid = 0;
+    const cc_pop* P = &sh.pop[0];
+    double* st = sh.state + (size_t)(n ? li : 0) * 4;
+    NState s{0.0, 0.0, 0.0, 0.0};
+    if (n) {
+        gid = sh.gid[li];
+        P = &sh.pop[neuron_pop(sh, gid)];
+        const double2 a0 = reinterpret_cast<const double2*>(st)[0];
+        const double2 a1 = reinterpret_cast<const double2*>(st)[1];
+        s = NState{a0.x, a0.y, a1.x, a1.y};
+    }
     const bool cflag = s.c != 0.0;
     bool stale = false;                      // spiked: factors need recomputing
-    for (uint32_t i = 0; i < n; ++i) {
-        double tj, wv, em, ec, f, ecr;
-        src.fetch(i, tj, wv, em, ec, f, ecr);
-        bool spike = false;
-        if (!stale && s.ru <= s.last) {
-            // fast path (no refractory window involved, factors valid):
-            // free_from == last, V_s == V, not refractory; ec = 1, f = 0 when
-            // the neuron started the step without fatigue (c stays 0 then)
-            double Vt = P.E + (s.V - P.E) * em;
-            if (s.c != 0.0) {
-                Vt = Vt - P.sfa * s.c * f;
-                s.c = s.c * ec;
+    const double2* my = S + lane * UB_STRIDE;
+    for (uint32_t b0 = 0; b0 < nmax; b0 += UB) {
+        __syncwarp();                        // previous batch consumed
+        {
+            const double2* Rn = R + 3 * (size_t)(off + b0);
+            const uint32_t m = n > b0 ? min(n - b0, (uint32_t)UB) : 0u;
+#pragma unroll
+            for (int k = 0; k < UB; ++k) {
+                if ((uint32_t)k < m) {
+                    cp_async16(S + lane * UB_STRIDE + 3 * k, Rn + 3 * k);
+                    cp_async16(S + lane * UB_STRIDE + 3 * k + 1, Rn + 3 * k + 1);
+                    cp_async16(S + lane * UB_STRIDE + 3 * k + 2, Rn + 3 * k + 2);
+                }
             }
-            s.last = tj;
-            const double V = Vt + wv;
-            if (V > P.V_theta) spike = true; else s.V = V;
-        } else {
-            spike = slow_step(s, P, tj, stale, cflag, em, ec, f, ecr, wv);
         }
-        if (spike) {                             // strict threshold crossed
-            s.V = P.V_r;
-            s.c = s.c + P.alpha_c;
-            s.ru = tj + P.tau_arp;
-            stale = true;
-            ++my_spikes;
-            if (sh.direct_log) {
-                log_spike(sh, t, gid, tj);
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        const uint32_t e = min(n, b0 + (uint32_t)UB);
+        for (uint32_t i = b0; i < e; ++i) {
+            const double2 r0 = my[3 * (i - b0)], r1 = my[3 * (i - b0) + 1],
+                          r2 = my[3 * (i - b0) + 2];
+            const double tj = r0.x, wv = r0.y, em = r1.x, ec = r1.y, f = r2.x, ecr = r2.y;
+            bool spike = false;
+            if (!stale && s.ru <= s.last) {
+                // fast path (no refractory window involved, factors valid):
+                // free_from == last, V_s == V, not refractory; ec = 1, f = 0 when
+                // the neuron started the step without fatigue (c stays 0 then)
+                double Vt = P->E + (s.V - P->E) * em;
+                if (s.c != 0.0) {
+                    Vt = Vt - P->sfa * s.c * f;
+                    s.c = s.c * ec;
+                }
+                s.last = tj;
+                const double V = Vt + wv;
+                if (V > P->V_theta) spike = true; else s.V = V;
             } else {
-                const unsigned o = atomicAdd(&ctl->out_n, 1u);
-                if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = tj; }
-                else cc_raise(ctl, CC_ERR_OUTLIST, t);
+                spike = slow_step(s, *P, tj, stale, cflag, em, ec, f, ecr, wv);
             }
-            const unsigned long long r = atomicAdd(&ctl->raster_n, 1ull);
-            if (r < (unsigned long long)sh.raster_cap) {
-                sh.raster_gid[r] = gid;
-                sh.raster_t[r] = tj;
-            } else {
-                cc_raise(ctl, CC_ERR_RASTER, t);
+            if (spike) {                             // strict threshold crossed
+                s.V = P->V_r;
+                s.c = s.c + P->alpha_c;
+                s.ru = tj + P->tau_arp;
+                stale = true;
+                ++my_spikes;
+                if (sh.direct_log) {
+                    log_spike(sh, t, gid, tj);
+                } else {
+                    const unsigned o = atomicAdd(&ctl->out_n, 1u);
+                    if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = tj; }
+                    else cc_raise(ctl, CC_ERR_OUTLIST, t);
+                }
+                const unsigned long long rr = atomicAdd(&ctl->raster_n, 1ull);
+                if (rr < (unsigned long long)sh.raster_cap) {
+                    sh.raster_gid[rr] = gid;
+                    sh.raster_t[rr] = tj;
+                } else {
+                    cc_raise(ctl, CC_ERR_RASTER, t);
+                }
             }
         }
     }
-    reinterpret_cast<double2*>(st)[0] = make_double2(s.V, s.c);
-    reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
+    if (n) {
+        reinterpret_cast<double2*>(st)[0] = make_double2(s.V, s.c);
+        reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
+    }
 }
 
 // Planning pass of phase A: per group of 32 neurons, the input counts
@@ -840,13 +868,8 @@ k_stage(const cc_shard sh) {
         if (prev + 1u == sh.grp_items[group]) {
             __threadfence();
             if (lane == 0) sh.grp_done[group] = 0u;
-            const int lg = li0 + lane;
-            const uint32_t ng = lg < sh.n_local ? (uint32_t)sh.ev_n[lg] : 0u;
-            if (ng) {
-                Recs src(reinterpret_cast<const double2*>(sh.evrec)
-                         + 3 * (size_t)__ldcg(&sh.ev_off[lg]), ng);
-                update_neuron(sh, lg, ng, t, src, my_spikes);
-            }
+            update_group(sh, li0, t, reinterpret_cast<double2*>(nsm + wib * stage_warp_bytes()),
+                         my_spikes);
         }
         {
             unsigned smid_;

@@ -246,8 +246,6 @@ class Simulator:
         sh.probe_steps = b["probe_out"].shape[0] if n_probe else 0
         self.shard = sh
         self.n_local = n_local
-        self._graph = None
-        self._graph_steps = 0
         # per-kernel device time of graph-replayed chunks (RunResult.substep_seconds)
         self.substeps = substeps
         self._timer = None
@@ -260,10 +258,29 @@ class Simulator:
         _lib.check(self.L.cc_init_state(C.byref(sh), stream), "cc_init_state")
         _lib.check(self.L.cc_prepare(), "cc_prepare")
         self._graph_t = None
-        if use_graphs:                     # capture once, outside any timed region
-            self._capture(self.chunk, torch.cuda.Stream(dev))
+        self._graphs = [None, None]
+        if use_graphs:
+            # Pipelined chunks (advance): two graphs alternate between two raster
+            # buffers; each ends by snapshotting the counters and emptying the
+            # raster, so the host drains chunk k while chunk k+1 runs.
+            rc2 = max(1024, n_local * bound * self.chunk)
+            b["raster_gid2"] = T.empty(rc2, dtype=i32, device=dev)
+            b["raster_t2"] = T.empty(rc2, dtype=f64, device=dev)
+            b["snap"] = T.zeros((2, b["ctl"].numel()), dtype=i64, device=dev)
+            sh2 = _lib.Shard.from_buffer_copy(sh)
+            sh2.raster_gid, sh2.raster_t = b["raster_gid2"].data_ptr(), b["raster_t2"].data_ptr()
+            sh2.raster_cap = rc2
+            self.shards = [sh, sh2]
+            self._rasters = [(b["raster_gid"], b["raster_t"]), (b["raster_gid2"], b["raster_t2"])]
+            self._snap_host = T.empty((2, b["ctl"].numel()), dtype=i64, pin_memory=True)
+            self._copy_stream = T.cuda.Stream(dev)
+            self._copied = [None, None]
+            self.device_bytes = sum(x.numel() * x.element_size() for x in b.values())
+            # capture once, outside any timed region
+            for i in range(2):
+                self._capture(self.chunk, torch.cuda.Stream(dev), slot=i)
             if substeps:
-                self._capture(self.chunk, torch.cuda.Stream(dev), timed=True)
+                self._capture(self.chunk, torch.cuda.Stream(dev), timed=True, slot=0)
 
     # ------------------------------------------------------------------ steps
     def _launch_step(self, stream) -> None:
@@ -289,31 +306,36 @@ class Simulator:
             self.buf["ctl"][4] = 0
         return c
 
-    def _capture(self, steps: int, stream_obj, timed: bool = False):
-        """The chunk graph; timed: event-record nodes before and after each
-        step's delivery (2 per step + 1 at the end) - used for one sampled
-        chunk only, since the nodes cost ~9 % of the step."""
+    def _capture(self, steps: int, stream_obj, timed: bool = False, slot: int = 0):
+        """The chunk graph of pipeline slot `slot` (its raster buffer), ending
+        with the counter snapshot and the raster reset; timed: event-record
+        nodes before and after each step's delivery (2 per step + 1 at the
+        end) - used for one sampled chunk only, since the nodes cost ~9 % of
+        the step."""
         torch = self.torch
         if timed and self._timer is None:
             self._timer = C.c_void_p()
             _lib.check(self.L.cc_timer_create(2 * steps + 1, C.byref(self._timer)))
         tm = self._timer if timed else None
+        sh = self.shards[slot]
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream_obj):
             s = torch.cuda.current_stream(self.dev).cuda_stream
             for i in range(steps):
                 if tm is not None:
                     _lib.check(self.L.cc_timer_record(tm, 2 * i, s))
-                _lib.check(self.L.cc_deliver(C.byref(self.shard), s), "cc_deliver")
+                _lib.check(self.L.cc_deliver(C.byref(sh), s), "cc_deliver")
                 if tm is not None:
                     _lib.check(self.L.cc_timer_record(tm, 2 * i + 1, s))
-                _lib.check(self.L.cc_neuron_step(C.byref(self.shard), s), "cc_neuron_step")
+                _lib.check(self.L.cc_neuron_step(C.byref(sh), s), "cc_neuron_step")
             if tm is not None:
                 _lib.check(self.L.cc_timer_record(tm, 2 * steps, s))
+            self.buf["snap"][slot].copy_(self.buf["ctl"])
+            self.buf["ctl"][4].zero_()                       # raster_n
         if timed:
             self._graph_t = g
         else:
-            self._graph, self._graph_steps = g, steps
+            self._graphs[slot] = g
         return g
 
     def _read_substeps(self, steps: int) -> None:
@@ -351,27 +373,64 @@ class Simulator:
         return g
 
     def advance(self, n_steps: int, collect_raster: bool = True) -> None:
-        """Run n_steps more steps (chunks replayed from a CUDA graph)."""
-        torch = self.torch
-        done = 0
-        while done < n_steps:
-            k = min(self.chunk, n_steps - done)
-            if self.use_graphs and k == self.chunk:
-                if self._graph is None or self._graph_steps != k:
-                    self._capture(k, torch.cuda.Stream(self.dev))
-                # substep timing on the first graph chunk only
-                timed = self._graph_t is not None and not self.kernel_ms["steps"]
-                (self._graph_t if timed else self._graph).replay()
-            else:
-                s = torch.cuda.current_stream(self.dev).cuda_stream
-                for _ in range(k):
-                    self._launch_step(s)
-                timed = False
+        """Run n_steps more steps: full chunks as pipelined graph replays, the
+        remainder eagerly."""
+        full = n_steps // self.chunk if self.use_graphs else 0
+        if full:
+            self._advance_graphs(full, collect_raster)
+        rest = n_steps - full * self.chunk
+        s = self.torch.cuda.current_stream(self.dev).cuda_stream
+        while rest > 0:
+            k = min(self.chunk, rest)
+            for _ in range(k):
+                self._launch_step(s)
             self.t += k
-            done += k
+            rest -= k
             self.check(collect_raster)
-            if timed:
-                self._read_substeps(k)
+
+    def _advance_graphs(self, n_chunks: int, collect_raster: bool) -> None:
+        """Chunk k runs graph k % 2; the host drains chunk k (counters, errors,
+        raster) on a copy stream while chunk k + 1 runs, and chunk k + 2 waits
+        for that drain before reusing the raster buffer."""
+        torch = self.torch
+        main = torch.cuda.current_stream(self.dev)
+        pend = []
+        for k in range(n_chunks):
+            i = k & 1
+            timed = k == 0 and self._graph_t is not None and not self.kernel_ms["steps"]
+            if self._copied[i] is not None:
+                main.wait_event(self._copied[i])
+            (self._graph_t if timed else self._graphs[i]).replay()
+            ev = torch.cuda.Event()
+            ev.record(main)
+            self.t += self.chunk
+            pend.append((i, ev, timed))
+            if len(pend) == 2:
+                self._drain(*pend.pop(0), collect_raster)
+        while pend:
+            self._drain(*pend.pop(0), collect_raster)
+
+    def _drain(self, i: int, ev, timed: bool, collect_raster: bool) -> None:
+        torch = self.torch
+        cs = self._copy_stream
+        cs.wait_event(ev)
+        with torch.cuda.stream(cs):
+            self._snap_host[i].copy_(self.buf["snap"][i], non_blocking=True)
+        cs.synchronize()
+        c = _lib.Ctl.from_buffer_copy(self._snap_host[i].numpy().tobytes())
+        if c.error_bits:
+            raise _lib.EngineError(f"step {c.error_step}: {_lib.decode_errors(c.error_bits)}")
+        n = int(c.raster_n)
+        if n and collect_raster:
+            rg, rt = self._rasters[i]
+            with torch.cuda.stream(cs):
+                self.raster_g.append(rg[:n].cpu().numpy().view(np.uint32).astype(np.uint64))
+                self.raster_t.append(rt[:n].cpu().numpy())
+        done = torch.cuda.Event()
+        done.record(cs)
+        self._copied[i] = done
+        if timed:
+            self._read_substeps(self.chunk)
 
     def raster(self):
         g = np.concatenate(self.raster_g) if self.raster_g else np.empty(0, np.uint64)

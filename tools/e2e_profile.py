@@ -14,7 +14,7 @@ sim = Simulator(cfg, net, chunk=100)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
 for _ in range(12):
-    sim._graph.replay()
+    sim._graphs[0].replay()
 torch.cuda.synchronize()
 dev = time.perf_counter() - t0
 del sim
