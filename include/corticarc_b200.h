@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 13
+#define CC_ABI_VERSION 14
 
 /* Work items are queued in this many size classes, largest first. */
 #define CC_ITEM_CLASSES 8
@@ -40,9 +40,12 @@ extern "C" {
 /* Constants of one neuron population (model.py:44-86, NeuronBlock
  * per-neuron arrays model.py:243-267).  k1 = tau_c - tau_m and
  * k2 = tau_m * tau_c are pre-evaluated in float64 on the host (identical IEEE
- * results to the reference's in-line expressions, model.py:133). */
+ * results to the reference's in-line expressions, model.py:133); r_* are the
+ * correctly rounded reciprocals 1/tau_m, 1/tau_c, 1/k2 used by the kernels'
+ * exact division by these constants. */
 typedef struct cc_pop {
     double tau_m, tau_c, E, V_theta, V_r, tau_arp, alpha_c, sfa, k1, k2;
+    double r_tau_m, r_tau_c, r_k2;
 } cc_pop;
 
 /* Device-resident loop control and counters (one per shard). */

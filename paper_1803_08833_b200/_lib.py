@@ -15,7 +15,7 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BIT
 
 LIB_PATH = os.environ.get("CC_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 13
+ABI_VERSION = 14
 ITEM_CLASSES = 8
 
 ERR_BITS = {
@@ -36,7 +36,8 @@ class EngineError(RuntimeError):
 
 class Pop(C.Structure):
     _fields_ = [(n, C.c_double) for n in
-                ("tau_m", "tau_c", "E", "V_theta", "V_r", "tau_arp", "alpha_c", "sfa", "k1", "k2")]
+                ("tau_m", "tau_c", "E", "V_theta", "V_r", "tau_arp", "alpha_c", "sfa", "k1", "k2",
+                 "r_tau_m", "r_tau_c", "r_k2")]
 
 
 class Ctl(C.Structure):

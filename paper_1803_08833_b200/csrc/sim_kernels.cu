@@ -50,6 +50,17 @@ __device__ __forceinline__ long long pos_mod(long long a, long long m) {
     return r < 0 ? r + m : r;
 }
 
+// a / b, correctly rounded, for a constant divisor with rb = RN(1/b) (host
+// float64): q0 = RN(a rb) is within 1 ulp of a/b, r = a - q0 b is exact in one
+// FMA, and RN(q0 + r rb) = RN(a/b) (Markstein's theorem; no under/overflow for
+// the time differences and tau constants here).  3 fp64 ops instead of the
+// 14-instruction Newton division with its slow-path check.
+__device__ __forceinline__ double div_rn(double a, double b, double rb) {
+    const double q0 = __dmul_rn(a, rb);
+    const double r = __fma_rn(-q0, b, a);
+    return __fma_rn(r, rb, q0);
+}
+
 // Free evolution of one neuron to time te (NeuronBlock.advance,
 // model.py:272-287 with _voltage_decay, model.py:116-143).
 struct NState { double V, c, last, ru; };
@@ -58,18 +69,18 @@ __device__ __forceinline__ void advance(NState& s, const cc_pop& P, double te) {
     const double ff = fmin(fmax(s.last, s.ru), te);            // free_from
     double cs = s.c;
     if (ff != s.last && cs != 0.0)                             // exp(-0/tau) == 1 exactly
-        cs = cs * exp(-(ff - s.last) / P.tau_c);
+        cs = cs * exp(-div_rn(ff - s.last, P.tau_c, P.r_tau_c));
     const double Vs = (s.last < s.ru) ? P.V_r : s.V;
     const double dt = te - ff;
     // dt == 0: em = exp(-0/tau) = 1 and f = 0 * 1 exactly
-    const double em = dt == 0.0 ? 1.0 : exp(-dt / P.tau_m);
+    const double em = dt == 0.0 ? 1.0 : exp(-div_rn(dt, P.tau_m, P.r_tau_m));
     double Vt = P.E + (Vs - P.E) * em;
     double ct = cs;
     if (cs != 0.0 && dt != 0.0) {
         // with c == 0 the fatigue term is (sfa*0)*f == 0 for the always
         // finite f, and c*ec == 0: both skipped exactly
-        const double ec = exp(-dt / P.tau_c);
-        const double x = dt * P.k1 / P.k2;
+        const double ec = exp(-div_rn(dt, P.tau_c, P.r_tau_c));
+        const double x = div_rn(dt * P.k1, P.k2, P.r_k2);
         double f;
         if (x == 0.0)
             f = dt * em;
@@ -212,10 +223,10 @@ __device__ __forceinline__ void decay_factors(const cc_pop& P, double dt, bool w
         em = 1.0;
         return;
     }
-    em = exp(-dt / P.tau_m);
+    em = exp(-div_rn(dt, P.tau_m, P.r_tau_m));
     if (with_c) {
-        ec = exp(-dt / P.tau_c);
-        const double x = dt * P.k1 / P.k2;
+        ec = exp(-div_rn(dt, P.tau_c, P.r_tau_c));
+        const double x = div_rn(dt * P.k1, P.k2, P.r_k2);
         if (x == 0.0)
             f = dt * em;
         else if (fabs(x) <= 1.0)
@@ -258,7 +269,7 @@ __device__ __forceinline__ bool slow_step(NState& s, const cc_pop& P, double tj,
     const double ff = fmin(fmax(s.last, s.ru), tj);
     double cs = s.c;
     if (ff != s.last && cs != 0.0) {                  // leaving / inside a refractory window
-        if (stale) cs = cs * exp(-(ff - s.last) / P.tau_c);
+        if (stale) cs = cs * exp(-div_rn(ff - s.last, P.tau_c, P.r_tau_c));
         else cs = cs * ecr0;
     }
     double emj = em0, ecj = ec0, fj = f0;
@@ -850,7 +861,7 @@ k_stage(const cc_shard sh) {
                 const cc_pop& P = sh.pop[fl & 1u];
                 decay_factors(P, te - ff, (fl & 2u) != 0, em, ec, f);
                 // fatigue decay over the refractory part of the gap (slow_step)
-                const double ecr = (ff != last && (fl & 2u)) ? exp(-(ff - last) / P.tau_c) : 1.0;
+                const double ecr = (ff != last && (fl & 2u)) ? exp(-div_rn(ff - last, P.tau_c, P.r_tau_c)) : 1.0;
                 const double wv = (Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
                 R[3 * p] = make_double2(te, wv);
                 R[3 * p + 1] = make_double2(em, ec);

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional
@@ -105,6 +106,7 @@ def _pop(p) -> _lib.Pop:
     q.sfa = p.g_c / p.C_m
     q.k1 = p.tau_c - p.tau_m
     q.k2 = p.tau_m * p.tau_c
+    q.r_tau_m, q.r_tau_c, q.r_k2 = 1.0 / q.tau_m, 1.0 / q.tau_c, 1.0 / q.k2
     return q
 
 
@@ -128,7 +130,7 @@ class Simulator:
     """One shard's device state and step loop."""
 
     def __init__(self, cfg, net: DeviceNetwork, *, probes=None, probe_steps: int = 0,
-                 bin_cap: Optional[int] = None, piece_len: int = 256, chunk: int = 100,
+                 bin_cap: Optional[int] = None, piece_len: Optional[int] = None, chunk: int = 100,
                  use_graphs: bool = True, direct_log: Optional[bool] = None,
                  raster_steps: Optional[int] = None, substeps: bool = False, device=None):
         import torch
@@ -148,6 +150,8 @@ class Simulator:
         if bin_cap is None:
             bin_cap = default_bin_cap(cfg)
         n_groups = (n_local + 31) // 32
+        if piece_len is None:                 # tuning knob (tools/sweep_variants.py)
+            piece_len = int(os.environ.get("CC_PIECE_LEN", "256"))
         self.chunk = max(1, int(chunk))
         self.use_graphs = use_graphs
         direct = (net.size == 1) if direct_log is None else direct_log
