@@ -447,7 +447,9 @@ k_plan(const cc_shard sh) {
             if (v[u] != 0xffffffffu) atomicAdd(&lane_cnt[wib][v[u] & 31u], 1u);
     }
     const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + o0;
-    for (uint32_t r = lane; r < c_ovf; r += 32) atomicAdd(&lane_cnt[wib][ov[r].y], 1u);
+    // (& 31: after an overflow-list error the slots of dropped records hold
+    // stale data; the run is failed then, but shared memory stays in bounds)
+    for (uint32_t r = lane; r < c_ovf; r += 32) atomicAdd(&lane_cnt[wib][ov[r].y & 31u], 1u);
     __syncwarp();
     if (lane == 0 && gvalid) {
         sh.grp_n[group] = c_list + c_ovf;

@@ -303,6 +303,21 @@ def test_capacity_violation_raises_with_step(cuda):
     assert int(sim.ctl().rec_events) == rec     # kernels are no-ops after the error
 
 
+def test_runaway_raises_without_fault(cuda):
+    """Runaway activity (BASELINE config 1 at 200 Hz drive) fills the ring's
+    overflow list within ~10 steps and must end in EngineError, not a device
+    fault: the step's planning pass reads the overflow slots of dropped
+    records, which hold stale data (this faulted before the lane mask)."""
+    import torch
+    from paper_1803_08833_b200 import _lib
+    from paper_1803_08833_b200.engine import run_b200
+    from paper_1803_08833_b200.presets import baseline_config
+    cfg = baseline_config(1, "calibrated", drive_hz=200.0, duration_s=0.03)
+    with pytest.raises(_lib.EngineError, match=r"step \d+: .*overflow list full"):
+        run_b200(cfg, 1)
+    torch.cuda.synchronize()                    # no device fault
+
+
 def test_zero_duration_is_construction_only(cuda):
     from paper_1803_08833_b200.engine import run_b200
     res = run_b200(tiny_config(duration_s=0.0), 1)
