@@ -192,9 +192,11 @@ def config_block(cfg, net, args):
             "grid": f"{cfg.grid.nx}x{cfg.grid.ny}", "neurons": cfg.grid.n_neurons,
             "synapses": int(net.n_synapses) if net is not None else None,
             "kernel": cfg.kernel.kind, "drive_hz": cfg.external.rate_per_synapse_hz,
-            "j_inh_mv": cfg.genspec.j_inh_exc, "dt_ms": cfg.timestep_ms, "seed": cfg.seed,
-            "l2": "no flush between steps: per-step working set is scattered over the "
-                  "CSR (0.86 GB at config 1) + delay ring (> 126 MB L2)",
+            "j_inh_mv": cfg.genspec.j_inh_exc, "j_inh_inh_mv": cfg.genspec.j_inh_inh,
+            "dt_ms": cfg.timestep_ms, "seed": cfg.seed,
+            "l2": "no flush between steps: the per-step working set (CSR rows of the "
+                  "spiking sources, delay ring, spike log; 0.86 GB CSR at config 1) is "
+                  "scattered over more than the 126 MB L2",
             "parallelism": f"column blocks over {args.gpus} GPU(s)"}
 
 
@@ -283,7 +285,9 @@ def bench_single(args):
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("k_deliver", {}).get("dram_bytes_per_launch")
+            prof_d = json.load(open(prof))
+            traffic = prof_d.get(f"config{args.config}", {}).get("k_deliver", {}).get(
+                "dram_bytes_per_launch")
         except Exception:
             traffic = None
     kernels = {

@@ -22,14 +22,21 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 14
+#define CC_ABI_VERSION 17
 
 /* Work items are queued in this many size classes, largest first. */
+/* Input lists per 32-neuron group (events of delay d go to sub-list
+ * d % CC_SUBLISTS) and the largest stride (u32 words) between their fill
+ * counters the host allocates for. */
+#ifndef CC_SUBLISTS
+#define CC_SUBLISTS 1
+#endif
+#define CC_CNT_STRIDE_MAX 64
 #define CC_ITEM_CLASSES 8
 
 /* error bits raised by kernels into cc_ctl.error_bits */
 #define CC_ERR_SPIKE_LOG      0x01u  /* more spikes in one step than log capacity   */
-#define CC_ERR_PIECES         0x02u  /* delivery work list full                     */
+#define CC_ERR_DSEG           0x02u  /* CSR row longer than 65535 (delay segments)  */
 #define CC_ERR_OVERFLOW_BIN   0x04u  /* overflow record list full                   */
 #define CC_ERR_SCRATCH        0x08u  /* event staging scratch exhausted             */
 #define CC_ERR_POISSON        0x10u  /* Poisson draw budget exceeded (engine.py:187)*/
@@ -81,13 +88,13 @@ typedef struct cc_shard {
     int32_t n_local;        /* neurons owned                                   */
     int32_t n_col;          /* neurons per column                              */
     int32_t n_exc_col;      /* excitatory slots per column                     */
-    int32_t d_max;          /* delay ring slots (SimConfig.d_max)              */
-    int32_t bin_cap;        /* records per (slot, 32-neuron group) list        */
+    int32_t d_max;          /* SimConfig.d_max (delays 1..d_max steps)          */
+    int32_t bin_cap;        /* records per input sub-list (per group and step)  */
     int32_t log_slots;      /* d_max + 1                                       */
     int32_t spk_cap;        /* spike-log entries per step (a power of two)     */
-    int32_t piece_len;      /* synapses per delivery work piece                */
-    int64_t ovf_cap;        /* overflow records per slot                       */
-    int64_t piece_cap;      /* delivery pieces per step                        */
+    int32_t seg_stride;     /* u16 per delay-segment table row: >= d_max + 1, %8 == 0 */
+    int64_t ovf_cap;        /* overflow records per step                       */
+    int64_t pad64_;
     int64_t raster_cap;     /* raster entries                                  */
     int64_t scratch_cap;    /* staging events (global spill, 56 B each)        */
     int64_t n_rows;         /* CSR rows (= global neuron count)                */
@@ -115,25 +122,38 @@ typedef struct cc_shard {
     const float* syn_w;     /* [S] weight, mV                                  */
     const uint8_t* syn_d;   /* [S] delay, steps                                */
 
-    /* delay ring of event records (DelayRing, engine.py:124-163): one append
-     * list per (arrival slot, group of 32 consecutive neurons); a record is
-     * (spike_ref << 5 | lane) | w_bits << 32 */
+    /* input lists of the current step (DelayRing.drain's bucket,
+     * engine.py:151-163): one append list per group of 32 consecutive neurons,
+     * filled by cc_deliver with the events arriving this step; a record is
+     * (spike_ref << 5 | lane) | w_bits << 32.  The delay ring proper is the
+     * spike log below: step t delivers the delay-d segment of every spike of
+     * step t - d (rows are sorted by delay, network.py:257). */
     int32_t n_groups;       /* ceil(n_local / 32)                              */
-    int32_t pad_g;
-    uint32_t* bin_cnt;      /* [d_max][n_groups] list fill                      */
-    uint64_t* bin_rec;      /* [d_max][n_groups][bin_cap]                      */
-    uint32_t* grp_n;        /* [n_groups] inputs of the current slot per group  */
-    uint32_t* ovf_rec;      /* [d_max][ovf_cap][4] {group, lane, spike_ref, w_bits} */
-    uint32_t* ovf_cnt;      /* [d_max]                                         */
-    uint32_t* ovf_sorted;   /* [ovf_cap][4] overflow of the current slot, grouped by group */
+    int32_t bin_pad;        /* unused records after each list: list stride is
+                               bin_cap + bin_pad (staggers the list starts over
+                               L2 slices / DRAM channels)                      */
+    uint32_t* bin_cnt;      /* [n_groups][CC_SUBLISTS][stride] sub-list fill (word 0) */
+    uint64_t* bin_rec;      /* [n_groups][CC_SUBLISTS][bin_cap + bin_pad]      */
+    uint32_t* grp_n;        /* [n_groups] inputs of the current step per group  */
+    uint32_t* grp_sub;      /* [n_groups][CC_SUBLISTS] records kept per sub-list */
+    uint32_t* ovf_rec;      /* [ovf_cap][4] {group, lane, spike_ref, w_bits}   */
+    uint32_t* ovf_cnt;      /* [1]                                             */
+    uint32_t* ovf_sorted;   /* [ovf_cap][4] overflow of the current step, grouped by group */
     int32_t* ovf_off;       /* [n_groups] start of a group's run in ovf_sorted  */
     int32_t* ovf_fill;      /* [n_groups] grouping cursors (zero between steps) */
 
-    /* spike log (AER payloads, network.py:60-63) and delivery work list */
+    /* spike log (AER payloads, network.py:60-63), one slot per emission step,
+     * log_slots = d_max + 1; each entry carries its row start and the row's
+     * delay-segment offsets (copied from dseg when the spike is logged) */
     double* log_t;          /* [log_slots][spk_cap]                            */
     uint32_t* log_gid;      /* [log_slots][spk_cap]                            */
-    unsigned long long* log_ctr; /* [log_slots] (pieces << 32) | spikes        */
-    uint32_t* pieces;       /* [2][piece_cap][4] {syn_lo, syn_hi, ref, count}  */
+    unsigned long long* log_ctr; /* [log_slots] spikes logged                  */
+    unsigned long long* log_len; /* [log_slots] sum of their row lengths (the
+                               reference's recurrent_events, engine.py:366)     */
+    int64_t* log_r0;        /* [log_slots][spk_cap] CSR row start              */
+    uint16_t* log_dseg;     /* [log_slots][spk_cap][seg_stride]                */
+    const uint16_t* dseg;   /* [n_rows][seg_stride]: dseg[r][d] = synapses of row
+                               r with delay <= d (d = 0..d_max), cc_build_dseg */
 
     /* outputs */
     uint32_t* raster_gid;   /* [raster_cap]                                    */
@@ -179,10 +199,12 @@ int cc_timer_destroy(void* handle);
  * Replaces engine.py:297-302 and NeuronBlock.__init__ (model.py:263-267). */
 int cc_init_state(const cc_shard* sh, void* stream);
 
-/* Step phase (3): arborise the spikes emitted in step t-1 (the log slot the
- * previous cc_neuron_step or cc_ingest filled) into the delay ring.
- * Replaces the expand block engine.py:338-367 and DelayRing.insert
- * (engine.py:138-149). */
+/* Step phase (3): deliver the events arriving in step t - the delay-d segment
+ * of the row of every spike logged for step t - d, d = 1..d_max - into the
+ * step's per-group input lists; adds the row lengths of step t-1's spikes to
+ * ctl->rec_events.  Replaces the expand block engine.py:338-367 with
+ * DelayRing.insert/drain (engine.py:138-163): the same events reach the same
+ * step, expanded at arrival instead of at emission. */
 int cc_deliver(const cc_shard* sh, void* stream);
 
 /* One-time launch configuration of the step kernels (shared-memory opt-in,
@@ -216,9 +238,18 @@ int cc_pack_aer(const cc_shard* sh, const uint32_t* dest_mask_by_local, int32_t 
                 int32_t cap, int64_t* send, const int32_t* local_of_col, void* stream);
 
 /* Multi-shard receive of n_src packed slots (same layout): log the received
- * spikes of step ctl->t - 1 (cuts their local rows into delivery pieces). */
+ * spikes of step ctl->t - 1 that have rows on this shard. */
 int cc_ingest_aer(const cc_shard* sh, const int64_t* recv, int32_t n_src, int32_t cap,
                   void* stream);
+
+/* CC_SUBLISTS as compiled (hosts size bin_cnt / bin_rec / grp_sub with it). */
+int32_t cc_sublists(void);
+
+/* Delay-segment table of a CSR whose rows are sorted by delay: out[r][d] =
+ * synapses of row r with delay <= d, d = 0..d_max (u16, row stride `stride`).
+ * Sets *err (CC_ERR_DSEG) if a row exceeds 65535 synapses. */
+int cc_build_dseg(const int64_t* row_off, const uint8_t* syn_d, int64_t n_rows, int32_t d_max,
+                  int32_t stride, uint16_t* out, unsigned* err, void* stream);
 
 /* ------------------------------------------------- connectivity generator */
 /* Philox4x64-10 generator of the incoming-synapse CSR of one shard, bit-exact

@@ -15,13 +15,14 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BIT
 
 LIB_PATH = os.environ.get("CC_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 14
+ABI_VERSION = 17
 ITEM_CLASSES = 8
+CNT_STRIDE_MAX = 64          # bin_cnt words per group allocated (CC_CNT_STRIDE <= this)
 
 ERR_BITS = {
     0x01: "spike log full (more spikes in one step than planned)",
-    0x02: "delivery work list full",
-    0x04: "delay-ring overflow list full",
+    0x02: "CSR row longer than 65535 synapses (delay-segment table)",
+    0x04: "input-list overflow list full",
     0x08: "event staging scratch exhausted",
     0x10: "Poisson draw budget exceeded (engine.py:187)",
     0x20: "raster buffer full",
@@ -60,8 +61,8 @@ class Shard(C.Structure):
     _fields_ = [
         ("n_local", C.c_int32), ("n_col", C.c_int32), ("n_exc_col", C.c_int32),
         ("d_max", C.c_int32), ("bin_cap", C.c_int32), ("log_slots", C.c_int32),
-        ("spk_cap", C.c_int32), ("piece_len", C.c_int32),
-        ("ovf_cap", C.c_int64), ("piece_cap", C.c_int64), ("raster_cap", C.c_int64),
+        ("spk_cap", C.c_int32), ("seg_stride", C.c_int32),
+        ("ovf_cap", C.c_int64), ("pad64_", C.c_int64), ("raster_cap", C.c_int64),
         ("scratch_cap", C.c_int64), ("n_rows", C.c_int64),
         ("out_cap", C.c_int32), ("ext_budget", C.c_int32), ("n_probe", C.c_int32),
         ("direct_log", C.c_int32), ("debug_skip", C.c_int32), ("pad_", C.c_int32),
@@ -70,10 +71,11 @@ class Shard(C.Structure):
         ("pop", Pop * 2),
         ("gid", _P), ("state", _P),
         ("row_off", _P), ("syn_tgt", _P), ("syn_w", _P), ("syn_d", _P),
-        ("n_groups", C.c_int32), ("pad_g", C.c_int32),
-        ("bin_cnt", _P), ("bin_rec", _P), ("grp_n", _P), ("ovf_rec", _P), ("ovf_cnt", _P),
+        ("n_groups", C.c_int32), ("bin_pad", C.c_int32),
+        ("bin_cnt", _P), ("bin_rec", _P), ("grp_n", _P), ("grp_sub", _P), ("ovf_rec", _P), ("ovf_cnt", _P),
         ("ovf_sorted", _P), ("ovf_off", _P), ("ovf_fill", _P),
-        ("log_t", _P), ("log_gid", _P), ("log_ctr", _P), ("pieces", _P),
+        ("log_t", _P), ("log_gid", _P), ("log_ctr", _P), ("log_len", _P),
+        ("log_r0", _P), ("log_dseg", _P), ("dseg", _P),
         ("raster_gid", _P), ("raster_t", _P), ("out_gid", _P), ("out_t", _P),
         ("scratch", _P), ("ev_n", _P), ("ev_nr", _P),
         ("evrec", _P), ("evrec_cap", C.c_int64), ("ev_off", _P), ("grp_items", _P),
@@ -118,6 +120,8 @@ _SIGS = {
     "cc_gen_fill": (C.c_int, [C.POINTER(Gen), _P, C.c_int64, _P, _P, _P, _P, _P, _P,
                               C.c_int64, _P, _P]),
     "cc_gen_warps": (C.c_int64, []),
+    "cc_build_dseg": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]),
+    "cc_sublists": (C.c_int32, []),
     "cc_csr_checksum": (C.c_int, [_P, _P, C.c_int64, _P, _P, _P, C.c_int32, C.c_int32, _P, _P]),
     "cc_test_philox": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_int32,
                                  _P, _P]),
@@ -146,6 +150,11 @@ def load_library(path: str = LIB_PATH):
                               f"{getattr(L, name)()} != {C.sizeof(st)}")
     _lib = L
     return L
+
+
+def sublists() -> int:
+    """Input sub-lists per neuron group, as compiled into the library."""
+    return int(load_library().cc_sublists())
 
 
 def lib():

@@ -14,6 +14,21 @@
 #include <climits>
 #include "cc_common.cuh"
 
+// cache-policy experiments (tools/sweep_variants.py): evict-first CSR loads in
+// k_deliver, evict-first ordered-input records in k_stage
+// list fill counters CC_CNT_STRIDE words apart: a step's reservations (one
+// atomic per run) hit n_groups counters, which a dense array would put in a
+// handful of L2 slices
+#ifndef CC_CNT_STRIDE
+#define CC_CNT_STRIDE 64
+#endif
+#ifndef CC_CSR_STREAM
+#define CC_CSR_STREAM 0
+#endif
+#ifndef CC_EVREC_STREAM
+#define CC_EVREC_STREAM 0
+#endif
+
 namespace {
 
 
@@ -110,31 +125,52 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t& total) 
     return x - v;
 }
 
-// Append one spike to the delivery log of emission step t (slot e) and cut
-// its CSR row into work pieces for the next step's k_deliver.
+// A group's input lists: CC_SUBLISTS sub-lists (delivery of delay d appends to
+// sub-list d % CC_SUBLISTS, spreading the reservation atomics over more
+// counters), read as one concatenation.  init: lane j < CC_SUBLISTS holds the
+// record count of sub-list j; every lane gets the exclusive prefix.
+constexpr int NSUB = CC_SUBLISTS;
+struct SubMap {
+    uint32_t pre[NSUB + 1];
+    __device__ __forceinline__ void init(uint32_t cj) {
+        uint32_t x = 0;
+#pragma unroll
+        for (int j = 0; j < NSUB; ++j) { pre[j] = x; x += __shfl_sync(0xffffffffu, cj, j); }
+        pre[NSUB] = x;
+    }
+    // record index of concatenated position r (< pre[NSUB]) in the group's region
+    __device__ __forceinline__ size_t at(uint32_t r, size_t ks) const {
+        int j = 0;
+        uint32_t base = 0;
+#pragma unroll
+        for (int i = 1; i < NSUB; ++i)
+            if (r >= pre[i]) { j = i; base = pre[i]; }
+        return (size_t)j * ks + (r - base);
+    }
+};
+
+// Append one spike to the log slot of emission step t: time, gid, row start
+// and the row's delay-segment offsets (the delay-d part of its row is
+// delivered in step t + d).  len == 0: no synapse on this shard.
 __device__ __forceinline__ void log_spike(const cc_shard& sh, long long t, uint32_t gid,
                                           double te) {
     const int64_t r0 = sh.row_off[gid];
     const int64_t len = sh.row_off[gid + 1] - r0;
-    if (len == 0) return;                       // no synapse on this shard
+    if (len == 0) return;
     const int e = (int)pos_mod(t, sh.log_slots);
-    const unsigned long long np = (unsigned long long)((len + sh.piece_len - 1) / sh.piece_len);
-    const unsigned long long old = atomicAdd(&sh.log_ctr[e], (np << 32) | 1ull);
-    const unsigned long long idx = old & 0xffffffffull;
-    const unsigned long long pb = old >> 32;
-    if (idx >= (unsigned long long)sh.spk_cap || pb + np > (unsigned long long)sh.piece_cap) {
-        cc_raise(sh.ctl, idx >= (unsigned long long)sh.spk_cap ? CC_ERR_SPIKE_LOG : CC_ERR_PIECES, t);
+    const unsigned long long idx = atomicAdd(&sh.log_ctr[e], 1ull);
+    if (idx >= (unsigned long long)sh.spk_cap) {
+        cc_raise(sh.ctl, CC_ERR_SPIKE_LOG, t);
         return;
     }
+    atomicAdd(&sh.log_len[e], (unsigned long long)len);
     const uint32_t ref = (uint32_t)(e * sh.spk_cap + idx);
     sh.log_t[ref] = te;
     sh.log_gid[ref] = gid;
-    uint4* pcs = reinterpret_cast<uint4*>(sh.pieces) + (size_t)(t & 1) * sh.piece_cap + pb;
-    for (unsigned long long k = 0; k < np; ++k) {
-        const int64_t s0 = r0 + (int64_t)k * sh.piece_len;
-        const int64_t cnt = min((int64_t)sh.piece_len, len - (int64_t)k * sh.piece_len);
-        pcs[k] = make_uint4((uint32_t)s0, (uint32_t)((uint64_t)s0 >> 32), ref, (uint32_t)cnt);
-    }
+    sh.log_r0[ref] = r0;
+    const uint4* src = reinterpret_cast<const uint4*>(sh.dseg + (size_t)gid * sh.seg_stride);
+    uint4* dst = reinterpret_cast<uint4*>(sh.log_dseg + (size_t)ref * sh.seg_stride);
+    for (int j = 0; j < sh.seg_stride / 8; ++j) dst[j] = src[j];
 }
 
 __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, int t_mod_l) {
@@ -422,25 +458,31 @@ k_plan(const cc_shard sh) {
     const int group = gvalid ? group0 : 0;
     const int li = group * 32 + lane;
     const bool active = gvalid && li < sh.n_local;
-    const int slot = (int)pos_mod(t, sh.d_max);
-    // inputs from the ring: count this slot's records of the group per lane
+    // inputs of this step: count the group's list records per lane
     __shared__ uint32_t lane_cnt[4][32];
     const int wib = threadIdx.x >> 5;
     lane_cnt[wib][lane] = 0u;
     const uint32_t K = (uint32_t)sh.bin_cap;
-    uint32_t* gc = sh.bin_cnt + (size_t)slot * sh.n_groups + group;
-    const uint32_t c_all = gvalid ? *gc : 0u;
-    const uint32_t c_list = min(c_all, K);
+    const size_t KS = (size_t)K + sh.bin_pad;
+    uint32_t* gcb = sh.bin_cnt + (size_t)group * NSUB * CC_CNT_STRIDE;
+    const uint32_t cj_all = (gvalid && lane < NSUB) ? gcb[lane * CC_CNT_STRIDE] : 0u;
+    const uint32_t cj = min(cj_all, K);
+    SubMap M;
+    M.init(cj);
+    const uint32_t c_list = M.pre[NSUB];
+    uint32_t ovf_all = cj_all - cj;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ovf_all += __shfl_xor_sync(0xffffffffu, ovf_all, o);
     const long long o0 = sh.ovf_off[group];
-    const uint32_t c_ovf = c_all > K ? (uint32_t)max(0ll, min((long long)(c_all - K), sh.ovf_cap - o0)) : 0u;
+    const uint32_t c_ovf = ovf_all ? (uint32_t)max(0ll, min((long long)ovf_all, sh.ovf_cap - o0)) : 0u;
     __syncwarp();
-    const uint64_t* lst = sh.bin_rec + ((size_t)slot * sh.n_groups + group) * K;
+    const uint64_t* lst = sh.bin_rec + (size_t)group * NSUB * KS;
     for (uint32_t r0 = 0; r0 < c_list; r0 += 32 * 8) {
         uint32_t v[8];                             // 8 loads in flight per lane
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const uint32_t r = r0 + u * 32 + lane;
-            v[u] = r < c_list ? (uint32_t)lst[r] : 0xffffffffu;   // ref < 2^27: never all-ones
+            v[u] = r < c_list ? (uint32_t)lst[M.at(r, KS)] : 0xffffffffu;   // ref < 2^27: never all-ones
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u)
@@ -451,10 +493,11 @@ k_plan(const cc_shard sh) {
     // stale data; the run is failed then, but shared memory stays in bounds)
     for (uint32_t r = lane; r < c_ovf; r += 32) atomicAdd(&lane_cnt[wib][ov[r].y & 31u], 1u);
     __syncwarp();
-    if (lane == 0 && gvalid) {
-        sh.grp_n[group] = c_list + c_ovf;
-        *gc = 0u;                                  // drain the ring slot (read back via grp_n)
+    if (gvalid && lane < NSUB) {
+        gcb[lane * CC_CNT_STRIDE] = 0u;            // drain the lists (read back via grp_sub)
+        sh.grp_sub[(size_t)group * NSUB + lane] = cj;
     }
+    if (lane == 0 && gvalid) sh.grp_n[group] = c_list + c_ovf;
     const unsigned long long pt1 = gtimer();
     uint32_t n_r = 0, n_e = 0;
     if (active) {
@@ -582,7 +625,7 @@ k_plan(const cc_shard sh) {
         unsigned smid_;
         asm volatile("mov.u32 %0, %smid;" : "=r"(smid_));
         d_[0] = pt0; d_[1] = pt1; d_[2] = pt2; d_[3] = pt3; d_[4] = gtimer();
-        d_[5] = smid_; d_[6] = c_all; d_[7] = (unsigned long long)ni;
+        d_[5] = smid_; d_[6] = c_list + c_ovf; d_[7] = (unsigned long long)ni;
     }
 }
 
@@ -598,8 +641,6 @@ k_stage(const cc_shard sh) {
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     StageBuf B = carve(nsm + wib * stage_warp_bytes());
-    const int D = sh.d_max;
-    const int slot = (int)pos_mod(t, D);
     const int t_mod_l = (int)pos_mod(t, sh.log_slots);
     const uint32_t K = (uint32_t)sh.bin_cap;
     const double t0 = (double)t * sh.dt;
@@ -687,8 +728,11 @@ k_stage(const cc_shard sh) {
         //      the group's run of the grouped overflow), keep the item's lanes
         {
             const uint32_t c_all = sh.grp_n[group];
-            const uint32_t c_list = min(c_all, K);
-            const uint64_t* lst = sh.bin_rec + ((size_t)slot * sh.n_groups + group) * K;
+            SubMap M;
+            M.init(lane < NSUB ? sh.grp_sub[(size_t)group * NSUB + lane] : 0u);
+            const uint32_t c_list = M.pre[NSUB];
+            const size_t KS = (size_t)K + sh.bin_pad;
+            const uint64_t* lst = sh.bin_rec + (size_t)group * NSUB * KS;
             const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + sh.ovf_off[group];
             B.hist[lane] = 0u;                          // per-lane fill cursors
             __syncwarp();
@@ -699,7 +743,7 @@ k_stage(const cc_shard sh) {
                     const uint32_t r = r0 + u * 32 + lane;
                     rec[u] = ~0ull;
                     if (r < c_list) {
-                        rec[u] = lst[r];
+                        rec[u] = lst[M.at(r, KS)];
                     } else if (r < c_all) {
                         const uint4 q = ov[r - c_list];
                         rec[u] = (uint64_t)((q.z << 5) | q.y) | ((uint64_t)q.w << 32);
@@ -843,7 +887,7 @@ k_stage(const cc_shard sh) {
         unsigned long long rbase = 0;
         if (lane == 0 && rtot) {
             rbase = atomicAdd(&ctl->stream_used, (unsigned long long)rtot);
-            // cannot happen: evrec_cap covers a full ring slot + overflow + drive
+            // evrec_cap covers a step's expected list capacity + overflow + drive
             if (rbase + rtot > (unsigned long long)sh.evrec_cap) cc_raise(ctl, CC_ERR_SCRATCH, t);
         }
         rbase = __shfl_sync(0xffffffffu, rbase, 0);
@@ -865,9 +909,15 @@ k_stage(const cc_shard sh) {
                 // fatigue decay over the refractory part of the gap (slow_step)
                 const double ecr = (ff != last && (fl & 2u)) ? exp(-div_rn(ff - last, P.tau_c, P.r_tau_c)) : 1.0;
                 const double wv = (Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
+#if CC_EVREC_STREAM
+                __stcs(R + 3 * p, make_double2(te, wv));
+                __stcs(R + 3 * p + 1, make_double2(em, ec));
+                __stcs(R + 3 * p + 2, make_double2(f, ecr));
+#else
                 R[3 * p] = make_double2(te, wv);
                 R[3 * p + 1] = make_double2(em, ec);
                 R[3 * p + 2] = make_double2(f, ecr);
+#endif
             }
         }
         if (go) sh.ev_off[li] = (int32_t)(rbase + roff);
@@ -907,7 +957,7 @@ k_stage(const cc_shard sh) {
         __threadfence();
         if (atomicAdd(&ctl->done_stage, 1u) == gridDim.x - 1) {
             ctl->done_stage = 0;
-            sh.ovf_cnt[slot] = 0;              // ring slot t fully consumed
+            sh.ovf_cnt[0] = 0;                 // step t's inputs fully consumed
             __threadfence();
             *(volatile long long*)&ctl->t = t + 1;
         }
@@ -943,14 +993,21 @@ __device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
     __shared__ uint32_t carry;
     const int n = sh.n_groups;
     const uint32_t K = (uint32_t)sh.bin_cap;
-    const uint32_t* cnt = sh.bin_cnt + (size_t)s * n;
+    const uint32_t* cnt = sh.bin_cnt;                 // (s: single step since pull delivery)
+    (void)s;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     for (int base = 0; base < n; base += blockDim.x) {
         const int i = base + threadIdx.x;
-        const uint32_t c = i < n ? cnt[i] : 0u;
-        const uint32_t v = c > K ? c - K : 0u;
+        uint32_t v = 0u;
+        if (i < n) {
+#pragma unroll
+            for (int j = 0; j < NSUB; ++j) {
+                const uint32_t c = cnt[((size_t)i * NSUB + j) * CC_CNT_STRIDE];
+                v += c > K ? c - K : 0u;
+            }
+        }
         uint32_t x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -986,7 +1043,13 @@ __device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
     for (unsigned j = threadIdx.x; j < m; j += blockDim.x) sh.ovf_fill[rec[j].x] = 0;
 }
 
-// One warp per delivery piece (<= piece_len synapses of one spiking source).
+// Delivery of step t (pull): the events arriving at t are the delay-d segments
+// of the rows of the spikes of step t - d, d = 1..d_max.  A work unit is
+// (d, 4 consecutive spikes of log slot t - d); each spike's segment is walked
+// by 8 lanes, U synapses per lane per pass, software-pipelined (the next
+// pass's or unit's CSR loads are issued before this pass's reservations and
+// deposits).  Deposits go to the step's per-group lists, which stay L2
+// resident from here to k_plan / k_stage.
 #ifndef CC_DEL_THREADS
 #define CC_DEL_THREADS 256
 #endif
@@ -994,16 +1057,28 @@ __device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
 #define CC_DEL_MINB 2
 #endif
 #ifndef CC_DEL_U
-#define CC_DEL_U 8          // synapses per lane per pipelined unit
+#define CC_DEL_U 8          // synapses per lane per pass
 #endif
+constexpr int DEL_SPU = 4;                  // spikes per unit (8 lanes each)
+constexpr int DEL_DMAX = 256;               // d_max <= 255 (uint8 delays)
+
 __global__ void __launch_bounds__(CC_DEL_THREADS, CC_DEL_MINB)
 k_deliver(const cc_shard sh) {
     const unsigned long long dbg_t0 = gtimer();
     cc_ctl* ctl = sh.ctl;
     const long long t = *(volatile long long*)&ctl->t;
     if (*(volatile unsigned*)&ctl->error_bits) return;      // failed run: stop working
+    const int L = sh.log_slots, D = sh.d_max;
+    __shared__ unsigned s_n[DEL_DMAX], s_pre[DEL_DMAX + 1];
+    for (int k = threadIdx.x; k < D; k += blockDim.x)
+        s_n[k] = (unsigned)min(sh.log_ctr[pos_mod(t - 1 - k, L)], (unsigned long long)sh.spk_cap);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        sh.log_ctr[pos_mod(t, sh.log_slots)] = 0ull;   // the slot k_neuron(t) fills
+        // recurrent_events: row lengths of the spikes of step t - 1, counted at
+        // their expansion step like engine.py:366
+        const unsigned long long ev = sh.log_len[pos_mod(t - 1, L)];
+        if (ev) atomicAdd(&ctl->rec_events, ev);
+        sh.log_ctr[pos_mod(t, L)] = 0ull;      // the slot k_stage(t) fills (step t - d_max - 1)
+        sh.log_len[pos_mod(t, L)] = 0ull;
         ctl->scratch_used = 0ull;
         ctl->stream_used = 0ull;
         ctl->n_rounds = 0u;
@@ -1011,131 +1086,148 @@ k_deliver(const cc_shard sh) {
 #pragma unroll
         for (int c = 0; c < CC_ITEM_CLASSES; ++c) ctl->cls_n[c] = 0u;
     }
-    const int ep = (int)pos_mod(t - 1, sh.log_slots);
-    const unsigned long long n_pieces = sh.log_ctr[ep] >> 32;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned acc = 0;
+        for (int k = 0; k < D; ++k) { s_pre[k] = acc; acc += (s_n[k] + DEL_SPU - 1) / DEL_SPU; }
+        s_pre[D] = acc;
+    }
+    __syncthreads();
+    const unsigned n_units = s_pre[D];
     const int lane = threadIdx.x & 31;
-    const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-    const uint4* pcs = reinterpret_cast<const uint4*>(sh.pieces) + (size_t)((t - 1) & 1) * sh.piece_cap;
-    const int D = sh.d_max;
-    const int base = (int)pos_mod(t - 1, D);
+    const int sl = lane & 7;                                 // lane within the spike's 8
+    const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned nw = (gridDim.x * blockDim.x) >> 5;
     const int NG = sh.n_groups;
     const int K = sh.bin_cap;
+    const size_t KS = (size_t)K + sh.bin_pad;
     const int32_t* __restrict__ tgt_a = sh.syn_tgt;
     const float* __restrict__ w_a = sh.syn_w;
-    const uint8_t* __restrict__ d_a = sh.syn_d;
-    unsigned long long events = 0;
     const unsigned long long dbg_t1 = gtimer();
-    // Software pipeline over 128-synapse units of this warp's pieces (p = wid,
-    // wid + nw, ...): the next unit's descriptor and CSR loads are issued
-    // before the current unit's reservations and deposits.
     constexpr int U = CC_DEL_U;
-    const long long np_ = (long long)n_pieces;
-    long long p = wid;
-    uint4 pc = p < np_ ? pcs[p] : make_uint4(0, 0, 0, 0);
-    long long pn = p + nw;
-    uint4 pcn = pn < np_ ? pcs[pn] : make_uint4(0, 0, 0, 0);
-    int j0 = 0;
-    int tg[U], sl[U];
-    float w[U];
-    auto load_unit = [&](const uint4& q, int jb, int* tg_, int* sl_, float* w_) {
-        const size_t b0 = (size_t)q.x | ((size_t)q.y << 32);
-        const int cnt = (int)q.w;
+    constexpr int SPAN = 8 * U;                              // synapses per spike per pass
+    // unit u -> delay index k (monotone cursor: a warp's units increase) and
+    // this lane's spike: segment start, length, log reference
+    int kc = 0;
+    auto unit_desc = [&](unsigned u, uint64_t& st, uint32_t& ln, uint32_t& rf, int& kk) {
+        while (s_pre[kc + 1] <= u) ++kc;                     // s_pre[D] = n_units > u
+        kk = kc;
+        const unsigned idx = (u - s_pre[kc]) * DEL_SPU + (unsigned)(lane >> 3);
+        st = 0; ln = 0; rf = 0;
+        if (idx < s_n[kc]) {
+            const int e = (int)pos_mod(t - 1 - kc, L);
+            rf = (uint32_t)(e * sh.spk_cap + idx);
+            const uint16_t* ds = sh.log_dseg + (size_t)rf * sh.seg_stride;
+            const uint32_t a = __ldg(ds + kc), b = __ldg(ds + kc + 1);   // delay kc + 1
+            st = (uint64_t)__ldg(sh.log_r0 + rf) + a;
+            ln = b - a;
+        }
+    };
+    auto warp_max = [](uint32_t v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+        return v;
+    };
+    auto load_pass = [&](uint64_t st, uint32_t ln, int p, int* tg_, float* w_) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int j = jb + u * 32 + lane;
-            sl_[u] = -1;
-            if (j < cnt) {
-                const size_t si = b0 + j;
-                tg_[u] = __ldg(tgt_a + si);
-                w_[u] = __ldg(w_a + si);
-                const int s = base + (int)__ldg(d_a + si);
-                sl_[u] = s >= D ? s - D : s;
+            const uint32_t j = (uint32_t)(p * SPAN + u * 8 + sl);
+            tg_[u] = -1;
+            if (j < ln) {
+                tg_[u] = __ldg(tgt_a + st + j);
+                w_[u] = __ldg(w_a + st + j);
             }
         }
     };
-    if (p < np_) load_unit(pc, 0, tg, sl, w);
-    while (p < np_) {
-        // next unit: rest of this piece, else the next piece of this warp
-        long long p2 = p;
-        uint4 pc2 = pc;
-        int j2 = j0 + 32 * U;
-        const bool adv = j2 >= (int)pc.w;
-        if (adv) { p2 = pn; pc2 = pcn; j2 = 0; }
-        int tg2[U], sl2[U];
+    unsigned u = wid;
+    uint64_t st = 0, stn = 0;
+    uint32_t ln = 0, rf = 0, lnn = 0, rfn = 0;
+    int kcur = 0, kn = 0;
+    if (u < n_units) unit_desc(u, st, ln, rf, kcur);
+    if (u + nw < n_units) unit_desc(u + nw, stn, lnn, rfn, kn);
+    uint32_t lmax = warp_max(ln);
+    int p = 0;
+    int tg[U];
+    float w[U];
+    if (u < n_units) load_pass(st, ln, 0, tg, w);
+    while (u < n_units) {
+        // next pass of this unit, else the first pass of the warp's next unit
+        unsigned u2 = u;
+        int p2 = p + 1;
+        uint64_t st2 = st;
+        uint32_t ln2 = ln, rf2 = rf, lmax2 = lmax;
+        int k2 = kcur;
+        const bool adv = (uint32_t)(p2 * SPAN) >= lmax;
+        if (adv) {
+            u2 = u + nw; p2 = 0; st2 = stn; ln2 = lnn; rf2 = rfn; k2 = kn;
+            lmax2 = warp_max(lnn);
+        }
+        int tg2[U];
         float w2[U];
-        if (p2 < np_) load_unit(pc2, j2, tg2, sl2, w2);
+        if (u2 < n_units) load_pass(st2, ln2, p2, tg2, w2);
         else {
 #pragma unroll
-            for (int u = 0; u < U; ++u) sl2[u] = -1;
+            for (int k = 0; k < U; ++k) tg2[k] = -1;
         }
-        if (adv) {
-            pn = p2 + nw;
-            if (pn < np_) pcn = pcs[pn];
-        }
-        if (j0 == 0) events += (unsigned long long)pc.w;
-        const uint32_t ref = pc.z;
-        // one atomic per run of consecutive lanes with the same (slot, group)
-        // key: rows are sorted by (delay, target), so a warp's 32 synapses form
-        // 1-3 runs; runs are found with a shuffle and a ballot (any split into
-        // equal-key runs is a valid reservation; __match_any_sync costs ~56 SM
-        // cycles with many distinct keys, tools/micro/match.cu)
+        if (adv && u2 + nw < n_units) unit_desc(u2 + nw, stn, lnn, rfn, kn);
+        const int sub = kcur % NSUB;             // sub-list of this unit's delay
+        // one atomic per run of consecutive lanes with the same group: a
+        // segment is sorted by target (network.py:257), so a spike's 8 lanes
+        // form 1-3 runs; runs are found with a shuffle and a ballot
         unsigned key[U], pos[U], got[U];
         int lead[U];
         const unsigned upto = 0xffffffffu >> (31 - lane);      // bits 0..lane
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            key[u] = sl[u] >= 0 ? (unsigned)(sl[u] * NG + (tg[u] >> 5)) : 0xffffffffu;
-            const unsigned prev = __shfl_up_sync(0xffffffffu, key[u], 1);
-            const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || key[u] != prev);
-            lead[u] = 31 - __clz(heads & upto);
+        for (int k = 0; k < U; ++k) {
+            key[k] = tg[k] >= 0 ? (unsigned)(tg[k] >> 5) : 0xffffffffu;
+            const unsigned prev = __shfl_up_sync(0xffffffffu, key[k], 1);
+            const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || key[k] != prev);
+            lead[k] = 31 - __clz(heads & upto);
             const unsigned after = heads & ~upto;
             const int end = after ? __ffs(after) - 1 : 32;
-            got[u] = 0u;
-            if (sl[u] >= 0 && lane == lead[u])
-                got[u] = atomicAdd(&sh.bin_cnt[key[u]], (unsigned)(end - lead[u]));
+            got[k] = 0u;
+            if (tg[k] >= 0 && lane == lead[k]) {
+                if (sh.debug_skip & 1024) got[k] = 0u;       // timing experiment: no reservation
+                else got[k] = atomicAdd(&sh.bin_cnt[((size_t)key[k] * NSUB + sub) * CC_CNT_STRIDE],
+                                        (unsigned)(end - lead[k]));
+            }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-            pos[u] = __shfl_sync(0xffffffffu, got[u], lead[u]) + (unsigned)(lane - lead[u]);
+        for (int k = 0; k < U; ++k)
+            pos[k] = __shfl_sync(0xffffffffu, got[k], lead[k]) + (unsigned)(lane - lead[k]);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (sl[u] < 0) continue;
-            const uint32_t lig = (uint32_t)tg[u] & 31u;
-            if (pos[u] < (unsigned)K) {
-                sh.bin_rec[(size_t)key[u] * K + pos[u]] =
-                    (uint64_t)((ref << 5) | lig) | ((uint64_t)__float_as_uint(w[u]) << 32);
+        for (int k = 0; k < U; ++k) {
+            if (tg[k] < 0 || (sh.debug_skip & 2048)) continue;  // 2048: timing, no deposit
+            const uint32_t lig = (uint32_t)tg[k] & 31u;
+            if (pos[k] < (unsigned)K) {
+                sh.bin_rec[((size_t)key[k] * NSUB + sub) * KS + pos[k]] =
+                    (uint64_t)((rf << 5) | lig) | ((uint64_t)__float_as_uint(w[k]) << 32);
             } else {
-                const unsigned o = atomicAdd(&sh.ovf_cnt[sl[u]], 1u);
+                const unsigned o = atomicAdd(&sh.ovf_cnt[0], 1u);
                 atomicAdd(&ctl->ovf_total, 1ull);
                 if (o < (unsigned)sh.ovf_cap) {
-                    reinterpret_cast<uint4*>(sh.ovf_rec)[(size_t)sl[u] * sh.ovf_cap + o] =
-                        make_uint4((uint32_t)tg[u] >> 5, lig, ref, __float_as_uint(w[u]));
+                    reinterpret_cast<uint4*>(sh.ovf_rec)[o] =
+                        make_uint4(key[k], lig, rf, __float_as_uint(w[k]));
                 } else {
                     cc_raise(ctl, CC_ERR_OVERFLOW_BIN, t);
                 }
             }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) { tg[u] = tg2[u]; sl[u] = sl2[u]; w[u] = w2[u]; }
-        p = p2; pc = pc2; j0 = j2;
+        for (int k = 0; k < U; ++k) { tg[k] = tg2[k]; w[k] = w2[k]; }
+        u = u2; p = p2; st = st2; ln = ln2; rf = rf2; lmax = lmax2; kcur = k2;
     }
+    (void)NG;
     if ((sh.debug_skip & 256) && lane == 0) {
         unsigned long long* d_ = reinterpret_cast<unsigned long long*>(sh.scratch)
                                  + (size_t)sh.scratch_cap * 7 - 65536ull * 8 - (size_t)(wid + 1) * 4;
         unsigned smid_;
         asm volatile("mov.u32 %0, %smid;" : "=r"(smid_));
-        d_[0] = dbg_t0; d_[1] = dbg_t1; d_[2] = gtimer(); d_[3] = (unsigned long long)smid_ | ((unsigned long long)n_pieces << 32);
+        d_[0] = dbg_t0; d_[1] = dbg_t1; d_[2] = gtimer(); d_[3] = (unsigned long long)smid_ | ((unsigned long long)n_units << 32);
     }
-    __shared__ unsigned long long blk_ev;
-    if (threadIdx.x == 0) blk_ev = 0;
-    __syncthreads();
-    if (lane == 0 && events) atomicAdd(&blk_ev, events);
-    __syncthreads();
-    if (threadIdx.x == 0 && blk_ev) atomicAdd(&ctl->rec_events, blk_ev);
 
-    // Arrival step t is complete now (k_deliver(t) is its last depositor): the
-    // last block out groups its overflow records by target for k_neuron(t).
+    // Step t's inputs are complete now (k_deliver(t) is their only depositor):
+    // the last block out groups the overflow records by group for k_plan(t).
     __shared__ bool am_last;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1150,11 +1242,37 @@ k_deliver(const cc_shard sh) {
     }
     if (!am_last) return;
     __threadfence();
-    const int s = (int)pos_mod(t, D);
-    const unsigned m = min(*(volatile unsigned*)&sh.ovf_cnt[s], (unsigned)sh.ovf_cap);
+    const unsigned m = min(*(volatile unsigned*)&sh.ovf_cnt[0], (unsigned)sh.ovf_cap);
     if (threadIdx.x == 0) { ctl->done_deliver = 0; ctl->ovf_grouped = m; }
     if (m == 0) return;
-    group_overflow(sh, s, m);
+    group_overflow(sh, 0, m);
+}
+
+// Delay-segment table: dseg[r][d] = synapses of row r with delay <= d,
+// d = 0..d_max (rows sorted by delay).  One warp per row.
+__global__ void k_build_dseg(const int64_t* row_off, const uint8_t* syn_d, int64_t n_rows,
+                             int d_max, int stride, uint16_t* out, unsigned* err) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_rows;
+         r += nwarp) {
+        const int64_t a = row_off[r];
+        const int64_t len = row_off[r + 1] - a;
+        uint16_t* o = out + (size_t)r * stride;
+        if (len > 65535) {
+            if (lane == 0) atomicOr(err, CC_ERR_DSEG);
+            continue;
+        }
+        // delay d starts at the first j with syn_d[j] >= d: lane j writes
+        // o[d] = j for d in (syn_d[j-1], syn_d[j]]; the rest is len
+        for (int64_t j = lane; j < len; j += 32) {
+            const int dj = syn_d[a + j];
+            const int dp = j ? (int)syn_d[a + j - 1] : 0;
+            for (int d = dp; d < dj; ++d) o[d] = (uint16_t)j;
+        }
+        const int dl = len ? (int)syn_d[a + len - 1] : 0;
+        for (int d = dl + lane; d < stride; d += 32) o[d] = (uint16_t)len;
+    }
 }
 
 // Multi-shard receive: log the AER events of step ctl->t - 1 that have rows here.
@@ -1244,6 +1362,20 @@ static int sm_count() {
         if (n <= 0) n = 148;
     }
     return n;
+}
+
+extern "C" int32_t cc_sublists(void) { return CC_SUBLISTS; }
+
+extern "C" int cc_build_dseg(const int64_t* row_off, const uint8_t* syn_d, int64_t n_rows,
+                             int32_t d_max, int32_t stride, uint16_t* out, unsigned* err,
+                             void* stream) {
+    if (d_max < 1 || d_max >= DEL_DMAX || stride < d_max + 1 || stride % 8)
+        return cc_set_error("cc_build_dseg: need 1 <= d_max < %d, stride >= d_max + 1, "
+                            "stride %% 8 == 0", DEL_DMAX);
+    if (n_rows <= 0) return 0;
+    k_build_dseg<<<sm_count() * 8, 256, 0, (cudaStream_t)stream>>>(row_off, syn_d, n_rows, d_max,
+                                                                   stride, out, err);
+    return cc_check_launch("k_build_dseg");
 }
 
 extern "C" int cc_init_state(const cc_shard* sh, void* stream) {

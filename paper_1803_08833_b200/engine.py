@@ -130,7 +130,7 @@ class Simulator:
     """One shard's device state and step loop."""
 
     def __init__(self, cfg, net: DeviceNetwork, *, probes=None, probe_steps: int = 0,
-                 bin_cap: Optional[int] = None, piece_len: Optional[int] = None, chunk: int = 100,
+                 bin_cap: Optional[int] = None, chunk: int = 100,
                  use_graphs: bool = True, direct_log: Optional[bool] = None,
                  raster_steps: Optional[int] = None, substeps: bool = False, device=None):
         import torch
@@ -147,11 +147,14 @@ class Simulator:
         n_local = len(gids)
         D = cfg.d_max
         bound = _spikes_per_step_bound(cfg)
-        if bin_cap is None:
-            bin_cap = default_bin_cap(cfg)
+        step_cap = default_bin_cap(cfg)        # records per group and step
+        if bin_cap is None:                    # per sub-list: 2x an even share
+            bin_cap = max(256, 2 * step_cap // _lib.sublists())
         n_groups = (n_local + 31) // 32
-        if piece_len is None:                 # tuning knob (tools/sweep_variants.py)
-            piece_len = int(os.environ.get("CC_PIECE_LEN", "256"))
+        # list stride bin_cap + bin_pad records: with a power-of-two stride the
+        # appends of one step (same small offsets in thousands of lists) land in
+        # few L2 slices / DRAM channels
+        bin_pad = int(os.environ.get("CC_BIN_PAD", "0"))
         self.chunk = max(1, int(chunk))
         self.use_graphs = use_graphs
         direct = (net.size == 1) if direct_log is None else direct_log
@@ -161,32 +164,38 @@ class Simulator:
         spk_cap = 1 << (spk_cap - 1).bit_length()     # power of two: ref -> slot is a shift
         if spk_cap * (D + 1) >= 2 ** 32:
             raise MemoryBudgetError("spike log references exceed 32 bits")
-        piece_cap = max(1, net.pieces_upper_bound(piece_len) * bound)
         ovf_cap = max(4096, n_local * 8)
         if spk_cap * (D + 1) >= 2 ** 27:
             raise MemoryBudgetError("spike log references exceed the 27 bits of a ring record")
+        seg_stride = (D + 1 + 7) // 8 * 8
+        dseg = net.delay_segments(D, seg_stride)
         raster_cap = max(1024, n_local * bound * max(self.chunk, raster_steps or 0))
         scratch_cap = max(1 << 16, n_local * 16)
-        # ordered-input records of one step: at most a full ring slot, its
-        # overflow list and every neuron's Poisson budget
+        # ordered-input records of one step: the expected list capacity of a step,
+        # the overflow list and every neuron's Poisson budget (beyond it the
+        # step fails with "event staging scratch exhausted")
         lam = cfg.external.mean_per_step(cfg.timestep_ms)
         ext_m = int(math.ceil(lam + 12.0 * math.sqrt(lam))) + 20 if lam > 0 else 0
-        evrec_cap = n_groups * bin_cap + ovf_cap + n_local * ext_m
+        evrec_cap = n_groups * step_cap + ovf_cap + n_local * ext_m
         self.buf = dict(
             gid=T.from_numpy(gids.astype(np.uint32).view(np.int32)).to(dev),
             state=T.zeros((n_local, 4), dtype=f64, device=dev),
-            bin_cnt=T.zeros((D, n_groups), dtype=i32, device=dev),
-            bin_rec=T.empty((D, n_groups, bin_cap), dtype=i64, device=dev),
+            bin_cnt=T.zeros(n_groups * _lib.sublists() * _lib.CNT_STRIDE_MAX, dtype=i32,
+                            device=dev),
+            bin_rec=T.empty((n_groups, _lib.sublists(), bin_cap + bin_pad), dtype=i64, device=dev),
             grp_n=T.zeros(n_groups, dtype=i32, device=dev),
-            ovf_rec=T.empty((D, ovf_cap, 4), dtype=i32, device=dev),
-            ovf_cnt=T.zeros(D, dtype=i32, device=dev),
+            grp_sub=T.zeros((n_groups, _lib.sublists()), dtype=i32, device=dev),
+            ovf_rec=T.empty((ovf_cap, 4), dtype=i32, device=dev),
+            ovf_cnt=T.zeros(1, dtype=i32, device=dev),
             ovf_sorted=T.empty((ovf_cap, 4), dtype=i32, device=dev),
             ovf_off=T.zeros(n_groups, dtype=i32, device=dev),
             ovf_fill=T.zeros(n_groups, dtype=i32, device=dev),
             log_t=T.empty((D + 1, spk_cap), dtype=f64, device=dev),
             log_gid=T.empty((D + 1, spk_cap), dtype=i32, device=dev),
             log_ctr=T.zeros(D + 1, dtype=i64, device=dev),
-            pieces=T.empty((2, piece_cap, 4), dtype=i32, device=dev),
+            log_len=T.zeros(D + 1, dtype=i64, device=dev),
+            log_r0=T.empty((D + 1, spk_cap), dtype=i64, device=dev),
+            log_dseg=T.empty((D + 1, spk_cap, seg_stride), dtype=T.int16, device=dev),
             raster_gid=T.empty(raster_cap, dtype=i32, device=dev),
             raster_t=T.empty(raster_cap, dtype=f64, device=dev),
             out_gid=T.empty(max(1, n_local * bound), dtype=i32, device=dev),
@@ -216,9 +225,9 @@ class Simulator:
         sh = _lib.Shard()
         sh.n_local, sh.n_col, sh.n_exc_col = n_local, n, grid.n_excitatory_per_column
         sh.d_max, sh.bin_cap, sh.log_slots = D, bin_cap, D + 1
-        sh.n_groups = n_groups
-        sh.spk_cap, sh.piece_len = spk_cap, piece_len
-        sh.ovf_cap, sh.piece_cap, sh.raster_cap = ovf_cap, piece_cap, raster_cap
+        sh.n_groups, sh.bin_pad = n_groups, bin_pad
+        sh.spk_cap, sh.seg_stride = spk_cap, seg_stride
+        sh.ovf_cap, sh.raster_cap = ovf_cap, raster_cap
         sh.scratch_cap, sh.n_rows = scratch_cap, grid.n_neurons
         sh.evrec_cap = evrec_cap
         sh.round_cap = ((n_local + 31) // 32) * 32
@@ -240,10 +249,11 @@ class Simulator:
         sh.pop[1] = _pop(cfg.inh_params)
         sh.gid, sh.state = b["gid"].data_ptr(), b["state"].data_ptr()
         sh.row_off, sh.syn_tgt = net.row_off.data_ptr(), net.syn_tgt.data_ptr()
+        sh.dseg = dseg.data_ptr()
         sh.syn_w, sh.syn_d = net.syn_w.data_ptr(), net.syn_d.data_ptr()
-        for k in ("bin_cnt", "bin_rec", "grp_n", "ovf_rec", "ovf_cnt", "ovf_sorted", "ovf_off",
-                  "ovf_fill", "log_t", "log_gid", "log_ctr",
-                  "pieces", "raster_gid", "raster_t", "out_gid", "out_t", "scratch",
+        for k in ("bin_cnt", "bin_rec", "grp_n", "grp_sub", "ovf_rec", "ovf_cnt", "ovf_sorted", "ovf_off",
+                  "ovf_fill", "log_t", "log_gid", "log_ctr", "log_len", "log_r0", "log_dseg",
+                  "raster_gid", "raster_t", "out_gid", "out_t", "scratch",
                   "ev_n", "ev_nr", "rounds", "evrec", "ev_off", "grp_items", "grp_done",
                   "probe_map", "probe_out", "ctl"):
             setattr(sh, k, b[k].data_ptr())

@@ -46,7 +46,7 @@ class DeviceNetwork:
     checksum: int                 # wire-record checksum of the records stored here
     construction_seconds: float
     row_len_max: int
-    piece_bound: dict = field(default_factory=dict)   # cached per piece_len
+    dseg_cache: dict = field(default_factory=dict)    # delay-segment tables per (d_max, stride)
 
     @property
     def n_local(self) -> int:
@@ -61,13 +61,27 @@ class DeviceNetwork:
     def peak_bytes(self) -> int:
         return self.steady_bytes + 4 * len(self.src_gids) * 3
 
-    def pieces_upper_bound(self, piece_len: int) -> int:
-        """Delivery pieces if every source with a row spiked once."""
-        if piece_len not in self.piece_bound:
+    def delay_segments(self, d_max: int, stride: int):
+        """[n_rows, stride] int16 (u16 bits) table: synapses of each row with
+        delay <= d, d = 0..d_max (rows are sorted by delay, network.py:257);
+        the delivery kernel reads a spike's delay-d segment from it."""
+        key = (d_max, stride)
+        if key not in self.dseg_cache:
             import torch
-            ln = self.row_off[1:] - self.row_off[:-1]
-            self.piece_bound[piece_len] = int(((ln + piece_len - 1) // piece_len).sum().item())
-        return self.piece_bound[piece_len]
+            from . import _lib
+            L = _lib.lib()
+            n_rows = self.row_off.numel() - 1
+            out = torch.zeros((max(1, n_rows), stride), dtype=torch.int16,
+                              device=self.row_off.device)
+            err = torch.zeros(1, dtype=torch.int32, device=self.row_off.device)
+            stream = torch.cuda.current_stream(self.row_off.device).cuda_stream
+            _lib.check(L.cc_build_dseg(self.row_off.data_ptr(), self.syn_d.data_ptr(), n_rows,
+                                       d_max, stride, out.data_ptr(), err.data_ptr(), stream),
+                       "cc_build_dseg")
+            if int(err.item()):
+                raise _lib.EngineError("cc_build_dseg: " + _lib.decode_errors(int(err.item())))
+            self.dseg_cache[key] = out
+        return self.dseg_cache[key]
 
     def nonempty_rows(self) -> int:
         ln = self.row_off[1:] - self.row_off[:-1]

@@ -304,17 +304,18 @@ def test_capacity_violation_raises_with_step(cuda):
 
 
 def test_runaway_raises_without_fault(cuda):
-    """Runaway activity (BASELINE config 1 at 200 Hz drive) fills the ring's
-    overflow list within ~10 steps and must end in EngineError, not a device
-    fault: the step's planning pass reads the overflow slots of dropped
-    records, which hold stale data (this faulted before the lane mask)."""
+    """Runaway activity (BASELINE config 1 at 400 Hz drive, small input lists)
+    fills the overflow list within a few steps and must end in EngineError, not
+    a device fault: the step's planning pass reads the overflow slots of
+    dropped records, which hold stale data (this faulted before the lane
+    mask)."""
     import torch
     from paper_1803_08833_b200 import _lib
     from paper_1803_08833_b200.engine import run_b200
     from paper_1803_08833_b200.presets import baseline_config
-    cfg = baseline_config(1, "calibrated", drive_hz=200.0, duration_s=0.03)
+    cfg = baseline_config(1, "calibrated", drive_hz=400.0, duration_s=0.1)
     with pytest.raises(_lib.EngineError, match=r"step \d+: .*overflow list full"):
-        run_b200(cfg, 1)
+        run_b200(cfg, 1, bin_cap=64)            # small lists: the overflow list fills first
     torch.cuda.synchronize()                    # no device fault
 
 

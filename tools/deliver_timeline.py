@@ -19,8 +19,9 @@ sim.advance(400)
 L = sim.L
 st = torch.cuda.current_stream().cuda_stream
 nw = 148 * 2 * 8
+extra = int(os.environ.get("DBG", "0"))
 for rep in range(3):
-    sim.shard.debug_skip = 256
+    sim.shard.debug_skip = 256 | extra
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     _lib.check(L.cc_deliver(C.byref(sim.shard), st))
@@ -35,9 +36,9 @@ for rep in range(3):
     start = (tail[:, 0] - t0) / 1e3
     setup = (tail[:, 1] - tail[:, 0]) / 1e3
     loop = (tail[:, 2] - tail[:, 1]) / 1e3
-    npieces = tail[0, 3] >> 32
-    busy = np.arange(nw) < npieces
-    print(f"rep {rep}: event-timed {e0.elapsed_time(e1)*1e3:.1f} us, pieces {npieces}, span {((tail[:,2]-t0)/1e3).max():.1f} us")
+    nunits = tail[0, 3] >> 32          # work units (delay, 4 spikes)
+    busy = np.arange(nw) < nunits
+    print(f"rep {rep}: event-timed {e0.elapsed_time(e1)*1e3:.1f} us, units {nunits}, span {((tail[:,2]-t0)/1e3).max():.1f} us")
     print(f"  warp start: p50 {np.median(start):.2f} max {start.max():.2f}; setup p50 {np.median(setup):.2f} max {setup.max():.2f}")
     print(f"  loop (busy warps): p50 {np.median(loop[busy]):.2f} p90 {np.percentile(loop[busy],90):.2f} max {loop[busy].max():.2f}")
     nb = 148 * 2

@@ -26,12 +26,9 @@ lam = cfg.external.mean_per_step(cfg.timestep_ms)
 stats = []
 for t in range(400, 440):
     _lib.check(L.cc_deliver(C.byref(sim.shard), st))
-    torch.cuda.synchronize()
-    nr = sim.buf["bin_cnt"][t % cfg.d_max].cpu().numpy().astype(np.int64)
-    ne = poisson_counts(cfg.seed, sim.gids.astype(np.uint64), t, lam)
-    n = nr + ne
     _lib.check(L.cc_neuron_step(C.byref(sim.shard), st))
     torch.cuda.synchronize()
+    n = sim.buf["ev_n"].cpu().numpy().astype(np.int64)      # inputs per neuron (ring + drive)
     w = n[: len(n) // 32 * 32].reshape(-1, 32)
     stats.append(dict(t=t, mean=float(n.mean()), max=int(n.max()), e2e=float((n * n).sum() / max(1, n.sum())),
                       warp_max_sum=int(w.max(1).sum()), warp_sum=int(w.sum()),

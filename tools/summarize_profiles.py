@@ -9,13 +9,16 @@ import sys
 from collections import defaultdict
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+config = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 src = os.path.join(root, "gpurun_out")
 dst = os.path.join(root, "profiles")
 os.makedirs(dst, exist_ok=True)
 
 # --- launch list: share of step time per kernel (steady state = last 400 launches of step kernels)
-rows = [r for r in csv.reader(open(os.path.join(src, f"{tag}_launches.csv"))) if len(r) > 5]
+have_launches = os.path.exists(os.path.join(src, f"{tag}_launches.csv"))
+rows = [r for r in csv.reader(open(os.path.join(src, f"{tag}_launches.csv"))) if len(r) > 5] \
+    if have_launches else [["Kernel Name", "Metric Value", "Metric Unit", "", "", ""]]
 h = rows[0]
 ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
 launches = []
@@ -33,10 +36,13 @@ for k, v in tail:
     agg[k][0] += 1
     agg[k][1] += v
 tot = sum(a[1] for a in agg.values())
-with open(os.path.join(dst, f"{tag}_launches.md"), "w") as fh:
+with open(os.path.join(dst, f"{tag}_launches.md") if have_launches else os.devnull, "w") as fh:
     fh.write(f"# {tag}: ncu launch list (gpu__time_duration, --clock-control none)\n\n")
-    fh.write("Command: `python bench.py --steps 100 --warmup 400 --no-cpu --no-e2e "
-             "--instrument-steps 10` under `ncu --metrics gpu__time_duration.sum`.\n"
+    fh.write(("Command: `python bench.py --steps 100 --warmup 400 --no-cpu --no-e2e "
+              "--instrument-steps 10`" if config == 1 else
+              f"Command: `python bench.py --config {config} --steps 20 --warmup 200 --no-cpu "
+              "--no-e2e --instrument-steps 5`") +
+             " under `ncu --metrics gpu__time_duration.sum`.\n"
              "Serialised, cold-cache per-launch times: compare SHARES, not absolutes.\n\n")
     fh.write(f"Total launches captured: {len(launches)}; step-kernel launches: {len(step_k)}; "
              f"summary over the last {len(tail)} step-kernel launches.\n\n")
@@ -67,11 +73,13 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
-        "lts__t_bytes.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]
+        "lts__t_bytes.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "lts__t_sector_hit_rate.pct", "lts__t_sectors_srcunit_tex_op_atom.sum",
+        "lts__t_sectors_srcunit_tex_op_write.sum", "lts__t_sectors_srcunit_tex_op_read.sum"]
 units = raw[1]
 summary = {}
 with open(os.path.join(dst, f"{tag}_kernels.md"), "w") as fh:
-    fh.write(f"# {tag}: ncu --set full, steady-state step kernels (launch ~1350+)\n\n")
+    fh.write(f"# {tag}: ncu --set full, steady-state step kernels, BASELINE config {config}\n\n")
     for r in raw[2:]:
         name = r[h.index("Kernel Name")].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
         d = {}
@@ -81,7 +89,12 @@ with open(os.path.join(dst, f"{tag}_kernels.md"), "w") as fh:
         fh.write(f"## {name}\n\n| metric | value | unit |\n|---|---|---|\n")
         for k, (v, u) in d.items():
             fh.write(f"| {k} | {v} | {u} |\n")
-        fh.write("\n")
+        st = sorted(((h[i].replace("smsp__average_warps_issue_stalled_", "")
+                      .replace("_per_issue_active.ratio", ""), float(r[i] or 0))
+                     for i in range(len(h)) if h[i].startswith("smsp__average_warps_issue_stalled_")
+                     and h[i].endswith("_per_issue_active.ratio")), key=lambda x: -x[1])[:6]
+        fh.write("\nwarp stall cycles per issued instruction: "
+                 + ", ".join(f"{k} {v:.2f}" for k, v in st) + "\n\n")
 
         def num(k):
             v, u = d.get(k, ("0", ""))
@@ -89,9 +102,15 @@ with open(os.path.join(dst, f"{tag}_kernels.md"), "w") as fh:
             return x * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1}.get(u, 1)
         summary[name.split("<")[0]] = {
             "dram_bytes_per_launch": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
-            "duration_us_ncu": float(d["gpu__time_duration.sum"][0].replace(",", "")) /
-            (1e3 if d["gpu__time_duration.sum"][1] in ("nsecond", "ns") else 1),
+            "duration_us_ncu": float(d["gpu__time_duration.sum"][0].replace(",", "")) *
+            {"nsecond": 1e-3, "ns": 1e-3, "msecond": 1e3, "ms": 1e3}.get(
+                d["gpu__time_duration.sum"][1], 1.0),
             "source": f"profiles/{tag}_kernels.md"}
-json.dump(summary, open(os.path.join(dst, "ncu_summary.json"), "w"), indent=1)
-print(open(os.path.join(dst, f"{tag}_launches.md")).read())
+path = os.path.join(dst, "ncu_summary.json")
+allsum = json.load(open(path)) if os.path.exists(path) else {}
+allsum = {k: v for k, v in allsum.items() if k.startswith("config")}   # older flat layout
+allsum[f"config{config}"] = summary
+json.dump(allsum, open(path, "w"), indent=1)
+if have_launches:
+    print(open(os.path.join(dst, f"{tag}_launches.md")).read())
 print(json.dumps(summary, indent=1))
