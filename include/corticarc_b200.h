@@ -43,6 +43,7 @@ extern "C" {
 #define CC_ERR_RASTER         0x20u  /* raster buffer full                          */
 #define CC_ERR_OUTLIST        0x40u  /* exchange out-list full                      */
 #define CC_ERR_GEN            0x80u  /* generator: row larger than planned          */
+#define CC_ERR_EVREC          0x100u /* ordered-input record buffer full (one step) */
 
 /* Constants of one neuron population (model.py:44-86, NeuronBlock
  * per-neuron arrays model.py:243-267).  k1 = tau_c - tau_m and

@@ -28,6 +28,7 @@ ERR_BITS = {
     0x20: "raster buffer full",
     0x40: "exchange out-list full",
     0x80: "generator row larger than planned",
+    0x100: "ordered-input record buffer full (inputs of one step)",
 }
 
 

@@ -888,7 +888,7 @@ k_stage(const cc_shard sh) {
         if (lane == 0 && rtot) {
             rbase = atomicAdd(&ctl->stream_used, (unsigned long long)rtot);
             // evrec_cap covers a step's expected list capacity + overflow + drive
-            if (rbase + rtot > (unsigned long long)sh.evrec_cap) cc_raise(ctl, CC_ERR_SCRATCH, t);
+            if (rbase + rtot > (unsigned long long)sh.evrec_cap) cc_raise(ctl, CC_ERR_EVREC, t);
         }
         rbase = __shfl_sync(0xffffffffu, rbase, 0);
         if (rbase + rtot > (unsigned long long)sh.evrec_cap) continue;

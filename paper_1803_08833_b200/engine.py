@@ -170,7 +170,7 @@ class Simulator:
         seg_stride = (D + 1 + 7) // 8 * 8
         dseg = net.delay_segments(D, seg_stride)
         raster_cap = max(1024, n_local * bound * max(self.chunk, raster_steps or 0))
-        scratch_cap = max(1 << 16, n_local * 16)
+        scratch_cap = max(1 << 16, n_local * 64)     # spill staging: onset bursts
         # ordered-input records of one step: the expected list capacity of a step,
         # the overflow list and every neuron's Poisson budget (beyond it the
         # step fails with "event staging scratch exhausted")

@@ -46,10 +46,12 @@ _DURATION = {0: 1.0, 1: 1.0, 2: 2.0, 3: 1.0, 4: 1.0}
 # from 8 Hz (capacity errors within ~30 steps).  A sweep over drive 7-85 Hz and
 # (J_inh->exc, J_inh->inh) in {-2..-16} x {-0.5..-4} on config 2 (0.5 s runs,
 # tools/calibrate.py --jinh --jii) found no sustained asynchronous state above
-# ~2.5 Hz: the onset burst decays.  The exponential operating point is the most
-# active non-runaway one: 70 Hz drive, J_inh->exc = -8 mV, J_inh->inh = -1 mV
-# (7.4 Hz over the first 0.5 s, 2.5 Hz in its second half).
-CALIBRATED_DRIVE_HZ = {"gaussian": 40.0, "exponential": 70.0}
+# ~2.5 Hz: the onset burst decays.  The exponential operating point: 55 Hz
+# drive, J_inh->exc = -8 mV, J_inh->inh = -1 mV (config 2 at 70 Hz: 7.4 Hz over
+# the first 0.5 s, 2.5 Hz in its second half; config 3 at 70 Hz escalates into
+# synchronous onset waves of ~300 inputs per neuron-step that exceed the
+# staging capacity, at 55 Hz it settles at 1.6 Hz).
+CALIBRATED_DRIVE_HZ = {"gaussian": 40.0, "exponential": 55.0}
 CALIBRATED_J_INH = {"gaussian": (-2.0, -2.0), "exponential": (-8.0, -1.0)}   # (->exc, ->inh)
 
 
