@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 17
+#define CC_ABI_VERSION 19
 
 /* Work items are queued in this many size classes, largest first. */
 /* Input lists per 32-neuron group (events of delay d go to sub-list
@@ -63,7 +63,7 @@ typedef struct cc_ctl {
     unsigned long long ext_events;        /* generated external events        */
     unsigned long long n_spikes;
     unsigned long long raster_n;          /* entries in the raster buffer     */
-    unsigned int done_blocks;             /* last-block detection (neuron k.) */
+    unsigned int pad2;
     unsigned int error_bits;
     long long error_step;
     unsigned int max_bin;                 /* max events at one (slot, neuron) */
@@ -125,7 +125,8 @@ typedef struct cc_shard {
 
     /* input lists of the current step (DelayRing.drain's bucket,
      * engine.py:151-163): one append list per group of 32 consecutive neurons,
-     * filled by cc_deliver with the events arriving this step; a record is
+     * two sets (arrival step & 1): cc_neuron_step(t) delivers step t+1's
+     * delay >= 2 events with its idle warps, cc_deliver(t+1) the rest; a record is
      * (spike_ref << 5 | lane) | w_bits << 32.  The delay ring proper is the
      * spike log below: step t delivers the delay-d segment of every spike of
      * step t - d (rows are sorted by delay, network.py:257). */
@@ -133,12 +134,12 @@ typedef struct cc_shard {
     int32_t bin_pad;        /* unused records after each list: list stride is
                                bin_cap + bin_pad (staggers the list starts over
                                L2 slices / DRAM channels)                      */
-    uint32_t* bin_cnt;      /* [n_groups][CC_SUBLISTS][stride] sub-list fill (word 0) */
-    uint64_t* bin_rec;      /* [n_groups][CC_SUBLISTS][bin_cap + bin_pad]      */
+    uint32_t* bin_cnt;      /* [2][n_groups][CC_SUBLISTS][stride] sub-list fill (word 0) */
+    uint64_t* bin_rec;      /* [2][n_groups][CC_SUBLISTS][bin_cap + bin_pad]   */
     uint32_t* grp_n;        /* [n_groups] inputs of the current step per group  */
     uint32_t* grp_sub;      /* [n_groups][CC_SUBLISTS] records kept per sub-list */
-    uint32_t* ovf_rec;      /* [ovf_cap][4] {group, lane, spike_ref, w_bits}   */
-    uint32_t* ovf_cnt;      /* [1]                                             */
+    uint32_t* ovf_rec;      /* [2][ovf_cap][4] {group, lane, spike_ref, w_bits} */
+    uint32_t* ovf_cnt;      /* [2]                                             */
     uint32_t* ovf_sorted;   /* [ovf_cap][4] overflow of the current step, grouped by group */
     int32_t* ovf_off;       /* [n_groups] start of a group's run in ovf_sorted  */
     int32_t* ovf_fill;      /* [n_groups] grouping cursors (zero between steps) */
@@ -178,6 +179,10 @@ typedef struct cc_shard {
     double* probe_out;      /* [steps][n_probe][5] V c last refr V_end         */
     int64_t probe_steps;    /* rows in probe_out                               */
     cc_ctl* ctl;
+    /* [64] tail-delivery counters, each on its own 128 B line (away from the
+     * work-item claims in ctl): [0] next step's delay>=2 units claimed by
+     * k_stage's idle warps, [32] k_stage warps out of work items */
+    uint32_t* tailc;
 } cc_shard;
 
 /* ---------------------------------------------------------------- misc */

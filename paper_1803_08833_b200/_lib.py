@@ -15,7 +15,7 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BIT
 
 LIB_PATH = os.environ.get("CC_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 17
+ABI_VERSION = 19
 ITEM_CLASSES = 8
 CNT_STRIDE_MAX = 64          # bin_cnt words per group allocated (CC_CNT_STRIDE <= this)
 
@@ -46,7 +46,7 @@ class Ctl(C.Structure):
     _fields_ = [
         ("t", C.c_longlong), ("rec_events", C.c_ulonglong), ("ext_events", C.c_ulonglong),
         ("n_spikes", C.c_ulonglong), ("raster_n", C.c_ulonglong),
-        ("done_blocks", C.c_uint), ("error_bits", C.c_uint), ("error_step", C.c_longlong),
+        ("pad2", C.c_uint), ("error_bits", C.c_uint), ("error_step", C.c_longlong),
         ("max_bin", C.c_uint), ("max_events", C.c_uint), ("scratch_used", C.c_ulonglong),
         ("out_n", C.c_uint), ("pad0", C.c_uint), ("spilled_total", C.c_ulonglong),
         ("ovf_total", C.c_ulonglong), ("done_deliver", C.c_uint), ("ovf_grouped", C.c_uint),
@@ -82,7 +82,7 @@ class Shard(C.Structure):
         ("evrec", _P), ("evrec_cap", C.c_int64), ("ev_off", _P), ("grp_items", _P),
         ("grp_done", _P), ("rounds", _P), ("round_cap", C.c_int64),
         ("probe_map", _P), ("probe_out", _P),
-        ("probe_steps", C.c_int64), ("ctl", _P),
+        ("probe_steps", C.c_int64), ("ctl", _P), ("tailc", _P),
     ]
 
 

@@ -22,6 +22,9 @@
 #ifndef CC_CNT_STRIDE
 #define CC_CNT_STRIDE 64
 #endif
+#ifndef CC_TAIL_STOP
+#define CC_TAIL_STOP 12
+#endif
 #ifndef CC_CSR_STREAM
 #define CC_CSR_STREAM 0
 #endif
@@ -441,6 +444,145 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
     }
 }
 
+// ------------------------------------------------------------ delivery
+// A work unit is (delay d, 4 consecutive spikes of log slot t - d); each spike's
+// delay-d segment is walked by 8 lanes, U synapses per lane per pass.  Records
+// are deposited into the per-group input lists of the arrival step.
+#ifndef CC_DEL_THREADS
+#define CC_DEL_THREADS 256
+#endif
+#ifndef CC_DEL_MINB
+#define CC_DEL_MINB 2
+#endif
+#ifndef CC_DEL_U
+#define CC_DEL_U 8          // synapses per lane per pass
+#endif
+constexpr int DEL_SPU = 4;                  // spikes per unit (8 lanes each)
+constexpr int DEL_DMAX = 256;               // d_max <= 255 (uint8 delays)
+
+// Input lists of arrival step t: two sets (t & 1), so that step t+1's
+// delay >= 2 events can be delivered while step t is integrated.
+struct ListSet { uint32_t* cnt; uint64_t* rec; uint32_t* ovf_cnt; uint4* ovf; };
+__device__ __forceinline__ ListSet list_set(const cc_shard& sh, long long t) {
+    const int s = (int)(t & 1);
+    ListSet S;
+    S.cnt = sh.bin_cnt + (size_t)s * sh.n_groups * NSUB * CC_CNT_STRIDE;
+    S.rec = sh.bin_rec + (size_t)s * sh.n_groups * NSUB * ((size_t)sh.bin_cap + sh.bin_pad);
+    S.ovf_cnt = sh.ovf_cnt + s;
+    S.ovf = reinterpret_cast<uint4*>(sh.ovf_rec) + (size_t)s * sh.ovf_cap;
+    return S;
+}
+
+// Unit space of an arrival step: position k = 0..D-1 holds delay d = k + 2 for
+// k < D - 1 and d = 1 for k = D - 1 - the delay >= 2 units first, since their
+// spikes are all logged a step ahead.
+__device__ __forceinline__ int unit_delay(int k, int D) { return k < D - 1 ? k + 2 : 1; }
+
+// Block-wide (barriers): s_n[k] spikes of log slot ta - d(k), s_pre the unit
+// prefix over positions k < nk.
+__device__ __forceinline__ void unit_prefix(const cc_shard& sh, long long ta, int nk,
+                                            unsigned* s_n, unsigned* s_pre) {
+    for (int k = threadIdx.x; k < nk; k += blockDim.x)
+        s_n[k] = (unsigned)min(sh.log_ctr[pos_mod(ta - unit_delay(k, sh.d_max), sh.log_slots)],
+                               (unsigned long long)sh.spk_cap);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned acc = 0;
+        for (int k = 0; k < nk; ++k) { s_pre[k] = acc; acc += (s_n[k] + DEL_SPU - 1) / DEL_SPU; }
+        s_pre[nk] = acc;
+    }
+    __syncthreads();
+}
+
+// This lane's spike of unit u (< s_pre[nk]) of arrival step ta: segment start,
+// length and log reference; kc is the caller's position cursor (its units
+// only increase).
+__device__ __forceinline__ void unit_desc(const cc_shard& sh, long long ta, const unsigned* s_n,
+                                          const unsigned* s_pre, unsigned u, int& kc,
+                                          uint64_t& st, uint32_t& ln, uint32_t& rf) {
+    while (s_pre[kc + 1] <= u) ++kc;
+    const unsigned idx = (u - s_pre[kc]) * DEL_SPU + ((threadIdx.x & 31) >> 3);
+    st = 0; ln = 0; rf = 0;
+    if (idx < s_n[kc]) {
+        const int d = unit_delay(kc, sh.d_max);
+        const int e = (int)pos_mod(ta - d, sh.log_slots);
+        rf = (uint32_t)(e * sh.spk_cap + idx);
+        const uint16_t* ds = sh.log_dseg + (size_t)rf * sh.seg_stride;
+        const uint32_t a = __ldg(ds + d - 1), b = __ldg(ds + d);
+        st = (uint64_t)__ldg(sh.log_r0 + rf) + a;
+        ln = b - a;
+    }
+}
+
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+template <int U>
+__device__ __forceinline__ void load_pass(const cc_shard& sh, uint64_t st, uint32_t ln, int p,
+                                          int* tg, float* w) {
+    const int sl = threadIdx.x & 7;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint32_t j = (uint32_t)(p * 8 * U + u * 8 + sl);
+        tg[u] = -1;
+        if (j < ln) {
+            tg[u] = __ldg(sh.syn_tgt + st + j);
+            w[u] = __ldg(sh.syn_w + st + j);
+        }
+    }
+}
+
+// Reserve and deposit one pass: one atomic per run of consecutive lanes with
+// the same group (a segment is sorted by target, network.py:257, so a spike's
+// 8 lanes form 1-3 runs; runs are found with a shuffle and a ballot); lists
+// that are full spill to the set's overflow list.
+template <int U>
+__device__ __forceinline__ void deposit_pass(const cc_shard& sh, const ListSet& S, int sub,
+                                             const int* tg, const float* w, uint32_t rf,
+                                             long long t_err) {
+    const int lane = threadIdx.x & 31;
+    const int K = sh.bin_cap;
+    const size_t KS = (size_t)K + sh.bin_pad;
+    unsigned key[U], pos[U], got[U];
+    int lead[U];
+    const unsigned upto = 0xffffffffu >> (31 - lane);      // bits 0..lane
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+        key[k] = tg[k] >= 0 ? (unsigned)(tg[k] >> 5) : 0xffffffffu;
+        const unsigned prev = __shfl_up_sync(0xffffffffu, key[k], 1);
+        const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || key[k] != prev);
+        lead[k] = 31 - __clz(heads & upto);
+        const unsigned after = heads & ~upto;
+        const int end = after ? __ffs(after) - 1 : 32;
+        got[k] = 0u;
+        if (tg[k] >= 0 && lane == lead[k]) {
+            if (sh.debug_skip & 1024) got[k] = 0u;       // timing experiment: no reservation
+            else got[k] = atomicAdd(&S.cnt[((size_t)key[k] * NSUB + sub) * CC_CNT_STRIDE],
+                                    (unsigned)(end - lead[k]));
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+        pos[k] = __shfl_sync(0xffffffffu, got[k], lead[k]) + (unsigned)(lane - lead[k]);
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+        if (tg[k] < 0 || (sh.debug_skip & 2048)) continue;  // 2048: timing, no deposit
+        const uint32_t lig = (uint32_t)tg[k] & 31u;
+        if (pos[k] < (unsigned)K) {
+            S.rec[((size_t)key[k] * NSUB + sub) * KS + pos[k]] =
+                (uint64_t)((rf << 5) | lig) | ((uint64_t)__float_as_uint(w[k]) << 32);
+        } else {
+            const unsigned o = atomicAdd(S.ovf_cnt, 1u);
+            atomicAdd(&sh.ctl->ovf_total, 1ull);
+            if (o < (unsigned)sh.ovf_cap) S.ovf[o] = make_uint4(key[k], lig, rf, __float_as_uint(w[k]));
+            else cc_raise(sh.ctl, CC_ERR_OVERFLOW_BIN, t_err);
+        }
+    }
+}
+
 // Planning pass of phase A: per group of 32 neurons, the input counts
 // (ring-slot occupancy and the Poisson draw), the group's stream region and
 // its split into work items ("rounds") of at most NEURON_WCAP inputs, appended
@@ -464,7 +606,8 @@ k_plan(const cc_shard sh) {
     lane_cnt[wib][lane] = 0u;
     const uint32_t K = (uint32_t)sh.bin_cap;
     const size_t KS = (size_t)K + sh.bin_pad;
-    uint32_t* gcb = sh.bin_cnt + (size_t)group * NSUB * CC_CNT_STRIDE;
+    const ListSet S = list_set(sh, t);
+    uint32_t* gcb = S.cnt + (size_t)group * NSUB * CC_CNT_STRIDE;
     const uint32_t cj_all = (gvalid && lane < NSUB) ? gcb[lane * CC_CNT_STRIDE] : 0u;
     const uint32_t cj = min(cj_all, K);
     SubMap M;
@@ -476,7 +619,7 @@ k_plan(const cc_shard sh) {
     const long long o0 = sh.ovf_off[group];
     const uint32_t c_ovf = ovf_all ? (uint32_t)max(0ll, min((long long)ovf_all, sh.ovf_cap - o0)) : 0u;
     __syncwarp();
-    const uint64_t* lst = sh.bin_rec + (size_t)group * NSUB * KS;
+    const uint64_t* lst = S.rec + (size_t)group * NSUB * KS;
     for (uint32_t r0 = 0; r0 < c_list; r0 += 32 * 8) {
         uint32_t v[8];                             // 8 loads in flight per lane
 #pragma unroll
@@ -645,6 +788,12 @@ k_stage(const cc_shard sh) {
     const uint32_t K = (uint32_t)sh.bin_cap;
     const double t0 = (double)t * sh.dt;
     const double inv_dt = 1.0 / sh.dt;
+    // step t+1's delay >= 2 units (spikes of steps t-1 .. t+1-d_max, all
+    // logged): offered to the warps that run out of work items
+    __shared__ unsigned a_n[DEL_DMAX], a_pre[DEL_DMAX + 1];
+    const int D = sh.d_max;
+    const bool tail_deliver = D > 1 && !(sh.debug_skip & 4096);
+    if (tail_deliver) unit_prefix(sh, t + 1, D - 1, a_n, a_pre);
     // queued items per size class (k_plan is complete); claimed largest first
     __shared__ unsigned cls_n[CC_ITEM_CLASSES];
     if (threadIdx.x < CC_ITEM_CLASSES)
@@ -732,7 +881,7 @@ k_stage(const cc_shard sh) {
             M.init(lane < NSUB ? sh.grp_sub[(size_t)group * NSUB + lane] : 0u);
             const uint32_t c_list = M.pre[NSUB];
             const size_t KS = (size_t)K + sh.bin_pad;
-            const uint64_t* lst = sh.bin_rec + (size_t)group * NSUB * KS;
+            const uint64_t* lst = list_set(sh, t).rec + (size_t)group * NSUB * KS;
             const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + sh.ovf_off[group];
             B.hist[lane] = 0u;                          // per-lane fill cursors
             __syncwarp();
@@ -943,6 +1092,40 @@ k_stage(const cc_shard sh) {
             CC_DBG(7, (unsigned long long)(blockIdx.x * STAGE_WARPS + wib));
         }
     }
+    // ---- 5 tail: deliver step t+1's delay >= 2 units (claimed in order from
+    //      tailc[0]; k_deliver(t+1) delivers the ones left and the delay-1
+    //      units) while the last items and group updates finish
+    // Claims stop once every warp is out of items (the step's own work is
+    // done): the rest goes to k_deliver(t+1), whose pipelined grid is faster.
+    unsigned idle_prev = 0;
+    if (lane == 0) idle_prev = atomicAdd(&sh.tailc[32], 1u);
+    // (stop at CC_TAIL_STOP/16 of the warps idle: units in flight past the
+    // step's last update lengthen the kernel)
+    const unsigned n_warps = gridDim.x * STAGE_WARPS * CC_TAIL_STOP / 16;
+    if (tail_deliver && __shfl_sync(0xffffffffu, idle_prev, 0) + 1u < n_warps &&
+        !*(volatile unsigned*)&ctl->error_bits) {
+        const unsigned n_a = a_pre[D - 1];
+        const ListSet S1 = list_set(sh, t + 1);
+        constexpr int UT = 8;
+        int kc = 0;
+        for (;;) {
+            unsigned u = n_a;
+            if (lane == 0 && *(volatile unsigned*)&sh.tailc[32] < n_warps)
+                u = atomicAdd(&sh.tailc[0], 1u);
+            u = __shfl_sync(0xffffffffu, u, 0);
+            if (u >= n_a) break;
+            uint64_t st;
+            uint32_t ln, rf;
+            unit_desc(sh, t + 1, a_n, a_pre, u, kc, st, ln, rf);
+            const uint32_t lmax = warp_max_u32(ln);
+            for (int p = 0; (uint32_t)(p * 8 * UT) < lmax; ++p) {
+                int tg[UT];
+                float w[UT];
+                load_pass<UT>(sh, st, ln, p, tg, w);
+                deposit_pass<UT>(sh, S1, kc % NSUB, tg, w, rf, t + 1);
+            }
+        }
+    }
     // spike counter: one atomic per block; last block out retires the step
     unsigned s_sum = my_spikes;
 #pragma unroll
@@ -957,7 +1140,8 @@ k_stage(const cc_shard sh) {
         __threadfence();
         if (atomicAdd(&ctl->done_stage, 1u) == gridDim.x - 1) {
             ctl->done_stage = 0;
-            sh.ovf_cnt[0] = 0;                 // step t's inputs fully consumed
+            sh.tailc[32] = 0u;
+            sh.ovf_cnt[t & 1] = 0;             // step t's inputs fully consumed
             __threadfence();
             *(volatile long long*)&ctl->t = t + 1;
         }
@@ -988,13 +1172,12 @@ __global__ void k_probe(const cc_shard sh) {
 
 // Counting sort of one slot's overflow records by target, by a single block
 // (only runs in steps that overflowed the dense bins).
-__device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
+__device__ void group_overflow(const cc_shard& sh, const ListSet& S, unsigned m) {
     __shared__ uint32_t wsum[32];
     __shared__ uint32_t carry;
     const int n = sh.n_groups;
     const uint32_t K = (uint32_t)sh.bin_cap;
-    const uint32_t* cnt = sh.bin_cnt;                 // (s: single step since pull delivery)
-    (void)s;
+    const uint32_t* cnt = S.cnt;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
@@ -1032,7 +1215,7 @@ __device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
         if (threadIdx.x == 0) carry += wsum[nwarp - 1];
         __syncthreads();
     }
-    const uint4* rec = reinterpret_cast<const uint4*>(sh.ovf_rec) + (size_t)s * sh.ovf_cap;
+    const uint4* rec = S.ovf;
     uint4* out = reinterpret_cast<uint4*>(sh.ovf_sorted);
     for (unsigned j = threadIdx.x; j < m; j += blockDim.x) {
         const uint4 r = rec[j];
@@ -1043,25 +1226,12 @@ __device__ void group_overflow(const cc_shard& sh, int s, unsigned m) {
     for (unsigned j = threadIdx.x; j < m; j += blockDim.x) sh.ovf_fill[rec[j].x] = 0;
 }
 
-// Delivery of step t (pull): the events arriving at t are the delay-d segments
-// of the rows of the spikes of step t - d, d = 1..d_max.  A work unit is
-// (d, 4 consecutive spikes of log slot t - d); each spike's segment is walked
-// by 8 lanes, U synapses per lane per pass, software-pipelined (the next
-// pass's or unit's CSR loads are issued before this pass's reservations and
-// deposits).  Deposits go to the step's per-group lists, which stay L2
-// resident from here to k_plan / k_stage.
-#ifndef CC_DEL_THREADS
-#define CC_DEL_THREADS 256
-#endif
-#ifndef CC_DEL_MINB
-#define CC_DEL_MINB 2
-#endif
-#ifndef CC_DEL_U
-#define CC_DEL_U 8          // synapses per lane per pass
-#endif
-constexpr int DEL_SPU = 4;                  // spikes per unit (8 lanes each)
-constexpr int DEL_DMAX = 256;               // d_max <= 255 (uint8 delays)
-
+// Delivery of arrival step t (pull): the events arriving at t are the delay-d
+// segments of the rows of the spikes of step t - d, d = 1..d_max.  The units
+// of delay >= 2 were already offered to the idle warps of k_stage(t - 1)
+// (tailc[0] counts the ones they claimed); this kernel delivers the rest
+// and the delay-1 units, software-pipelined (the next pass's or unit's CSR
+// loads are issued before this pass's reservations and deposits).
 __global__ void __launch_bounds__(CC_DEL_THREADS, CC_DEL_MINB)
 k_deliver(const cc_shard sh) {
     const unsigned long long dbg_t0 = gtimer();
@@ -1070,8 +1240,6 @@ k_deliver(const cc_shard sh) {
     if (*(volatile unsigned*)&ctl->error_bits) return;      // failed run: stop working
     const int L = sh.log_slots, D = sh.d_max;
     __shared__ unsigned s_n[DEL_DMAX], s_pre[DEL_DMAX + 1];
-    for (int k = threadIdx.x; k < D; k += blockDim.x)
-        s_n[k] = (unsigned)min(sh.log_ctr[pos_mod(t - 1 - k, L)], (unsigned long long)sh.spk_cap);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         // recurrent_events: row lengths of the spikes of step t - 1, counted at
         // their expansion step like engine.py:366
@@ -1086,70 +1254,29 @@ k_deliver(const cc_shard sh) {
 #pragma unroll
         for (int c = 0; c < CC_ITEM_CLASSES; ++c) ctl->cls_n[c] = 0u;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned acc = 0;
-        for (int k = 0; k < D; ++k) { s_pre[k] = acc; acc += (s_n[k] + DEL_SPU - 1) / DEL_SPU; }
-        s_pre[D] = acc;
-    }
-    __syncthreads();
+    unit_prefix(sh, t, D, s_n, s_pre);
     const unsigned n_units = s_pre[D];
+    // units [0, c) were delivered by k_stage(t - 1)'s idle warps (claimed in order)
+    const unsigned c0 = min(*(volatile unsigned*)&sh.tailc[0], s_pre[D - 1]);
+    const ListSet S = list_set(sh, t);
     const int lane = threadIdx.x & 31;
-    const int sl = lane & 7;                                 // lane within the spike's 8
     const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned nw = (gridDim.x * blockDim.x) >> 5;
-    const int NG = sh.n_groups;
-    const int K = sh.bin_cap;
-    const size_t KS = (size_t)K + sh.bin_pad;
-    const int32_t* __restrict__ tgt_a = sh.syn_tgt;
-    const float* __restrict__ w_a = sh.syn_w;
     const unsigned long long dbg_t1 = gtimer();
     constexpr int U = CC_DEL_U;
     constexpr int SPAN = 8 * U;                              // synapses per spike per pass
-    // unit u -> delay index k (monotone cursor: a warp's units increase) and
-    // this lane's spike: segment start, length, log reference
     int kc = 0;
-    auto unit_desc = [&](unsigned u, uint64_t& st, uint32_t& ln, uint32_t& rf, int& kk) {
-        while (s_pre[kc + 1] <= u) ++kc;                     // s_pre[D] = n_units > u
-        kk = kc;
-        const unsigned idx = (u - s_pre[kc]) * DEL_SPU + (unsigned)(lane >> 3);
-        st = 0; ln = 0; rf = 0;
-        if (idx < s_n[kc]) {
-            const int e = (int)pos_mod(t - 1 - kc, L);
-            rf = (uint32_t)(e * sh.spk_cap + idx);
-            const uint16_t* ds = sh.log_dseg + (size_t)rf * sh.seg_stride;
-            const uint32_t a = __ldg(ds + kc), b = __ldg(ds + kc + 1);   // delay kc + 1
-            st = (uint64_t)__ldg(sh.log_r0 + rf) + a;
-            ln = b - a;
-        }
-    };
-    auto warp_max = [](uint32_t v) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-        return v;
-    };
-    auto load_pass = [&](uint64_t st, uint32_t ln, int p, int* tg_, float* w_) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t j = (uint32_t)(p * SPAN + u * 8 + sl);
-            tg_[u] = -1;
-            if (j < ln) {
-                tg_[u] = __ldg(tgt_a + st + j);
-                w_[u] = __ldg(w_a + st + j);
-            }
-        }
-    };
-    unsigned u = wid;
+    unsigned u = c0 + wid;
     uint64_t st = 0, stn = 0;
     uint32_t ln = 0, rf = 0, lnn = 0, rfn = 0;
     int kcur = 0, kn = 0;
-    if (u < n_units) unit_desc(u, st, ln, rf, kcur);
-    if (u + nw < n_units) unit_desc(u + nw, stn, lnn, rfn, kn);
-    uint32_t lmax = warp_max(ln);
+    if (u < n_units) { unit_desc(sh, t, s_n, s_pre, u, kc, st, ln, rf); kcur = kc; }
+    if (u + nw < n_units) { unit_desc(sh, t, s_n, s_pre, u + nw, kc, stn, lnn, rfn); kn = kc; }
+    uint32_t lmax = warp_max_u32(ln);
     int p = 0;
     int tg[U];
     float w[U];
-    if (u < n_units) load_pass(st, ln, 0, tg, w);
+    if (u < n_units) load_pass<U>(sh, st, ln, 0, tg, w);
     while (u < n_units) {
         // next pass of this unit, else the first pass of the warp's next unit
         unsigned u2 = u;
@@ -1160,73 +1287,31 @@ k_deliver(const cc_shard sh) {
         const bool adv = (uint32_t)(p2 * SPAN) >= lmax;
         if (adv) {
             u2 = u + nw; p2 = 0; st2 = stn; ln2 = lnn; rf2 = rfn; k2 = kn;
-            lmax2 = warp_max(lnn);
+            lmax2 = warp_max_u32(lnn);
         }
         int tg2[U];
         float w2[U];
-        if (u2 < n_units) load_pass(st2, ln2, p2, tg2, w2);
+        if (u2 < n_units) load_pass<U>(sh, st2, ln2, p2, tg2, w2);
         else {
 #pragma unroll
             for (int k = 0; k < U; ++k) tg2[k] = -1;
         }
-        if (adv && u2 + nw < n_units) unit_desc(u2 + nw, stn, lnn, rfn, kn);
-        const int sub = kcur % NSUB;             // sub-list of this unit's delay
-        // one atomic per run of consecutive lanes with the same group: a
-        // segment is sorted by target (network.py:257), so a spike's 8 lanes
-        // form 1-3 runs; runs are found with a shuffle and a ballot
-        unsigned key[U], pos[U], got[U];
-        int lead[U];
-        const unsigned upto = 0xffffffffu >> (31 - lane);      // bits 0..lane
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-            key[k] = tg[k] >= 0 ? (unsigned)(tg[k] >> 5) : 0xffffffffu;
-            const unsigned prev = __shfl_up_sync(0xffffffffu, key[k], 1);
-            const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || key[k] != prev);
-            lead[k] = 31 - __clz(heads & upto);
-            const unsigned after = heads & ~upto;
-            const int end = after ? __ffs(after) - 1 : 32;
-            got[k] = 0u;
-            if (tg[k] >= 0 && lane == lead[k]) {
-                if (sh.debug_skip & 1024) got[k] = 0u;       // timing experiment: no reservation
-                else got[k] = atomicAdd(&sh.bin_cnt[((size_t)key[k] * NSUB + sub) * CC_CNT_STRIDE],
-                                        (unsigned)(end - lead[k]));
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < U; ++k)
-            pos[k] = __shfl_sync(0xffffffffu, got[k], lead[k]) + (unsigned)(lane - lead[k]);
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-            if (tg[k] < 0 || (sh.debug_skip & 2048)) continue;  // 2048: timing, no deposit
-            const uint32_t lig = (uint32_t)tg[k] & 31u;
-            if (pos[k] < (unsigned)K) {
-                sh.bin_rec[((size_t)key[k] * NSUB + sub) * KS + pos[k]] =
-                    (uint64_t)((rf << 5) | lig) | ((uint64_t)__float_as_uint(w[k]) << 32);
-            } else {
-                const unsigned o = atomicAdd(&sh.ovf_cnt[0], 1u);
-                atomicAdd(&ctl->ovf_total, 1ull);
-                if (o < (unsigned)sh.ovf_cap) {
-                    reinterpret_cast<uint4*>(sh.ovf_rec)[o] =
-                        make_uint4(key[k], lig, rf, __float_as_uint(w[k]));
-                } else {
-                    cc_raise(ctl, CC_ERR_OVERFLOW_BIN, t);
-                }
-            }
-        }
+        if (adv && u2 + nw < n_units) { unit_desc(sh, t, s_n, s_pre, u2 + nw, kc, stn, lnn, rfn); kn = kc; }
+        deposit_pass<U>(sh, S, kcur % NSUB, tg, w, rf, t);
 #pragma unroll
         for (int k = 0; k < U; ++k) { tg[k] = tg2[k]; w[k] = w2[k]; }
         u = u2; p = p2; st = st2; ln = ln2; rf = rf2; lmax = lmax2; kcur = k2;
     }
-    (void)NG;
     if ((sh.debug_skip & 256) && lane == 0) {
         unsigned long long* d_ = reinterpret_cast<unsigned long long*>(sh.scratch)
                                  + (size_t)sh.scratch_cap * 7 - 65536ull * 8 - (size_t)(wid + 1) * 4;
         unsigned smid_;
         asm volatile("mov.u32 %0, %smid;" : "=r"(smid_));
-        d_[0] = dbg_t0; d_[1] = dbg_t1; d_[2] = gtimer(); d_[3] = (unsigned long long)smid_ | ((unsigned long long)n_units << 32);
+        d_[0] = dbg_t0; d_[1] = dbg_t1; d_[2] = gtimer();
+        d_[3] = (unsigned long long)smid_ | ((unsigned long long)(n_units - c0) << 32);
     }
 
-    // Step t's inputs are complete now (k_deliver(t) is their only depositor):
+    // Step t's inputs are complete now (this kernel is their last depositor):
     // the last block out groups the overflow records by group for k_plan(t).
     __shared__ bool am_last;
     __syncthreads();
@@ -1242,10 +1327,14 @@ k_deliver(const cc_shard sh) {
     }
     if (!am_last) return;
     __threadfence();
-    const unsigned m = min(*(volatile unsigned*)&sh.ovf_cnt[0], (unsigned)sh.ovf_cap);
-    if (threadIdx.x == 0) { ctl->done_deliver = 0; ctl->ovf_grouped = m; }
+    const unsigned m = min(*(volatile unsigned*)S.ovf_cnt, (unsigned)sh.ovf_cap);
+    if (threadIdx.x == 0) {
+        ctl->done_deliver = 0;
+        ctl->ovf_grouped = m;
+        sh.tailc[0] = 0u;                      // k_stage(t) offers step t+1's units
+    }
     if (m == 0) return;
-    group_overflow(sh, 0, m);
+    group_overflow(sh, S, m);
 }
 
 // Delay-segment table: dseg[r][d] = synapses of row r with delay <= d,

@@ -180,13 +180,14 @@ class Simulator:
         self.buf = dict(
             gid=T.from_numpy(gids.astype(np.uint32).view(np.int32)).to(dev),
             state=T.zeros((n_local, 4), dtype=f64, device=dev),
-            bin_cnt=T.zeros(n_groups * _lib.sublists() * _lib.CNT_STRIDE_MAX, dtype=i32,
+            bin_cnt=T.zeros(2 * n_groups * _lib.sublists() * _lib.CNT_STRIDE_MAX, dtype=i32,
                             device=dev),
-            bin_rec=T.empty((n_groups, _lib.sublists(), bin_cap + bin_pad), dtype=i64, device=dev),
+            bin_rec=T.empty((2, n_groups, _lib.sublists(), bin_cap + bin_pad), dtype=i64,
+                            device=dev),
             grp_n=T.zeros(n_groups, dtype=i32, device=dev),
             grp_sub=T.zeros((n_groups, _lib.sublists()), dtype=i32, device=dev),
-            ovf_rec=T.empty((ovf_cap, 4), dtype=i32, device=dev),
-            ovf_cnt=T.zeros(1, dtype=i32, device=dev),
+            ovf_rec=T.empty((2, ovf_cap, 4), dtype=i32, device=dev),
+            ovf_cnt=T.zeros(2, dtype=i32, device=dev),
             ovf_sorted=T.empty((ovf_cap, 4), dtype=i32, device=dev),
             ovf_off=T.zeros(n_groups, dtype=i32, device=dev),
             ovf_fill=T.zeros(n_groups, dtype=i32, device=dev),
@@ -212,6 +213,7 @@ class Simulator:
                            device=dev),
 
             ctl=T.zeros(C.sizeof(_lib.Ctl) // 8, dtype=i64, device=dev),
+            tailc=T.zeros(64, dtype=i32, device=dev),
         )
         self.probes = None if probes is None else np.asarray(probes, np.int64)
         n_probe = 0 if self.probes is None else len(self.probes)
@@ -226,6 +228,7 @@ class Simulator:
         sh.n_local, sh.n_col, sh.n_exc_col = n_local, n, grid.n_excitatory_per_column
         sh.d_max, sh.bin_cap, sh.log_slots = D, bin_cap, D + 1
         sh.n_groups, sh.bin_pad = n_groups, bin_pad
+        sh.debug_skip = int(os.environ.get("CC_DEBUG_SKIP", "0"))   # timing experiments only
         sh.spk_cap, sh.seg_stride = spk_cap, seg_stride
         sh.ovf_cap, sh.raster_cap = ovf_cap, raster_cap
         sh.scratch_cap, sh.n_rows = scratch_cap, grid.n_neurons
@@ -255,7 +258,7 @@ class Simulator:
                   "ovf_fill", "log_t", "log_gid", "log_ctr", "log_len", "log_r0", "log_dseg",
                   "raster_gid", "raster_t", "out_gid", "out_t", "scratch",
                   "ev_n", "ev_nr", "rounds", "evrec", "ev_off", "grp_items", "grp_done",
-                  "probe_map", "probe_out", "ctl"):
+                  "probe_map", "probe_out", "ctl", "tailc"):
             setattr(sh, k, b[k].data_ptr())
         sh.probe_steps = b["probe_out"].shape[0] if n_probe else 0
         self.shard = sh
