@@ -16,7 +16,9 @@ e2e        = same metric through the public API run_b200(config) wall clock
              (host loop, per-chunk counter checks and raster device->host copies).
 roofline   = k_deliver against measured HBM bandwidth, 17 B per recurrent
              event; per-kernel times from event-record nodes
-             in an instrumented graph replay of the same workload.
+             in instrumented graph replays of the same workload: one as timed
+             (kernel shares), one with k_stage's tail delivery switched off so
+             that k_deliver deposits every arrival (the roofline line).
 cpu_baseline / --impl reference = the CPU oracle (numpy port of the
              reference loop) on the same connectivity, 1 core, bounded sample.
 """
@@ -264,23 +266,39 @@ def bench_single(args):
     spikes = c1.n_spikes - c0.n_spikes
     value = events / (ms / 1e3)
 
-    # instrumented replay: per-kernel durations from event-record nodes
+    # instrumented replays: per-kernel durations from event-record nodes.
+    # (a) as timed (k_stage's idle warps deliver most of the next step's
+    #     delay>=2 events): kernel shares;
+    # (b) with that tail delivery switched off (debug_skip 4096), so k_deliver
+    #     deposits every arrival: the delivery kernel's roofline.
     NI = min(args.instrument_steps, 1000)
-    timer = C.c_void_p()
-    _lib.check(L.cc_timer_create(3 * NI, C.byref(timer)))
-    g_t = sim.capture(NI, timer=timer)
-    c2 = sim.check(collect_raster=False)
-    g_t.replay()
-    torch.cuda.synchronize(dev)
-    sim.t += NI
-    c3 = sim.check(collect_raster=False)
-    t_del = [L.cc_timer_elapsed_ms(timer, 3 * i, 3 * i + 1) for i in range(NI)]
-    t_neu = [L.cc_timer_elapsed_ms(timer, 3 * i + 1, 3 * i + 2) for i in range(NI)]
-    L.cc_timer_destroy(timer)
-    rec_i = c3.rec_events - c2.rec_events
-    del_ms, neu_ms = float(np.sum(t_del)), float(np.sum(t_neu))
+
+    def instrumented(debug: int):
+        timer = C.c_void_p()
+        _lib.check(L.cc_timer_create(3 * NI, C.byref(timer)))
+        sim.shard.debug_skip = debug
+        g_t = sim.capture(NI, timer=timer)
+        sim.shard.debug_skip = 0
+        ca = sim.check(collect_raster=False)
+        g_t.replay()
+        torch.cuda.synchronize(dev)
+        sim.t += NI
+        cb = sim.check(collect_raster=False)
+        d_ms = float(np.sum([L.cc_timer_elapsed_ms(timer, 3 * i, 3 * i + 1) for i in range(NI)]))
+        n_ms = float(np.sum([L.cc_timer_elapsed_ms(timer, 3 * i + 1, 3 * i + 2)
+                             for i in range(NI)]))
+        L.cc_timer_destroy(timer)
+        return dict(del_ms=d_ms, neu_ms=n_ms, rec=cb.rec_events - ca.rec_events,
+                    ev=(cb.rec_events + cb.ext_events) - (ca.rec_events + ca.ext_events),
+                    dep=cb.del_events - ca.del_events, tail=cb.tail_events - ca.tail_events)
+
+    run_a = instrumented(0)
+    run_b = instrumented(4096)
+    del_ms, neu_ms = run_a["del_ms"], run_a["neu_ms"]
+    del_i, tail_i = run_a["dep"], run_a["tail"]
     hbm, peak_src = peaks()
-    achieved = rec_i * BYTES_PER_EVENT / (del_ms / 1e3) / 1e9 if del_ms > 0 else 0.0
+    achieved = (run_b["dep"] * BYTES_PER_EVENT / (run_b["del_ms"] / 1e3) / 1e9
+                if run_b["del_ms"] > 0 else 0.0)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
@@ -292,10 +310,19 @@ def bench_single(args):
             traffic = None
     kernels = {
         "k_deliver": {"avg_us": 1e3 * del_ms / NI, "share": del_ms / (del_ms + neu_ms),
-                      "bytes_per_launch": rec_i * BYTES_PER_EVENT / NI},
+                      "events_per_launch": del_i / NI,
+                      "bytes_per_launch": del_i * BYTES_PER_EVENT / NI},
+        "tail_delivery": {"events_per_step": tail_i / NI,
+                          "share_of_arrivals": tail_i / max(1, tail_i + del_i),
+                          "what": "step t+1's delay>=2 events deposited by k_stage(t)'s "
+                                  "idle warps (inside the k_neuron time)"},
         "k_neuron": {"avg_us": 1e3 * neu_ms / NI, "share": neu_ms / (del_ms + neu_ms),
-                     "neuron_events_per_launch": (c3.rec_events + c3.ext_events
-                                                  - c2.rec_events - c2.ext_events) / NI},
+                     "neuron_events_per_launch": run_a["ev"] / NI},
+        "k_deliver_all_arrivals": {"avg_us": 1e3 * run_b["del_ms"] / NI,
+                                   "events_per_launch": run_b["dep"] / NI,
+                                   "k_neuron_avg_us": 1e3 * run_b["neu_ms"] / NI,
+                                   "what": "replay (b): tail delivery off, k_deliver deposits "
+                                           "every arrival (roofline kernel)"},
         "instrumented_steps": NI,
         "instrumented_ms_per_step": (del_ms + neu_ms) / NI,
     }
@@ -311,6 +338,8 @@ def bench_single(args):
         "recurrent_events_per_s": rec / (ms / 1e3),
         "mean_rate_hz": spikes / (cfg.grid.n_neurons * K * cfg.timestep_ms / 1e3),
         "roofline": {"bound": "hbm", "kernel": "k_deliver", "achieved": achieved, "peak": hbm,
+                     "units": "events k_deliver deposited x 17 B / its average launch time, "
+                              "replay (b) with every arrival delivered by k_deliver",
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                      "peak_source": peak_src,
                      "bytes_per_event": BYTES_PER_EVENT},
@@ -329,7 +358,7 @@ def bench_single(args):
                          "spilled_neuron_steps": int(c1.spilled_total),
                          "bin_cap": sim.shard.bin_cap},
     }
-    del sim, g_main, g_rem, g_t
+    del sim, g_main, g_rem
     torch.cuda.empty_cache()
     if not args.no_e2e:
         res = run_b200(cfg, 1, net=net)

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 19
+#define CC_ABI_VERSION 20
 
 /* Work items are queued in this many size classes, largest first. */
 /* Input lists per 32-neuron group (events of delay d go to sub-list
@@ -81,6 +81,8 @@ typedef struct cc_ctl {
     unsigned int round_next;              /* next work item to claim          */
     unsigned int pad1;
     unsigned int cls_n[CC_ITEM_CLASSES];  /* work items queued per size class  */
+    unsigned long long del_events;        /* recurrent events deposited by cc_deliver */
+    unsigned long long tail_events;       /* ... by cc_neuron_step's idle warps (next step) */
 } cc_ctl;
 
 /* One shard's device state.  Layout documented in DESIGN.md section 3. */

@@ -15,7 +15,7 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BIT
 
 LIB_PATH = os.environ.get("CC_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 19
+ABI_VERSION = 20
 ITEM_CLASSES = 8
 CNT_STRIDE_MAX = 64          # bin_cnt words per group allocated (CC_CNT_STRIDE <= this)
 
@@ -52,6 +52,7 @@ class Ctl(C.Structure):
         ("ovf_total", C.c_ulonglong), ("done_deliver", C.c_uint), ("ovf_grouped", C.c_uint),
         ("stream_used", C.c_ulonglong), ("done_stage", C.c_uint), ("n_rounds", C.c_uint),
         ("round_next", C.c_uint), ("pad1", C.c_uint), ("cls_n", C.c_uint * 8),
+        ("del_events", C.c_ulonglong), ("tail_events", C.c_ulonglong),
     ]
 
 

@@ -1098,6 +1098,7 @@ k_stage(const cc_shard sh) {
     // Claims stop once every warp is out of items (the step's own work is
     // done): the rest goes to k_deliver(t+1), whose pipelined grid is faster.
     unsigned idle_prev = 0;
+    unsigned long long tail_ev = 0;
     if (lane == 0) idle_prev = atomicAdd(&sh.tailc[32], 1u);
     // (stop at CC_TAIL_STOP/16 of the warps idle: units in flight past the
     // step's last update lengthen the kernel)
@@ -1117,6 +1118,7 @@ k_stage(const cc_shard sh) {
             uint64_t st;
             uint32_t ln, rf;
             unit_desc(sh, t + 1, a_n, a_pre, u, kc, st, ln, rf);
+            if ((lane & 7) == 0) tail_ev += ln;          // one lane per spike
             const uint32_t lmax = warp_max_u32(ln);
             for (int p = 0; (uint32_t)(p * 8 * UT) < lmax; ++p) {
                 int tg[UT];
@@ -1126,6 +1128,9 @@ k_stage(const cc_shard sh) {
             }
         }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tail_ev += __shfl_xor_sync(0xffffffffu, tail_ev, o);
+    if (lane == 0 && tail_ev) atomicAdd(&ctl->tail_events, tail_ev);
     // spike counter: one atomic per block; last block out retires the step
     unsigned s_sum = my_spikes;
 #pragma unroll
@@ -1277,6 +1282,8 @@ k_deliver(const cc_shard sh) {
     int tg[U];
     float w[U];
     if (u < n_units) load_pass<U>(sh, st, ln, 0, tg, w);
+    const bool cnt_lane = (lane & 7) == 0;                   // one lane per spike counts
+    unsigned long long my_ev = (u < n_units && cnt_lane) ? ln : 0u;
     while (u < n_units) {
         // next pass of this unit, else the first pass of the warp's next unit
         unsigned u2 = u;
@@ -1297,6 +1304,7 @@ k_deliver(const cc_shard sh) {
             for (int k = 0; k < U; ++k) tg2[k] = -1;
         }
         if (adv && u2 + nw < n_units) { unit_desc(sh, t, s_n, s_pre, u2 + nw, kc, stn, lnn, rfn); kn = kc; }
+        if (adv && u2 < n_units && cnt_lane) my_ev += ln2;
         deposit_pass<U>(sh, S, kcur % NSUB, tg, w, rf, t);
 #pragma unroll
         for (int k = 0; k < U; ++k) { tg[k] = tg2[k]; w[k] = w2[k]; }
@@ -1314,7 +1322,14 @@ k_deliver(const cc_shard sh) {
     // Step t's inputs are complete now (this kernel is their last depositor):
     // the last block out groups the overflow records by group for k_plan(t).
     __shared__ bool am_last;
+    __shared__ unsigned long long blk_ev;
+    if (threadIdx.x == 0) blk_ev = 0ull;
     __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_ev += __shfl_xor_sync(0xffffffffu, my_ev, o);
+    if (lane == 0 && my_ev) atomicAdd(&blk_ev, my_ev);
+    __syncthreads();
+    if (threadIdx.x == 0 && blk_ev) atomicAdd(&ctl->del_events, blk_ev);
     if (threadIdx.x == 0) {
         __threadfence();
         am_last = atomicAdd(&ctl->done_deliver, 1u) == gridDim.x - 1;
