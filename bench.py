@@ -155,8 +155,8 @@ def run_reference_arm(args):
     from paper_1803_08833_b200.network import build_b200
     cfg = workload(args)
     if not torch.cuda.is_available():
-        print(json.dumps({"impl": "reference", "unavailable": "no CUDA device to build the "
-                          "shared connectivity"}))
+        emit({"impl": "reference", "unavailable": "no CUDA device to build the "
+                                                  "shared connectivity"})
         return
     net = build_b200(cfg)
     from oracle.mp_runner import run_oracle_mp
@@ -184,7 +184,7 @@ def run_reference_arm(args):
         "wall_s_per_sim_s": ms,
         "exchange_s": r["exchange_s"],
     }
-    print(json.dumps(line))
+    emit(line)
 
 
 def config_block(cfg, net, args):
@@ -202,7 +202,27 @@ def config_block(cfg, net, args):
             "parallelism": f"column blocks over {args.gpus} GPU(s)"}
 
 
+_JSON_OUT = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line on the real stdout (fd 1 is pointed at stderr while
+    the bench runs, so library banners - e.g. NCCL's version line - cannot mix
+    into the result stream)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
+def _isolate_stdout() -> None:
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
 def main():
+    _isolate_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
@@ -217,14 +237,19 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--instrument-steps", type=int, default=200)
+    ap.add_argument("--exchange", action="store_true",
+                    help="run the multi-GPU (exchange-mode) path even on one rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference_arm(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    if world > 1 or args.gpus > 1 or args.exchange:
         from paper_1803_08833_b200.distributed import bench_distributed
-        return bench_distributed(args, workload(args))
+        line = bench_distributed(args, workload(args))
+        if line is not None:
+            emit(line)
+        return None
     return bench_single(args)
 
 
@@ -372,7 +397,7 @@ def bench_single(args):
     if not args.no_cpu:
         cb = cpu_oracle_sample(cfg, net, float(os.environ.get("CC_CPU_BUDGET_S", "20")), 10 ** 9)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-    print(json.dumps(line))
+    emit(line)
 
 
 if __name__ == "__main__":

@@ -359,7 +359,7 @@ def run_multi_gpu(config, workers: int):
 
 def bench_distributed(args, cfg) -> None:
     """bench.py for N > 1 (launched by torchrun): K steps timed with CUDA
-    events on every rank (max over ranks), rank 0 prints the JSON line.  The
+    events on every rank (max over ranks); returns the JSON line on rank 0.  The
     step loop is host-driven (exchange per step), so the same timed region is
     also the end-to-end number (host loop, NCCL exchange, raster copies)."""
     import torch
@@ -434,5 +434,6 @@ def bench_distributed(args, cfg) -> None:
             "gpu_launches": 5 * args.steps,       # deliver, plan, stage, pack, ingest per step
             "clocks": clk,
         }
-        print(json.dumps(line))
+        dist.destroy_process_group()
+        return line
     dist.destroy_process_group()
