@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 20
+#define CC_ABI_VERSION 22
 
 /* Work items are queued in this many size classes, largest first. */
 /* Input lists per 32-neuron group (events of delay d go to sub-list
@@ -44,6 +44,7 @@ extern "C" {
 #define CC_ERR_OUTLIST        0x40u  /* exchange out-list full                      */
 #define CC_ERR_GEN            0x80u  /* generator: row larger than planned          */
 #define CC_ERR_EVREC          0x100u /* ordered-input record buffer full (one step) */
+#define CC_ERR_GRIDSYNC       0x200u /* k_stage grid barrier timed out              */
 
 /* Constants of one neuron population (model.py:44-86, NeuronBlock
  * per-neuron arrays model.py:243-267).  k1 = tau_c - tau_m and
@@ -106,7 +107,7 @@ typedef struct cc_shard {
     int32_t n_probe;
     int32_t direct_log;     /* 1: neuron kernel feeds the delivery log itself  */
     int32_t debug_skip;     /* timing experiments only: bit mask of k_neuron stages to skip */
-    int32_t pad_;
+    int32_t plan_in_stage;  /* set by cc_neuron_step: k_stage runs the planning itself */
     uint64_t h2_ext;        /* splitmix chain prefix for EXTERNAL (rng.py:85-86)      */
     uint64_t h2_time;       /* ... for EXTERNAL_TIME                                  */
     uint64_t h2_init;       /* ... for INIT_STATE                                     */
@@ -181,9 +182,9 @@ typedef struct cc_shard {
     double* probe_out;      /* [steps][n_probe][5] V c last refr V_end         */
     int64_t probe_steps;    /* rows in probe_out                               */
     cc_ctl* ctl;
-    /* [64] tail-delivery counters, each on its own 128 B line (away from the
-     * work-item claims in ctl): [0] next step's delay>=2 units claimed by
-     * k_stage's idle warps, [32] k_stage warps out of work items */
+    /* [128] counters, each on its own 128 B line (away from the work-item
+     * claims in ctl): [0] next step's delay>=2 units claimed by k_stage's idle
+     * warps, [32] k_stage warps out of work items, [64] k_stage grid barrier */
     uint32_t* tailc;
 } cc_shard;
 

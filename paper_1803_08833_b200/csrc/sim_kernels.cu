@@ -587,21 +587,20 @@ __device__ __forceinline__ void deposit_pass(const cc_shard& sh, const ListSet& 
 // (ring-slot occupancy and the Poisson draw), the group's stream region and
 // its split into work items ("rounds") of at most NEURON_WCAP inputs, appended
 // to a global queue so that heavy groups are spread over many warps.
-__global__ void __launch_bounds__(128)
-k_plan(const cc_shard sh) {
+// Block-wide (barriers): every warp of the block plans group group0 (or idles
+// if group0 is past the last group).
+__device__ __forceinline__ void plan_group(const cc_shard& sh, long long t, int group0) {
     const unsigned long long pt0 = gtimer();
     cc_ctl* ctl = sh.ctl;
-    const long long t = *(volatile long long*)&ctl->t;
     // (after a failed run the plan is still bounded - every write is checked -
     // and k_stage processes nothing; the block barriers below need all warps)
     const int lane = threadIdx.x & 31;
-    const int group0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const bool gvalid = group0 * 32 < sh.n_local;   // warps past the last group idle
     const int group = gvalid ? group0 : 0;
     const int li = group * 32 + lane;
     const bool active = gvalid && li < sh.n_local;
     // inputs of this step: count the group's list records per lane
-    __shared__ uint32_t lane_cnt[4][32];
+    __shared__ uint32_t lane_cnt[8][32];
     const int wib = threadIdx.x >> 5;
     lane_cnt[wib][lane] = 0u;
     const uint32_t K = (uint32_t)sh.bin_cap;
@@ -770,6 +769,13 @@ k_plan(const cc_shard sh) {
         d_[0] = pt0; d_[1] = pt1; d_[2] = pt2; d_[3] = pt3; d_[4] = gtimer();
         d_[5] = smid_; d_[6] = c_list + c_ovf; d_[7] = (unsigned long long)ni;
     }
+    __syncthreads();                               // block arrays reused by the next call
+}
+
+__global__ void __launch_bounds__(128)
+k_plan(const cc_shard sh) {
+    const long long t = *(volatile long long*)&sh.ctl->t;
+    plan_group(sh, t, (blockIdx.x * blockDim.x + threadIdx.x) >> 5);
 }
 
 // Phase A proper: persistent warps claim work items from the queue.
@@ -788,6 +794,27 @@ k_stage(const cc_shard sh) {
     const uint32_t K = (uint32_t)sh.bin_cap;
     const double t0 = (double)t * sh.dt;
     const double inv_dt = 1.0 / sh.dt;
+    // planning phase (k_plan's work, one group per warp per round), then a
+    // grid-wide barrier: the persistent grid is co-resident (cooperative launch).
+    // Chosen by cc_neuron_step when there are more groups than warps: k_plan's
+    // separate, 48-warps-per-SM grid is faster for a single round (config 1).
+    if (sh.plan_in_stage) {
+        const int rounds = (sh.n_groups + (int)(gridDim.x * STAGE_WARPS) - 1)
+                           / (int)(gridDim.x * STAGE_WARPS);
+        for (int r = 0; r < rounds; ++r)
+            plan_group(sh, t, (r * (int)gridDim.x + (int)blockIdx.x) * STAGE_WARPS + wib);
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(&sh.tailc[64], 1u);
+            unsigned spins = 0;
+            while (*(volatile unsigned*)&sh.tailc[64] < gridDim.x) {
+                __nanosleep(64);
+                if (++spins == (1u << 24)) { cc_raise(ctl, CC_ERR_GRIDSYNC, t); break; }
+            }
+            __threadfence();
+        }
+        __syncthreads();
+    }
     // step t+1's delay >= 2 units (spikes of steps t-1 .. t+1-d_max, all
     // logged): offered to the warps that run out of work items
     __shared__ unsigned a_n[DEL_DMAX], a_pre[DEL_DMAX + 1];
@@ -1251,6 +1278,7 @@ k_deliver(const cc_shard sh) {
         const unsigned long long ev = sh.log_len[pos_mod(t - 1, L)];
         if (ev) atomicAdd(&ctl->rec_events, ev);
         sh.log_ctr[pos_mod(t, L)] = 0ull;      // the slot k_stage(t) fills (step t - d_max - 1)
+        sh.tailc[64] = 0u;                     // k_stage(t)'s grid barrier
         sh.log_len[pos_mod(t, L)] = 0ull;
         ctl->scratch_used = 0ull;
         ctl->stream_used = 0ull;
@@ -1515,11 +1543,32 @@ extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_neuron_step: null shard");
     if (sh->n_local <= 0) return cc_set_error("cc_neuron_step: empty shard");
     const int groups = (sh->n_local + 31) / 32;
-    k_plan<<<(groups + 3) / 4, 128, 0, (cudaStream_t)stream>>>(*sh);
-    if (const int rc = cc_check_launch("k_plan")) return rc;
     const size_t smem = stage_warp_bytes() * STAGE_WARPS;
     if (const int rc = cc_prepare()) return rc;
-    k_stage<<<stage_blocks, 32 * STAGE_WARPS, smem, (cudaStream_t)stream>>>(*sh);
+    // debug_skip bits 16384 / 32768 force the separate / fused planning (tests)
+    const bool fused = (sh->debug_skip & 32768) ||
+                       (!(sh->debug_skip & 16384) && groups > stage_blocks * STAGE_WARPS);
+    if (!fused) {
+        k_plan<<<(groups + 3) / 4, 128, 0, (cudaStream_t)stream>>>(*sh);
+        if (const int rc = cc_check_launch("k_plan")) return rc;
+        k_stage<<<stage_blocks, 32 * STAGE_WARPS, smem, (cudaStream_t)stream>>>(*sh);
+    } else {
+        // cooperative: the grid barrier after the planning phase needs every
+        // block resident (the launch fails instead of hanging otherwise)
+        cc_shard s2 = *sh;
+        s2.plan_in_stage = 1;
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(stage_blocks);
+        lc.blockDim = dim3(32 * STAGE_WARPS);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = (cudaStream_t)stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        cudaLaunchKernelEx(&lc, k_stage, s2);
+    }
     if (const int rc = cc_check_launch("k_stage")) return rc;
     if (sh->n_probe > 0) {
         k_probe<<<(sh->n_local + 255) / 256, 256, 0, (cudaStream_t)stream>>>(*sh);

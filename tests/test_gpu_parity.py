@@ -233,6 +233,36 @@ def test_tail_delivery_off_same_run(cuda, name, monkeypatch):
     assert np.array_equal(t.view(np.uint64), arr["raster_times"].view(np.uint64))
 
 
+@pytest.mark.parametrize("name", ["config0_cal", "tiny_exp"])
+def test_planning_inside_k_stage_same_run(cuda, name, monkeypatch):
+    """The planning pass run by k_stage itself behind a grid barrier (chosen
+    when there are more neuron groups than k_stage warps; forced here with
+    debug bit 32768) reproduces the reference run."""
+    from paper_1803_08833_b200.engine import run_b200
+    cfg, meta, arr = golden_run(name)
+    monkeypatch.setenv("CC_DEBUG_SKIP", "32768")
+    _assert_same_run(run_b200(cfg, 1), meta, arr)
+
+
+def test_planning_modes_agree_at_scale(cuda, monkeypatch):
+    """10x10 columns (3,875 groups > k_stage's warps: planning inside k_stage by
+    default) - the same raster as with the separate k_plan kernel."""
+    from paper_1803_08833_b200.engine import run_b200
+    from paper_1803_08833_b200.network import build_b200
+    from paper_1803_08833_b200.presets import baseline_config
+    from dataclasses import replace
+    from paper_1803_08833_b200 import spec as S
+    cfg = baseline_config(1, "calibrated", duration_s=0.12)
+    cfg = replace(cfg, grid=S.GridSpec(nx=10, ny=10, neurons_per_column=1240))
+    net = build_b200(cfg)
+    a = run_b200(cfg, 1, net=net)
+    monkeypatch.setenv("CC_DEBUG_SKIP", "16384")
+    b = run_b200(cfg, 1, net=net)
+    assert a.n_spikes > 1000
+    assert a.raster_checksum == b.raster_checksum and a.n_spikes == b.n_spikes
+    assert a.recurrent_events == b.recurrent_events and a.external_events == b.external_events
+
+
 def test_delay_segment_table(cuda):
     """cc_build_dseg: dseg[r][d] = synapses of row r with delay <= d."""
     from paper_1803_08833_b200.network import build_b200
