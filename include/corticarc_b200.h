@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 22
+#define CC_ABI_VERSION 23
 
 /* Work items are queued in this many size classes, largest first. */
 /* Input lists per 32-neuron group (events of delay d go to sub-list
@@ -105,7 +105,7 @@ typedef struct cc_shard {
     int32_t out_cap;        /* exchange out-list capacity                      */
     int32_t ext_budget;     /* m = ceil(lam + 12 sqrt(lam)) + 20; 0 = no drive */
     int32_t n_probe;
-    int32_t direct_log;     /* 1: neuron kernel feeds the delivery log itself  */
+    int32_t direct_log;     /* 1: neuron kernel logs its spikes itself (0: out-list only) */
     int32_t debug_skip;     /* timing experiments only: bit mask of k_neuron stages to skip */
     int32_t plan_in_stage;  /* set by cc_neuron_step: k_stage runs the planning itself */
     uint64_t h2_ext;        /* splitmix chain prefix for EXTERNAL (rng.py:85-86)      */
@@ -186,6 +186,9 @@ typedef struct cc_shard {
      * claims in ctl): [0] next step's delay>=2 units claimed by k_stage's idle
      * warps, [32] k_stage warps out of work items, [64] k_stage grid barrier */
     uint32_t* tailc;
+    /* [n_local] or NULL: with direct_log, neurons with a destination shard
+     * other than this one also go to the exchange out-list (cc_pack_aer) */
+    const uint8_t* remote;
 } cc_shard;
 
 /* ---------------------------------------------------------------- misc */

@@ -15,7 +15,7 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BIT
 
 LIB_PATH = os.environ.get("CC_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 22
+ABI_VERSION = 23
 ITEM_CLASSES = 8
 CNT_STRIDE_MAX = 64          # bin_cnt words per group allocated (CC_CNT_STRIDE <= this)
 
@@ -84,7 +84,7 @@ class Shard(C.Structure):
         ("evrec", _P), ("evrec_cap", C.c_int64), ("ev_off", _P), ("grp_items", _P),
         ("grp_done", _P), ("rounds", _P), ("round_cap", C.c_int64),
         ("probe_map", _P), ("probe_out", _P),
-        ("probe_steps", C.c_int64), ("ctl", _P), ("tailc", _P),
+        ("probe_steps", C.c_int64), ("ctl", _P), ("tailc", _P), ("remote", _P),
     ]
 
 

@@ -421,9 +421,8 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
                 s.ru = tj + P->tau_arp;
                 stale = true;
                 ++my_spikes;
-                if (sh.direct_log) {
-                    log_spike(sh, t, gid, tj);
-                } else {
+                if (sh.direct_log) log_spike(sh, t, gid, tj);
+                if (!sh.direct_log || (sh.remote && sh.remote[li])) {   // to other shards
                     const unsigned o = atomicAdd(&ctl->out_n, 1u);
                     if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = tj; }
                     else cc_raise(ctl, CC_ERR_OUTLIST, t);

@@ -123,7 +123,7 @@ class DistributedSimulator:
     steps are captured into a CUDA graph with no host synchronisation."""
 
     def __init__(self, cfg, rank: int, size: int, device=None, group=None, chunk: int = 100,
-                 use_graphs: bool = True, **sim_kw):
+                 use_graphs: bool = True, force_exchange: bool = False, **sim_kw):
         import torch
         from .engine import Simulator
         from .network import build_b200
@@ -131,10 +131,15 @@ class DistributedSimulator:
         self.rank, self.size, self.group = rank, size, group
         self.dev = torch.device(device or f"cuda:{torch.cuda.current_device()}")
         self.net = build_b200(cfg, rank=rank, size=size, device=self.dev)
-        self.sim = Simulator(cfg, self.net, direct_log=False, use_graphs=False, device=self.dev,
-                             **sim_kw)
         has = _has_row_all_ranks(self.net, size, group)
-        masks = dest_masks_from_rows(has, self.sim.gids)
+        n = cfg.grid.neurons_per_column
+        gids = (self.net.owned_columns[:, None].astype(np.int64) * n + np.arange(n)[None, :]).ravel()
+        # own spikes are logged locally by the neuron kernel; only neurons with
+        # rows on other shards go through the exchange (self bit cleared)
+        masks = dest_masks_from_rows(has, gids) & ~np.int64(1 << rank)
+        self.has_remote = bool(masks.any())
+        self.sim = Simulator(cfg, self.net, direct_log=True, remote=masks != 0, use_graphs=False,
+                             device=self.dev, **sim_kw)
         self.mask = torch.as_tensor(masks.astype(np.uint32).view(np.int32), device=self.dev)
         n = cfg.grid.neurons_per_column
         self.local_of_col = np.full(cfg.grid.n_columns, -1, np.int64)
@@ -142,6 +147,9 @@ class DistributedSimulator:
         self.lut = torch.as_tensor(self.local_of_col.astype(np.int32), device=self.dev)
         self.n_col = n
         self.cap = _aer_cap(self.sim)
+        # one rank: nothing to exchange (force_exchange keeps the pack / NCCL /
+        # ingest kernels in the step, to measure or test that path on one GPU)
+        self.exchange_needed = size > 1 or force_exchange
         self.send = torch.zeros((size, 1 + 2 * self.cap), dtype=torch.int64, device=self.dev)
         self.recv = torch.zeros_like(self.send)
         self.chunk = max(1, int(chunk))
@@ -156,6 +164,8 @@ class DistributedSimulator:
         from . import _lib
         L, sim, s = self.sim.L, self.sim, stream.cuda_stream
         sim._launch_step(s)
+        if not self.exchange_needed:
+            return
         _lib.check(L.cc_pack_aer(C.byref(sim.shard), self.mask.data_ptr(), self.size, self.cap,
                                  self.send.data_ptr(), self.lut.data_ptr(), s), "cc_pack_aer")
         self.dist_a2a()
@@ -174,11 +184,12 @@ class DistributedSimulator:
             e[0].record(st)
             sim._launch_step(s)
             e[1].record(st)
-            _lib.check(L.cc_pack_aer(C.byref(sim.shard), self.mask.data_ptr(), self.size,
-                                     self.cap, self.send.data_ptr(), self.lut.data_ptr(), s))
-            self.dist_a2a()
-            _lib.check(L.cc_ingest_aer(C.byref(sim.shard), self.recv.data_ptr(), self.size,
-                                       self.cap, s))
+            if self.exchange_needed:
+                _lib.check(L.cc_pack_aer(C.byref(sim.shard), self.mask.data_ptr(), self.size,
+                                         self.cap, self.send.data_ptr(), self.lut.data_ptr(), s))
+                self.dist_a2a()
+                _lib.check(L.cc_ingest_aer(C.byref(sim.shard), self.recv.data_ptr(), self.size,
+                                           self.cap, s))
             e[2].record(st)
         torch.cuda.synchronize(self.dev)
         self.t += n_steps
@@ -222,7 +233,8 @@ class DistributedSimulator:
             self.sim.check()
 
 
-def run_local_shards(config, size: int, device=None, flat_ingest: bool = False):
+def run_local_shards(config, size: int, device=None, flat_ingest: bool = False,
+                     local_direct: bool = True):
     """All `size` shards of a multi-GPU run, stepped in turn on ONE device.
 
     Same shard code as run_multi_gpu - per-rank generator (build_b200 rank /
@@ -238,14 +250,23 @@ def run_local_shards(config, size: int, device=None, flat_ingest: bool = False):
     from .network import build_b200
     dev = torch.device(device or f"cuda:{torch.cuda.current_device()}")
     nets = [build_b200(config, rank=r, size=size, device=dev) for r in range(size)]
-    sims = [Simulator(config, nets[r], direct_log=False, use_graphs=False, device=dev)
-            for r in range(size)]
     has = [((n.row_off[1:] - n.row_off[:-1]) > 0).cpu().numpy() for n in nets]
+    n = config.grid.neurons_per_column
+    mk = []
+    for r in range(size):
+        gids = (nets[r].owned_columns[:, None].astype(np.int64) * n + np.arange(n)[None, :]).ravel()
+        m = dest_masks_from_rows(has, gids)
+        mk.append(m & ~np.int64(1 << r) if local_direct else m)
+    # local_direct: own spikes logged by the neuron kernel, the exchange carries
+    # only spikes with rows on other shards (DistributedSimulator's mode);
+    # otherwise every spike goes out-list -> pack -> exchange -> ingest
+    sims = [Simulator(config, nets[r], direct_log=local_direct,
+                      remote=(mk[r] != 0) if local_direct else None, use_graphs=False, device=dev)
+            for r in range(size)]
     cap = max(_aer_cap(sm) for sm in sims)
     masks, luts, sends = [], [], []
     for r in range(size):
-        masks.append(torch.as_tensor(dest_masks_from_rows(has, sims[r].gids)
-                                     .astype(np.uint32).view(np.int32), device=dev))
+        masks.append(torch.as_tensor(mk[r].astype(np.uint32).view(np.int32), device=dev))
         lut = np.full(config.grid.n_columns, -1, np.int32)
         lut[nets[r].owned_columns] = np.arange(len(nets[r].owned_columns))
         luts.append(torch.as_tensor(lut, device=dev))
@@ -365,7 +386,7 @@ def bench_distributed(args, cfg) -> None:
     import torch
     import torch.distributed as dist
     rank, size = _init_dist()
-    ds = DistributedSimulator(cfg, rank, size)
+    ds = DistributedSimulator(cfg, rank, size, force_exchange=getattr(args, "exchange", False))
     ds.advance(args.warmup)
     c0 = ds.sim.ctl()
     clocks = None

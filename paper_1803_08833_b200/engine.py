@@ -132,6 +132,7 @@ class Simulator:
     def __init__(self, cfg, net: DeviceNetwork, *, probes=None, probe_steps: int = 0,
                  bin_cap: Optional[int] = None, chunk: int = 100,
                  use_graphs: bool = True, direct_log: Optional[bool] = None,
+                 remote=None,
                  raster_steps: Optional[int] = None, substeps: bool = False, device=None):
         import torch
         self.L = _lib.lib()
@@ -243,6 +244,11 @@ class Simulator:
             sh.ext_budget, sh.ext_thresh = 0, 1.0
         sh.n_probe = n_probe
         sh.direct_log = 1 if direct else 0
+        # exchange with local logging: neurons that also have rows on other
+        # shards go to the out-list as well (uint8 tensor, one entry per neuron)
+        self.remote = None if remote is None else \
+            torch.as_tensor(np.asarray(remote, dtype=np.uint8), device=dev)
+        sh.remote = self.remote.data_ptr() if self.remote is not None else None
         sh.h2_ext = _h2(cfg.seed, P_EXTERNAL)
         sh.h2_time = _h2(cfg.seed, P_EXTERNAL_TIME)
         sh.h2_init = _h2(cfg.seed, P_INIT_STATE)

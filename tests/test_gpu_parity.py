@@ -417,7 +417,9 @@ def test_partition_invariance_on_one_gpu(cuda, name, size):
     SURVEY 8(e))."""
     from paper_1803_08833_b200.distributed import run_local_shards
     cfg, meta, arr = golden_run(name)
-    res = run_local_shards(cfg, size)
+    res = run_local_shards(cfg, size)                    # own spikes logged locally
+    _assert_same_run(res, meta, arr)
+    res = run_local_shards(cfg, size, local_direct=False)   # every spike exchanged
     _assert_same_run(res, meta, arr)
 
 
@@ -426,6 +428,8 @@ def test_partition_invariance_flat_ingest(cuda):
     from paper_1803_08833_b200.distributed import run_local_shards
     cfg, meta, arr = golden_run("tiny_gauss")
     res = run_local_shards(cfg, 2, flat_ingest=True)
+    _assert_same_run(res, meta, arr)
+    res = run_local_shards(cfg, 2, flat_ingest=True, local_direct=False)
     _assert_same_run(res, meta, arr)
 
 
@@ -442,7 +446,7 @@ def test_exchange_mode_single_rank_matches_reference(cuda):
     os.environ.setdefault("MASTER_PORT", "29517")
     dist.init_process_group("nccl", rank=0, world_size=1)
     try:
-        ds = DistributedSimulator(cfg, 0, 1, chunk=25)
+        ds = DistributedSimulator(cfg, 0, 1, chunk=25, force_exchange=True)
         ds.advance(cfg.n_steps)
         g, t = ds.sim.raster()
         c = ds.sim.ctl()
