@@ -22,6 +22,9 @@
 #ifndef CC_CNT_STRIDE
 #define CC_CNT_STRIDE 64
 #endif
+#ifndef CC_STATIC_FIRST
+#define CC_STATIC_FIRST 1     // k_stage: each warp's first item by its index
+#endif
 #ifndef CC_TAIL_STOP
 #define CC_TAIL_STOP 12
 #endif
@@ -830,10 +833,20 @@ k_stage(const cc_shard sh) {
     for (int c = 0; c < CC_ITEM_CLASSES; ++c) n_items += cls_n[c];
     if (*(volatile unsigned*)&ctl->error_bits) n_items = 0u;
     uint32_t my_spikes = 0;
+    // first item of every warp by its index (no burst of same-address claims
+    // at kernel start), the rest claimed in order after them
+    const unsigned n_stage_warps = gridDim.x * STAGE_WARPS;
+    bool first = CC_STATIC_FIRST != 0;
     for (;;) {
         unsigned item = 0;
-        if (lane == 0) item = atomicAdd(&ctl->round_next, 1u);
-        item = __shfl_sync(0xffffffffu, item, 0);
+        if (first) {
+            item = blockIdx.x * STAGE_WARPS + wib;
+            first = false;
+        } else {
+            if (lane == 0)
+                item = atomicAdd(&ctl->round_next, 1u) + (CC_STATIC_FIRST ? n_stage_warps : 0u);
+            item = __shfl_sync(0xffffffffu, item, 0);
+        }
         if (item >= n_items) break;
         CC_DBG(0, gtimer());
         unsigned r = item;                        // class c, position r in it
