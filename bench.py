@@ -90,12 +90,36 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def n_ranks(args) -> int:
+    return max(int(os.environ.get("WORLD_SIZE", "1")), args.gpus)
+
+
+def weak_tiling(n: int):
+    """Column blocks of the weak-scaling series: n GPUs -> (a, b) copies of the
+    single-GPU grid along x and y, a >= b, a * b = n (1, 2x1, 2x2, 4x2)."""
+    b = int(math.isqrt(n))
+    while n % b:
+        b -= 1
+    return n // b, b
+
+
 def workload(args):
+    from dataclasses import replace
     from paper_1803_08833_b200.presets import baseline_config
     cfg = baseline_config(args.config, "calibrated", kernel=args.kernel,
                           duration_s=(args.warmup + args.steps) / 1000.0, seed=args.seed,
                           drive_hz=args.drive)
+    n = n_ranks(args)
+    if n > 1 and args.scaling == "weak":
+        # per-GPU work fixed: the BASELINE grid once per GPU, tiled (the column
+        # partition hands each rank one block of about the single-GPU size)
+        a, b = weak_tiling(n)
+        cfg = replace(cfg, grid=replace(cfg.grid, nx=cfg.grid.nx * a, ny=cfg.grid.ny * b))
     return cfg
+
+
+def scaling_of(args) -> str:
+    return "weak" if n_ranks(args) > 1 and args.scaling == "weak" else "strong"
 
 
 def oracle_net(net):
@@ -174,7 +198,7 @@ def run_reference_arm(args):
     line = {
         "metric": "synaptic events/s (recurrent + external)", "value": r["value"],
         "unit": "events/s", "n_gpus": args.gpus, "steps": r["steps"], "warmup": 0,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": scaling_of(args),
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, same connectivity)",
         "config": config_block(cfg, None, args) | {"synapses": int(len(w))}, "impl": "reference",
         "cpu_baseline": {"value": r["value"], "unit": "events/s", "cores": k, "kind": "port",
@@ -237,6 +261,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--instrument-steps", type=int, default=200)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = the config's grid once per GPU (default), "
+                         "strong = the config's grid split over the GPUs")
     ap.add_argument("--exchange", action="store_true",
                     help="run the multi-GPU (exchange-mode) path even on one rank")
     args = ap.parse_args()

@@ -430,12 +430,19 @@ def bench_distributed(args, cfg) -> None:
             "metric": "synaptic events/s (recurrent + external)",
             "value": total / (ms_v / 1e3), "unit": "events/s", "n_gpus": size,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_v / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True,
+            "scaling": "weak" if (size > 1 and getattr(args, "scaling", "strong") == "weak")
+            else "strong",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded counter-based RNG (connectivity, Poisson drive), "
                     "bit-exact with the reference streams",
-            "config": {"workload": f"BASELINE config {args.config}: {cfg.grid.nx}x{cfg.grid.ny} "
-                                   f"columns x {cfg.grid.neurons_per_column} neurons, "
-                                   f"{cfg.kernel.kind} lateral decay, calibrated drive",
+            "config": {"workload": (f"BASELINE config {args.config}"
+                                    + (" grid once per GPU (weak scaling)"
+                                       if size > 1 and getattr(args, "scaling", "") == "weak"
+                                       else "")
+                                    + f": {cfg.grid.nx}x{cfg.grid.ny} columns x "
+                                      f"{cfg.grid.neurons_per_column} neurons, "
+                                      f"{cfg.kernel.kind} lateral decay, calibrated drive"),
                        "grid": f"{cfg.grid.nx}x{cfg.grid.ny}", "neurons": cfg.grid.n_neurons,
                        "parallelism": f"column blocks x{size} (one process per GPU, NCCL)",
                        "l2": "no flush between steps (per-step working set > 126 MB L2)"},
