@@ -71,7 +71,7 @@ SPILL_VARIANT = os.path.join(PKG, "libcorticarc_b200_w4.so")
 def build_test_variants(force: bool = False) -> None:
     if force or not os.path.exists(SPILL_VARIANT) or \
             os.path.getmtime(SPILL_VARIANT) < os.path.getmtime(LIB):
-        build(force=True, out=SPILL_VARIANT, defines=("CC_NEURON_WCAP=4",))
+        build(force=True, out=SPILL_VARIANT, defines=("CC_NEURON_WCAP=4", "CC_UPD_PIPE=0"))
 
 
 if __name__ == "__main__":
