@@ -344,7 +344,7 @@ __device__ __forceinline__ bool slow_step(NState& s, const cc_pop& P, double tj,
 // step-start refractory window; after a spike they are recomputed in line
 // (slow_step).  The ordered 48 B records {t, w}, {em, ec}, {f, ecr} reach the
 // warp's (idle) shared buffer by cp.async (L2 only): CC_UPD_NBUF batches of
-// CC_UPD_UB inputs per neuron are in flight while one is applied, so a
+// one input per neuron each are in flight while one is applied, so a
 // neuron's serial chain does not wait for an L2 round trip per input (1 input
 // x 3 buffers: 97.2 -> 94.3 us per step at config 1; the single-buffer
 // fallback, 5 inputs per round trip, serves builds whose buffer is too small).
@@ -353,15 +353,12 @@ constexpr int UB = stage_warp_bytes() / (32 * 48) < 5 ? (int)(stage_warp_bytes()
 constexpr int UB_STRIDE = 3 * UB;        // double2 per lane: 15 = 7 mod 8, conflict-free
 static_assert(32 * UB_STRIDE * 16 <= stage_warp_bytes(), "update batch > stage buffer");
 #ifndef CC_UPD_PIPE
-#define CC_UPD_PIPE 1        // update: CC_UPD_NBUF batches of CC_UPD_UB inputs in flight
+#define CC_UPD_PIPE 1        // update: CC_UPD_NBUF single-input batches in flight
 #endif
 #ifndef CC_UPD_NBUF
 #define CC_UPD_NBUF 3
 #endif
-#ifndef CC_UPD_UB
-#define CC_UPD_UB 1
-#endif
-static_assert(!CC_UPD_PIPE || CC_UPD_NBUF * 32 * 3 * CC_UPD_UB * 16 <= (int)stage_warp_bytes(),
+static_assert(!CC_UPD_PIPE || CC_UPD_NBUF * 32 * 3 * 16 <= (int)stage_warp_bytes(),
               "update pipeline > stage buffer");
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -394,33 +391,35 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
     const bool cflag = s.c != 0.0;
     bool stale = false;                      // spiked: factors need recomputing
 #if CC_UPD_PIPE
-    // NBUF buffers of UBP inputs per lane in flight: batch j+NBUF is loading
-    // while batch j is applied (cp.async groups, wait_group NBUF-1)
-    auto issue = [&](uint32_t j) {
-        double2* dst = S + ((j % CC_UPD_NBUF) * 32 + lane) * (3 * CC_UPD_UB);
-        const uint32_t b = j * CC_UPD_UB;
-        const double2* Rn = R + 3 * (size_t)(off + b);
-        const uint32_t m = n > b ? min(n - b, (uint32_t)CC_UPD_UB) : 0u;
-#pragma unroll
-        for (int k = 0; k < CC_UPD_UB; ++k) {
-            if ((uint32_t)k < m) {
-                cp_async16(dst + 3 * k, Rn + 3 * k);
-                cp_async16(dst + 3 * k + 1, Rn + 3 * k + 1);
-                cp_async16(dst + 3 * k + 2, Rn + 3 * k + 2);
-            }
+    // CC_UPD_NBUF single-input buffers per lane in flight: input i+NBUF is
+    // loading while input i is applied (cp.async groups, wait_group NBUF-1);
+    // rotating buffer indices, one 48 B slot per lane and buffer
+    double2* const sb = S + lane * 3;
+    constexpr int BS = 32 * 3;                   // double2 per buffer
+    const double2* Rp = R + 3 * (size_t)off;     // next record of this lane to fetch
+    uint32_t jn = 0;                             // its input index
+    int bn = 0, bi = 0;                          // buffer to fill next / to apply
+    auto issue = [&]() {
+        if (jn < n) {
+            double2* d = sb + bn * BS;
+            cp_async16(d, Rp);
+            cp_async16(d + 1, Rp + 1);
+            cp_async16(d + 2, Rp + 2);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
+        Rp += 3;
+        ++jn;
+        bn = bn + 1 == CC_UPD_NBUF ? 0 : bn + 1;
     };
-    const uint32_t nb = (nmax + CC_UPD_UB - 1) / CC_UPD_UB;
     __syncwarp();
 #pragma unroll
-    for (int j = 0; j < CC_UPD_NBUF; ++j) issue((uint32_t)j);
-    for (uint32_t jb = 0; jb < nb; ++jb) {
+    for (int j = 0; j < CC_UPD_NBUF; ++j) issue();
+    for (uint32_t b0 = 0; b0 < nmax; ++b0) {
         asm volatile("cp.async.wait_group %0;" ::"n"(CC_UPD_NBUF - 1) : "memory");
         __syncwarp();
-        const uint32_t b0 = jb * CC_UPD_UB;
-        const double2* my = S + ((jb % CC_UPD_NBUF) * 32 + lane) * (3 * CC_UPD_UB);
-        const uint32_t e = min(n, b0 + (uint32_t)CC_UPD_UB);
+        const double2* my = sb + bi * BS;
+        bi = bi + 1 == CC_UPD_NBUF ? 0 : bi + 1;
+        const uint32_t e = min(n, b0 + 1u);
 #else
     const double2* my = S + lane * UB_STRIDE;
     for (uint32_t b0 = 0; b0 < nmax; b0 += UB) {
@@ -483,8 +482,8 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
             }
         }
 #if CC_UPD_PIPE
-        __syncwarp();                            // buffer jb % NBUF consumed
-        issue(jb + CC_UPD_NBUF);
+        __syncwarp();                            // buffer consumed
+        issue();
 #endif
     }
     if (n) {
