@@ -67,7 +67,7 @@ typedef struct cc_ctl {
     unsigned int pad2;
     unsigned int error_bits;
     long long error_step;
-    unsigned int max_bin;                 /* max events at one (slot, neuron) */
+    unsigned int max_bin;                 /* max recurrent inputs of one neuron-step */
     unsigned int max_events;              /* max events of one neuron-step    */
     unsigned long long scratch_used;      /* staging events spilled (this step) */
     unsigned int out_n;                   /* exchange out-list fill           */
@@ -224,9 +224,10 @@ int cc_deliver(const cc_shard* sh, void* stream);
  * cc_neuron_step calls it itself otherwise. */
 int cc_prepare(void);
 
-/* Step phases (4)-(6): drain the ring slot of step t, generate the external
+/* Step phases (4)-(6): drain the step's input lists, generate the external
  * Poisson events, order each neuron's inputs by (time, source, weight) and
- * integrate them exactly; emit spikes.  Increments ctl->t.
+ * integrate them exactly; emit spikes; idle warps deliver the next step's
+ * delay >= 2 events.  Increments ctl->t.
  * Replaces DelayRing.drain (engine.py:151-163), _external_events
  * (engine.py:191-206), the lexsort (engine.py:386) and
  * NeuronBlock.integrate_sorted (model.py:289-337). */

@@ -1,12 +1,17 @@
 // Simulation-step kernels of the B200 engine (sm_100a).
 //
 // Per 1 ms step t (engine.py:318-394):
-//   k_deliver   arborise the spikes of step t-1 into the delay ring of event
-//               records (engine.py:338-367, DelayRing.insert :138-149)
-//   k_neuron    drain ring slot t, add the external Poisson events, order each
-//               neuron's inputs by (time, source, weight), integrate exactly in
-//               float64, emit spikes (engine.py:371-394, model.py:272-337)
-// plus k_ingest / k_pack_aer / k_ingest_aer for multi-shard runs and k_init_state.
+//   k_deliver   the events arriving at t not yet delivered: the delay-d segments
+//               of the rows of step t-d's spikes (engine.py:338-367 and
+//               DelayRing, :124-163, as a pull from the spike log)
+//   k_plan      per group of 32 neurons: input counts, the Poisson drive count
+//               (engine.py:172-188), work items
+//   k_stage     gather + drive times, order each neuron's inputs by (time,
+//               source, weight), decay factors, the in-order float64 update,
+//               spikes (engine.py:191-206, 386, model.py:272-337); its idle
+//               warps deliver step t+1's delay >= 2 events
+// plus k_ingest / k_pack_aer / k_ingest_aer for multi-shard runs, k_build_dseg
+// and k_init_state.
 //
 // Exactness contract: every float64 expression below
 // follows the reference's evaluation order; the file is compiled with
@@ -1238,12 +1243,7 @@ k_stage(const cc_shard sh) {
     }
 }
 
-// ------------------------------------------------------------------ k_update
-// Phase B: one thread per neuron walks its staged events in order (coalesced:
-// lane L reads slot 32 i + L) and applies the closed-form update, jump,
-// strict threshold, reset and refractory rule of NeuronBlock.integrate_sorted
-// (model.py:289-337).  After a spike the remaining factors of that neuron are
-// recomputed in line (the staged ones assumed the old refractory window).
+// ------------------------------------------------------------------ k_probe
 // Probe recording (tests only): state of the probed neurons after step t and
 // V advanced to (t+1)*dt on a copy, the harness of oracle/make_golden.py.
 __global__ void k_probe(const cc_shard sh) {
