@@ -510,7 +510,11 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
 #ifndef CC_DEL_U
 #define CC_DEL_U 8          // synapses per lane per pass
 #endif
-constexpr int DEL_SPU = 4;                  // spikes per unit (8 lanes each)
+#ifndef CC_DEL_SPU
+#define CC_DEL_SPU 4
+#endif
+constexpr int DEL_SPU = CC_DEL_SPU;         // spikes per unit
+constexpr int DEL_LPS = 32 / DEL_SPU;       // lanes per spike
 constexpr int DEL_DMAX = 256;               // d_max <= 255 (uint8 delays)
 
 // Input lists of arrival step t: two sets (t & 1), so that step t+1's
@@ -554,7 +558,7 @@ __device__ __forceinline__ void unit_desc(const cc_shard& sh, long long ta, cons
                                           const unsigned* s_pre, unsigned u, int& kc,
                                           uint64_t& st, uint32_t& ln, uint32_t& rf) {
     while (s_pre[kc + 1] <= u) ++kc;
-    const unsigned idx = (u - s_pre[kc]) * DEL_SPU + ((threadIdx.x & 31) >> 3);
+    const unsigned idx = (u - s_pre[kc]) * DEL_SPU + ((threadIdx.x & 31) / DEL_LPS);
     st = 0; ln = 0; rf = 0;
     if (idx < s_n[kc]) {
         const int d = unit_delay(kc, sh.d_max);
@@ -576,10 +580,10 @@ __device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
 template <int U>
 __device__ __forceinline__ void load_pass(const cc_shard& sh, uint64_t st, uint32_t ln, int p,
                                           int* tg, float* w) {
-    const int sl = threadIdx.x & 7;
+    const int sl = threadIdx.x % DEL_LPS;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const uint32_t j = (uint32_t)(p * 8 * U + u * 8 + sl);
+        const uint32_t j = (uint32_t)(p * DEL_LPS * U + u * DEL_LPS + sl);
         tg[u] = -1;
         if (j < ln) {
             tg[u] = __ldg(sh.syn_tgt + st + j);
@@ -1208,9 +1212,9 @@ k_stage(const cc_shard sh) {
             uint64_t st;
             uint32_t ln, rf;
             unit_desc(sh, t + 1, a_n, a_pre, u, kc, st, ln, rf);
-            if ((lane & 7) == 0) tail_ev += ln;          // one lane per spike
+            if (lane % DEL_LPS == 0) tail_ev += ln;      // one lane per spike
             const uint32_t lmax = warp_max_u32(ln);
-            for (int p = 0; (uint32_t)(p * 8 * UT) < lmax; ++p) {
+            for (int p = 0; (uint32_t)(p * DEL_LPS * UT) < lmax; ++p) {
                 int tg[UT];
                 float w[UT];
                 load_pass<UT>(sh, st, ln, p, tg, w);
@@ -1355,7 +1359,7 @@ k_deliver(const cc_shard sh) {
     const unsigned nw = (gridDim.x * blockDim.x) >> 5;
     const unsigned long long dbg_t1 = gtimer();
     constexpr int U = CC_DEL_U;
-    constexpr int SPAN = 8 * U;                              // synapses per spike per pass
+    constexpr int SPAN = DEL_LPS * U;                        // synapses per spike per pass
     int kc = 0;
     unsigned u = c0 + wid;
     uint64_t st = 0, stn = 0;
@@ -1368,7 +1372,7 @@ k_deliver(const cc_shard sh) {
     int tg[U];
     float w[U];
     if (u < n_units) load_pass<U>(sh, st, ln, 0, tg, w);
-    const bool cnt_lane = (lane & 7) == 0;                   // one lane per spike counts
+    const bool cnt_lane = lane % DEL_LPS == 0;               // one lane per spike counts
     unsigned long long my_ev = (u < n_units && cnt_lane) ? ln : 0u;
     while (u < n_units) {
         // next pass of this unit, else the first pass of the warp's next unit
