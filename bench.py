@@ -352,12 +352,13 @@ def bench_single(args):
     achieved = (run_b["dep"] * BYTES_PER_EVENT / (run_b["del_ms"] / 1e3) / 1e9
                 if run_b["del_ms"] > 0 else 0.0)
     traffic = None
+    stage_ncu = {}
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            prof_d = json.load(open(prof))
-            traffic = prof_d.get(f"config{args.config}", {}).get("k_deliver", {}).get(
-                "dram_bytes_per_launch")
+            prof_d = json.load(open(prof)).get(f"config{args.config}", {})
+            traffic = prof_d.get("k_deliver", {}).get("dram_bytes_per_launch")
+            stage_ncu = prof_d.get("k_stage", {})
         except Exception:
             traffic = None
     kernels = {
@@ -395,6 +396,18 @@ def bench_single(args):
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                      "peak_source": peak_src,
                      "bytes_per_event": BYTES_PER_EVENT},
+        "dominant_kernel": {
+            "kernel": "k_plan + k_stage (k_neuron)", "share": neu_ms / (del_ms + neu_ms),
+            "inputs_per_s": run_a["ev"] / NI / (neu_ms / NI / 1e3),
+            "bound": "fp64 latency / issue: per input 2 exp, 1 expm1, 4 divides, the "
+                     "exact ordering and a serial in-order update; 20 resident warps/SM",
+            "k_stage_ncu": {k: stage_ncu[k] for k in ("warp_instructions", "ipc_per_sm",
+                                                        "warps_active_per_sm",
+                                                        "dram_bytes_per_launch", "source")
+                            if k in stage_ncu},
+            "why_not_the_roofline_kernel": "neither HBM- nor tensor-bound (IPC ~1.5 of 4, "
+                                           "DRAM ~0.3 TB/s); the HBM roofline is reported "
+                                           "for the delivery kernel (north star)"},
         "step_roofline": {"achieved": rec / (ms / 1e3) * BYTES_PER_EVENT / 1e9, "peak": hbm,
                           "unit": "GB/s",
                           "frac": rec / (ms / 1e3) * BYTES_PER_EVENT / 1e9 / hbm,

@@ -102,6 +102,10 @@ with open(os.path.join(dst, f"{tag}_kernels.md"), "w") as fh:
             return x * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1}.get(u, 1)
         summary[name.split("<")[0]] = {
             "dram_bytes_per_launch": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
+            "warp_instructions": num("smsp__inst_executed.sum"),
+            "ipc_per_sm": (num("smsp__inst_executed.sum") / max(1.0, num("sm__cycles_active.avg"))
+                           / 148.0),
+            "warps_active_per_sm": num("sm__warps_active.avg.per_cycle_active"),
             "duration_us_ncu": float(d["gpu__time_duration.sum"][0].replace(",", "")) *
             {"nsecond": 1e-3, "ns": 1e-3, "msecond": 1e3, "ms": 1e3}.get(
                 d["gpu__time_duration.sum"][1], 1.0),
