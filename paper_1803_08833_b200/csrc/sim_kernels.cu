@@ -31,7 +31,7 @@
 #define CC_STATIC_FIRST 1     // k_stage: each warp's first item by its index
 #endif
 #ifndef CC_TAIL_STOP
-#define CC_TAIL_STOP 12
+#define CC_TAIL_STOP 10
 #endif
 #ifndef CC_CSR_STREAM
 #define CC_CSR_STREAM 0
