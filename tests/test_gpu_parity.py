@@ -263,6 +263,49 @@ def test_planning_modes_agree_at_scale(cuda, monkeypatch):
     assert a.recurrent_events == b.recurrent_events and a.external_events == b.external_events
 
 
+def _edge_config(name):
+    from dataclasses import replace
+    from paper_1803_08833_b200 import spec as S
+    from conftest import tiny_config
+    base = tiny_config(nx=3, ny=3, n_col=40, duration_s=0.12, seed=5)
+    g = base.genspec
+    if name == "dmax1":              # one delay step: no delay >= 2 units at all
+        return replace(base, genspec=replace(g, delay_min_ms=1.0, delay_max_ms=1.0,
+                                             d_max_steps=1))
+    if name == "dmax40":             # long ring: 41 log slots, 48-entry segment rows
+        return replace(base, genspec=replace(g, delay_min_ms=1.0, delay_max_ms=40.0,
+                                             d_max_steps=40))
+    if name == "expdelay":           # exponential delay law clipped at d_max
+        return replace(base, genspec=replace(g, delay_kind="exponential", delay_mean_ms=4.0,
+                                             d_max_steps=12))
+    if name == "one_column":         # no lateral targets, every synapse local
+        return replace(base, grid=S.GridSpec(nx=1, ny=1, neurons_per_column=64))
+    if name == "no_drive":           # ext_budget 0: no Poisson draws, silent network
+        return replace(base, external=S.ExternalInputSpec(synapses_per_neuron=0.0,
+                                                          rate_per_synapse_hz=0.0,
+                                                          weight_mv=0.0))
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("name", ["dmax1", "dmax40", "expdelay", "one_column", "no_drive"])
+def test_edge_configs_match_oracle(cuda, name):
+    """Corners of the delivery and drive paths against the CPU oracle (itself
+    pinned to the reference by tests/test_oracle_golden.py)."""
+    from oracle import corticarc_oracle as O
+    from paper_1803_08833_b200.engine import run_b200
+    cfg = _edge_config(name)
+    res = run_b200(cfg, 1, chunk=25)
+    ref = O.run_oracle(cfg)
+    assert res.construction_checksum == ref.construction_checksum
+    assert res.n_spikes == ref.n_spikes
+    if name != "no_drive":
+        assert res.n_spikes > 0
+    assert np.array_equal(res.raster_gids, ref.raster_gids)
+    assert np.array_equal(res.raster_times.view(np.uint64), ref.raster_times.view(np.uint64))
+    assert res.recurrent_events == ref.recurrent_events
+    assert res.external_events == ref.external_events
+
+
 def test_delay_segment_table(cuda):
     """cc_build_dseg: dseg[r][d] = synapses of row r with delay <= d."""
     from paper_1803_08833_b200.network import build_b200
