@@ -129,6 +129,8 @@ def _spikes_per_step_bound(cfg) -> int:
 class Simulator:
     """One shard's device state and step loop."""
 
+    TIMED_STEPS = 10          # steps of the sampled chunk carrying event-record nodes
+
     def __init__(self, cfg, net: DeviceNetwork, *, probes=None, probe_steps: int = 0,
                  bin_cap: Optional[int] = None, chunk: int = 100,
                  use_graphs: bool = True, direct_log: Optional[bool] = None,
@@ -333,8 +335,8 @@ class Simulator:
         """The chunk graph of pipeline slot `slot` (its raster buffer), ending
         with the counter snapshot and the raster reset; timed: event-record
         nodes before and after each step's delivery (2 per step + 1 at the
-        end) - used for one sampled chunk only, since the nodes cost ~9 % of
-        the step."""
+        end) on its first TIMED_STEPS steps - one sampled chunk only, since the
+        nodes cost ~9 % of a timed step."""
         torch = self.torch
         if timed and self._timer is None:
             self._timer = C.c_void_p()
@@ -342,17 +344,18 @@ class Simulator:
         tm = self._timer if timed else None
         sh = self.shards[slot]
         g = torch.cuda.CUDAGraph()
+        n_timed = min(steps, self.TIMED_STEPS)
         with torch.cuda.graph(g, stream=stream_obj):
             s = torch.cuda.current_stream(self.dev).cuda_stream
             for i in range(steps):
-                if tm is not None:
+                if tm is not None and i < n_timed:
                     _lib.check(self.L.cc_timer_record(tm, 2 * i, s))
                 _lib.check(self.L.cc_deliver(C.byref(sh), s), "cc_deliver")
-                if tm is not None:
+                if tm is not None and i < n_timed:
                     _lib.check(self.L.cc_timer_record(tm, 2 * i + 1, s))
                 _lib.check(self.L.cc_neuron_step(C.byref(sh), s), "cc_neuron_step")
-            if tm is not None:
-                _lib.check(self.L.cc_timer_record(tm, 2 * steps, s))
+                if tm is not None and i == n_timed - 1:
+                    _lib.check(self.L.cc_timer_record(tm, 2 * n_timed, s))
             self.buf["snap"][slot].copy_(self.buf["ctl"])
             self.buf["ctl"][4].zero_()                       # raster_n
         if timed:
@@ -362,6 +365,7 @@ class Simulator:
         return g
 
     def _read_substeps(self, steps: int) -> None:
+        steps = min(steps, self.TIMED_STEPS)
         el = self.L.cc_timer_elapsed_ms
         d = sum(el(self._timer, 2 * i, 2 * i + 1) for i in range(steps))
         n = sum(el(self._timer, 2 * i + 1, 2 * i + 2) for i in range(steps))
