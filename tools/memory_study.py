@@ -1,6 +1,7 @@
 """Bytes per synapse stored and on-device generation throughput, Gaussian vs
 exponential (the paper's memory study), for BASELINE configs
-1-4.  Config 4 (96x96) is built as rank 0 of an 8-GPU tiling (one GPU's shard)."""
+1-4, plus the simulation buffers a Simulator allocates on top.  Config 4
+(96x96) is built as rank 0 of an 8-GPU tiling (one GPU's shard)."""
 import json
 import os
 import sys
@@ -19,7 +20,7 @@ out = []
 for idx, kern, size in cases:
     if only and f"{idx}{kern[0]}" not in only:
         continue
-    cfg = baseline_config(idx, "literal", kernel=kern)
+    cfg = baseline_config(idx, "calibrated", kernel=kern)
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     t0 = time.perf_counter()
@@ -37,6 +38,15 @@ for idx, kern, size in cases:
                reference_bytes_per_synapse_steady=12.0, reference_peak_floor=24.0,
                max_row=net.row_len_max, halo_sources=len(net.src_gids),
                checksum=f"0x{net.checksum:016x}", gpu_mem_peak_gb=torch.cuda.max_memory_allocated() / 1e9)
+    # the simulation's own device buffers on top (input lists, spike log,
+    # ordered-input records, spill staging, raster, delay-segment table)
+    from paper_1803_08833_b200.engine import Simulator
+    sim = Simulator(cfg, net, use_graphs=False)
+    torch.cuda.synchronize()
+    row.update(sim_buffer_bytes=sim.device_bytes,
+               dseg_bytes=sum(v.numel() * v.element_size() for v in net.dseg_cache.values()),
+               device_allocated_gb=torch.cuda.memory_allocated() / 1e9)
+    del sim
     print(json.dumps(row), flush=True)
     out.append(row)
     del net
