@@ -42,7 +42,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BYTES_PER_EVENT = 17          # 9 B CSR record + 8 B deposit
-KERNELS_PER_STEP = 3          # k_deliver, k_plan, k_stage
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
@@ -414,7 +413,7 @@ def bench_single(args):
                           "definition": "recurrent events/s x 17 B over the whole step "
                                         "(BASELINE.md roofline formula)"},
         "kernels": kernels,
-        "gpu_launches": KERNELS_PER_STEP * K,
+        "gpu_launches": int(L.cc_kernels_per_step(sim.shard.n_groups)) * K,
         "clocks": clk,
         "construction_s": net.construction_seconds,
         "bytes_per_synapse_steady": net.steady_bytes / max(1, net.n_synapses),

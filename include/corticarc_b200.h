@@ -258,6 +258,10 @@ int cc_ingest_aer(const cc_shard* sh, const int64_t* recv, int32_t n_src, int32_
 /* CC_SUBLISTS as compiled (hosts size bin_cnt / bin_rec / grp_sub with it). */
 int32_t cc_sublists(void);
 
+/* Kernels cc_deliver + cc_neuron_step launch per step for a shard of n_groups
+ * 32-neuron groups (3, or 2 when the planning runs inside k_stage). */
+int32_t cc_kernels_per_step(int32_t n_groups);
+
 /* Delay-segment table of a CSR whose rows are sorted by delay: out[r][d] =
  * synapses of row r with delay <= d, d = 0..d_max (u16, row stride `stride`).
  * Sets *err (CC_ERR_DSEG) if a row exceeds 65535 synapses. */

@@ -125,6 +125,7 @@ _SIGS = {
     "cc_gen_warps": (C.c_int64, []),
     "cc_build_dseg": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]),
     "cc_sublists": (C.c_int32, []),
+    "cc_kernels_per_step": (C.c_int32, [C.c_int32]),
     "cc_csr_checksum": (C.c_int, [_P, _P, C.c_int64, _P, _P, _P, C.c_int32, C.c_int32, _P, _P]),
     "cc_test_philox": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_int32,
                                  _P, _P]),

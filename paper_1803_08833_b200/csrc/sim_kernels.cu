@@ -1560,6 +1560,14 @@ static int sm_count() {
 
 extern "C" int32_t cc_sublists(void) { return CC_SUBLISTS; }
 
+static int stage_blocks_(void);
+
+// Kernels cc_deliver + cc_neuron_step launch per step for a shard of n_groups
+// neuron groups (k_plan runs inside k_stage when groups outnumber its warps).
+extern "C" int32_t cc_kernels_per_step(int32_t n_groups) {
+    return n_groups > stage_blocks_() * STAGE_WARPS ? 2 : 3;
+}
+
 extern "C" int cc_build_dseg(const int64_t* row_off, const uint8_t* syn_d, int64_t n_rows,
                              int32_t d_max, int32_t stride, uint16_t* out, unsigned* err,
                              void* stream) {
@@ -1599,6 +1607,11 @@ extern "C" int cc_prepare(void) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage, 32 * STAGE_WARPS, smem);
     stage_blocks = sm_count() * (per_sm > 0 ? per_sm : 1);
     return 0;
+}
+
+static int stage_blocks_(void) {
+    cc_prepare();
+    return stage_blocks;
 }
 
 extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
