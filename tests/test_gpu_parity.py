@@ -452,8 +452,8 @@ def test_event_bookkeeping_matches_fanout(cuda):
     assert res.recurrent_events == int((row_off[g + 1] - row_off[g]).sum())
 
 
-@pytest.mark.parametrize("name,size", [("tiny_gauss", 2), ("tiny_gauss", 4), ("tiny_exp", 2),
-                                       ("config0_cal_0p1", 4)])
+@pytest.mark.parametrize("name,size", [("tiny_gauss", 2), ("tiny_gauss", 4), ("tiny_gauss", 8),
+                                       ("tiny_exp", 2), ("config0_cal_0p1", 4)])
 def test_partition_invariance_on_one_gpu(cuda, name, size):
     """W shards (per-rank generator, exchange-mode neuron step, AER exchange,
     cc_pack_aer / cc_ingest_aer) stepped on one B200 give the reference raster (acceptance #4,
