@@ -1068,7 +1068,7 @@ k_stage(const cc_shard sh) {
             // exclusive scan of the flattened counters: bucket starts, which
             // are already segmented by neuron (lane-major order); packed
             // start | count << 16
-            const uint32_t per = (nbt + 31u) / 32u;
+            const uint32_t per = ((nbt + 31u) / 32u) | 1u;      // odd: lane chunks hit distinct banks
             const uint32_t i0 = min(lane * per, nbt), i1 = min(i0 + per, nbt);
             uint32_t sum = 0;
             for (uint32_t i = i0; i < i1; ++i) sum += B.hist[i];
