@@ -306,6 +306,49 @@ def test_edge_configs_match_oracle(cuda, name):
     assert res.external_events == ref.external_events
 
 
+def test_baseline_config1_matches_oracle(cuda):
+    """BASELINE config 1 itself (8x8 columns, 95 M synapses, calibrated drive):
+    the first 40 steps - the synchronous onset of ~600 spikes per step -
+    bit-identical to the CPU oracle on the same (GPU-generated, reference-
+    identical) connectivity: every spike gid and float64 time, per-step counts."""
+    import time
+    from oracle import corticarc_oracle as O
+    from paper_1803_08833_b200.engine import Simulator
+    from paper_1803_08833_b200.network import build_b200
+    from paper_1803_08833_b200.presets import baseline_config
+    steps = 40
+    cfg = baseline_config(1, "calibrated", duration_s=steps / 1000.0)
+    net = build_b200(cfg)
+    row_off, tgt, w, d = net.host_csr()
+    ln = np.diff(row_off)
+    src = np.flatnonzero(ln).astype(np.uint64)
+    offs = np.concatenate([row_off[src.astype(np.int64)], [row_off[-1]]]).astype(np.int64)
+    onet = O.ShardNet(src, offs, tgt.astype(np.uint32), d.astype(np.uint16), w, net.checksum,
+                      net.n_synapses)
+    sim = Simulator(cfg, net, chunk=10)
+    sim.advance(steps)
+    g, t = sim.raster()
+    c = sim.ctl()
+    osim = O.ShardSim(cfg, onet)
+    og, ot = [], []
+    t0 = time.time()
+    for step in range(steps):
+        inc = [osim.outgoing()] if len(osim.prev_idx) else []
+        a, b = osim.step(step, inc)
+        og.append(a)
+        ot.append(b)
+    og, ot = np.concatenate(og), np.concatenate(ot)
+    o = np.lexsort((og, ot))
+    og, ot = og[o], ot[o]
+    assert len(og) > 5000, len(og)
+    assert np.array_equal(g, og.astype(np.uint64))
+    assert np.array_equal(t.view(np.uint64), ot.view(np.uint64))
+    assert int(c.ext_events) == osim.ext
+    # recurrent events: the oracle counts at expansion up to step 39, like the engine
+    assert int(c.rec_events) == osim.rec
+    assert time.time() - t0 < 600
+
+
 def test_delay_segment_table(cuda):
     """cc_build_dseg: dseg[r][d] = synapses of row r with delay <= d."""
     from paper_1803_08833_b200.network import build_b200
