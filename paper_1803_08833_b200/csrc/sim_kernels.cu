@@ -539,14 +539,22 @@ __device__ __forceinline__ int unit_delay(int k, int D) { return k < D - 1 ? k +
 // prefix over positions k < nk.
 __device__ __forceinline__ void unit_prefix(const cc_shard& sh, long long ta, int nk,
                                             unsigned* s_n, unsigned* s_pre) {
-    for (int k = threadIdx.x; k < nk; k += blockDim.x)
-        s_n[k] = (unsigned)min(sh.log_ctr[pos_mod(ta - unit_delay(k, sh.d_max), sh.log_slots)],
-                               (unsigned long long)sh.spk_cap);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned acc = 0;
-        for (int k = 0; k < nk; ++k) { s_pre[k] = acc; acc += (s_n[k] + DEL_SPU - 1) / DEL_SPU; }
-        s_pre[nk] = acc;
+    if (threadIdx.x < 32) {                  // warp 0: loads and a shuffle scan, 32 at a time
+        const int lane = threadIdx.x;
+        unsigned carry = 0;
+        for (int k0 = 0; k0 < nk; k0 += 32) {
+            const int k = k0 + lane;
+            unsigned n = 0;
+            if (k < nk)
+                n = (unsigned)min(sh.log_ctr[pos_mod(ta - unit_delay(k, sh.d_max), sh.log_slots)],
+                                  (unsigned long long)sh.spk_cap);
+            const unsigned units = (n + DEL_SPU - 1) / DEL_SPU;
+            unsigned tot;
+            const unsigned ex = warp_excl_scan(units, tot);
+            if (k < nk) { s_n[k] = n; s_pre[k] = carry + ex; }
+            carry += tot;
+        }
+        if (lane == 0) s_pre[nk] = carry;
     }
     __syncthreads();
 }
