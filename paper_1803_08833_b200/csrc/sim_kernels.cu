@@ -1357,10 +1357,13 @@ k_deliver(const cc_shard sh) {
 #pragma unroll
         for (int c = 0; c < CC_ITEM_CLASSES; ++c) ctl->cls_n[c] = 0u;
     }
+    // units [0, c) were delivered by k_stage(t - 1)'s idle warps (claimed in
+    // order); read by warp 1 while warp 0 builds the unit prefix
+    __shared__ unsigned s_c0;
+    if (threadIdx.x == 32) s_c0 = *(volatile unsigned*)&sh.tailc[0];
     unit_prefix(sh, t, D, s_n, s_pre);
     const unsigned n_units = s_pre[D];
-    // units [0, c) were delivered by k_stage(t - 1)'s idle warps (claimed in order)
-    const unsigned c0 = min(*(volatile unsigned*)&sh.tailc[0], s_pre[D - 1]);
+    const unsigned c0 = min(s_c0, s_pre[D - 1]);
     const ListSet S = list_set(sh, t);
     const int lane = threadIdx.x & 31;
     const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
