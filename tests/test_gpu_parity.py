@@ -542,3 +542,53 @@ def test_exchange_mode_single_rank_matches_reference(cuda):
         assert ds._graph is not None              # chunks ran as CUDA graphs (NCCL captured)
     finally:
         dist.destroy_process_group()
+
+
+def _random_config(seed):
+    """Small random networks over the parameter space the reference accepts:
+    grid, kernel, weights, delay law and d_max, time step, neuron constants,
+    drive (seeded; the oracle is the checker)."""
+    from paper_1803_08833_b200 import spec as S
+    r = np.random.default_rng(1000 + seed)
+    nx, ny = int(r.integers(1, 5)), int(r.integers(1, 5))
+    n_col = int(r.choice([20, 40, 64, 100]))
+    kernel = S.KernelSpec.gaussian() if r.random() < 0.5 else S.KernelSpec.exponential()
+    dt = float(r.choice([1.0, 0.5]))
+    d_max = int(r.choice([1, 3, 8, 20]))
+    if r.random() < 0.7:
+        dl = dict(delay_kind="uniform", delay_min_ms=dt, delay_max_ms=float(r.uniform(dt, d_max * dt)))
+    else:
+        dl = dict(delay_kind="exponential", delay_mean_ms=float(r.uniform(1.0, 4.0)))
+    je, ji = float(r.uniform(0.5, 2.0)), float(r.uniform(-6.0, -1.0))
+    gen = S.SynapseGenSpec(j_exc_exc=je, j_exc_inh=je, j_inh_exc=ji, j_inh_inh=ji,
+                           weight_sd_frac=float(r.uniform(0.1, 0.3)), timestep_ms=dt,
+                           d_max_steps=d_max, **dl)
+    if r.random() < 0.5:
+        nkw = dict(tau_m=float(r.choice([10.0, 20.0])), C_m=1.0, E=0.0,
+                   tau_c=float(r.choice([150.0, 300.0])), g_c=0.5, V_theta=20.0, V_r=15.0,
+                   tau_arp=float(r.choice([1.0, 2.0])), alpha_c=float(r.choice([0.01, 0.5])))
+    else:
+        nkw = dict(tau_arp=float(r.choice([1.0, 2.0])))
+    return S.SimConfig(
+        grid=S.GridSpec(nx=nx, ny=ny, neurons_per_column=n_col), kernel=kernel, genspec=gen,
+        exc_params=S.NeuronParams(is_excitatory=True, **nkw),
+        inh_params=S.NeuronParams(is_excitatory=False, **nkw),
+        external=S.ExternalInputSpec(synapses_per_neuron=80.0,
+                                     rate_per_synapse_hz=float(r.uniform(20.0, 60.0)),
+                                     weight_mv=float(r.uniform(0.5, 1.0))),
+        timestep_ms=dt, duration_s=0.06, seed=int(r.integers(1, 10 ** 6)))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_configs_match_oracle(cuda, seed):
+    from oracle import corticarc_oracle as O
+    from paper_1803_08833_b200.engine import run_b200
+    cfg = _random_config(seed)
+    res = run_b200(cfg, 1, chunk=16)
+    ref = O.run_oracle(cfg)
+    assert res.construction_checksum == ref.construction_checksum
+    assert res.n_spikes == ref.n_spikes
+    assert np.array_equal(res.raster_gids, ref.raster_gids)
+    assert np.array_equal(res.raster_times.view(np.uint64), ref.raster_times.view(np.uint64))
+    assert res.recurrent_events == ref.recurrent_events
+    assert res.external_events == ref.external_events
