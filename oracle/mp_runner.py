@@ -49,7 +49,7 @@ def shard_net(cfg, row_off, tgt_global, delay, weight, rank, size):
                       w.astype(np.float32), 0, 0)
 
 
-def _worker(rank, size, port, cfg, paths, steps, budget_s, q):
+def _worker(rank, size, port, cfg, paths, steps, budget_s, q, raster_path=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), OMP_NUM_THREADS="1")
     sys.path.insert(0, ROOT)
     import torch
@@ -73,13 +73,17 @@ def _worker(rank, size, port, cfg, paths, steps, budget_s, q):
         dist.barrier()
         t0 = time.perf_counter()
         done = 0
+        rg, rt = [], []
         for t in range(steps):
             li = torch.from_numpy(sim.prev_idx.astype(np.int64))
             g = torch.from_numpy(sim.gids[sim.prev_idx].astype(np.int64))
             tm = torch.from_numpy(sim.prev_t.astype(np.float64))
             in_g, in_t = x.exchange(li, g, tm)
             inc = [(in_g.numpy().astype(np.uint64), in_t.numpy())] if in_g.numel() else []
-            sim.step(t, inc)
+            g_out, t_out = sim.step(t, inc)
+            if raster_path is not None:
+                rg.append(np.asarray(g_out, np.uint64))
+                rt.append(np.asarray(t_out, np.float64))
             done += 1
             # all ranks agree on stopping (bounded sample)
             flag = torch.tensor([1 if time.perf_counter() - t0 > budget_s else 0])
@@ -87,15 +91,21 @@ def _worker(rank, size, port, cfg, paths, steps, budget_s, q):
             if flag.item():
                 break
         wall = time.perf_counter() - t0
+        if raster_path is not None:
+            np.save(f"{raster_path}_{rank}_g.npy",
+                    np.concatenate(rg) if rg else np.empty(0, np.uint64))
+            np.save(f"{raster_path}_{rank}_t.npy", np.concatenate(rt) if rt else np.empty(0))
         q.put((rank, done, wall, sim.rec, sim.ext, x.stats["seconds"]))
     finally:
         dist.destroy_process_group()
 
 
 def run_oracle_mp(cfg, row_off, tgt_global, delay, weight, workers: int, steps: int,
-                  budget_s: float):
+                  budget_s: float, collect_raster: bool = False):
     """Time the oracle loop on `workers` processes; returns a dict with
-    events/s, steps done, wall (max over ranks) and exchange seconds."""
+    events/s, steps done, wall (max over ranks) and exchange seconds (and with
+    collect_raster the merged raster sorted by (time, gid), and the recurrent /
+    external event counts)."""
     import multiprocessing as mp
     tmp = tempfile.mkdtemp(prefix="cc_oracle_")
     paths = []
@@ -106,13 +116,28 @@ def run_oracle_mp(cfg, row_off, tgt_global, delay, weight, workers: int, steps: 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, workers, port, cfg, paths, steps, budget_s, q))
+    rpath = os.path.join(tmp, "raster") if collect_raster else None
+    procs = [ctx.Process(target=_worker,
+                         args=(r, workers, port, cfg, paths, steps, budget_s, q, rpath))
              for r in range(workers)]
     for p in procs:
         p.start()
     res = [q.get(timeout=3600) for _ in range(workers)]
     for p in procs:
         p.join(timeout=120)
+    out = {}
+    if collect_raster:
+        gs, ts = [], []
+        for r in range(workers):
+            for kind, lst in (("g", gs), ("t", ts)):
+                f = f"{rpath}_{r}_{kind}.npy"
+                lst.append(np.load(f))
+                os.unlink(f)
+        g, t = np.concatenate(gs), np.concatenate(ts)
+        o = np.lexsort((g, t))
+        out = dict(raster_gids=g[o], raster_times=t[o],
+                   recurrent_events=int(sum(r[3] for r in res)),
+                   external_events=int(sum(r[4] for r in res)))
     for p in paths:
         os.unlink(p)
     os.rmdir(tmp)
@@ -120,4 +145,4 @@ def run_oracle_mp(cfg, row_off, tgt_global, delay, weight, workers: int, steps: 
     wall = max(r[2] for r in res)
     ev = sum(r[3] + r[4] for r in res)
     return dict(value=ev / wall if wall > 0 else 0.0, steps=steps_done, wall_s=wall,
-                events=int(ev), exchange_s=max(r[5] for r in res), workers=workers)
+                events=int(ev), exchange_s=max(r[5] for r in res), workers=workers, **out)

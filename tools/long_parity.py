@@ -1,0 +1,67 @@
+"""Full-length parity at a BASELINE config: the CUDA engine against the CPU
+oracle (numpy port of the reference loop, pinned to the reference's own
+fixtures) on the same connectivity, over the config's whole duration.
+
+    python tools/long_parity.py [CONFIG] [DURATION_S]
+
+Writes gpurun_out/long_parity_config<N>.json (committed under profiles/)."""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_1803_08833_b200.engine import run_b200  # noqa: E402
+from paper_1803_08833_b200.network import build_b200  # noqa: E402
+from paper_1803_08833_b200.presets import baseline_config  # noqa: E402
+from oracle.mp_runner import run_oracle_mp  # noqa: E402
+
+
+def main():
+    idx = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+    dur = float(sys.argv[2]) if len(sys.argv) > 2 else None
+    cfg = baseline_config(idx, "calibrated", duration_s=dur)
+    net = build_b200(cfg)
+    t0 = time.perf_counter()
+    res = run_b200(cfg, 1, net=net)
+    gpu_s = time.perf_counter() - t0
+    row_off, tgt, w, d = net.host_csr()
+    k = min(len(os.sched_getaffinity(0)), 16)
+    from paper_1803_08833_b200.partition import map_columns_to_workers
+    while k > 1:
+        try:
+            map_columns_to_workers(cfg.grid, k)
+            break
+        except ValueError:
+            k -= 1
+    t1 = time.perf_counter()
+    ref = run_oracle_mp(cfg, row_off, tgt.astype(np.int64), d, w, k, cfg.n_steps, 1e9,
+                        collect_raster=True)
+    cpu_s = time.perf_counter() - t1
+    same_g = bool(np.array_equal(res.raster_gids, ref["raster_gids"]))
+    same_t = bool(np.array_equal(res.raster_times.view(np.uint64),
+                                 ref["raster_times"].view(np.uint64)))
+    out = dict(config=idx, grid=f"{cfg.grid.nx}x{cfg.grid.ny}", steps=cfg.n_steps,
+               synapses=int(net.n_synapses), spikes_gpu=int(res.n_spikes),
+               spikes_oracle=int(len(ref["raster_gids"])), raster_gids_equal=same_g,
+               raster_times_bit_equal=same_t,
+               recurrent_events=[int(res.recurrent_events), ref["recurrent_events"]],
+               external_events=[int(res.external_events), ref["external_events"]],
+               raster_checksum=f"0x{res.raster_checksum:016x}", gpu_wall_s=gpu_s,
+               oracle_wall_s=cpu_s, oracle_processes=k,
+               mean_rate_hz=res.mean_rate_hz)
+    print(json.dumps(out))
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"long_parity_config{idx}.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+    ok = same_g and same_t and out["recurrent_events"][0] == out["recurrent_events"][1] \
+        and out["external_events"][0] == out["external_events"][1]
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
