@@ -38,10 +38,25 @@ def shard_net(cfg, row_off, tgt_global, delay, weight, rank, size):
     cols = pm.owned_columns(rank)
     col_rank = np.full(grid.n_columns, -1, np.int64)
     col_rank[cols] = np.arange(len(cols))
-    tcol = tgt_global // n
-    keep = col_rank[tcol] >= 0
-    src = np.repeat(np.arange(len(row_off) - 1, dtype=np.int64), np.diff(row_off))
-    src, tg, d, w = src[keep], tgt_global[keep], delay[keep], weight[keep]
+    # chunked over source rows (the global arrays are memory-mapped; the
+    # temporaries of one chunk stay small even for G-synapse stores)
+    parts = []
+    n_rows = len(row_off) - 1
+    r0 = 0
+    while r0 < n_rows:
+        r1 = min(n_rows, max(r0 + 1, int(np.searchsorted(row_off, row_off[r0] + 32_000_000))))
+        a, b = int(row_off[r0]), int(row_off[r1])
+        tg = np.asarray(tgt_global[a:b])
+        keep = col_rank[tg // n] >= 0
+        srcc = np.repeat(np.arange(r0, r1, dtype=np.int64), np.diff(row_off[r0:r1 + 1]))
+        parts.append((srcc[keep], tg[keep], np.asarray(delay[a:b])[keep],
+                      np.asarray(weight[a:b])[keep]))
+        r0 = r1
+    src = np.concatenate([q[0] for q in parts]) if parts else np.empty(0, np.int64)
+    tg = np.concatenate([q[1] for q in parts]) if parts else np.empty(0, np.int64)
+    d = np.concatenate([q[2] for q in parts]) if parts else np.empty(0, np.uint8)
+    w = np.concatenate([q[3] for q in parts]) if parts else np.empty(0, np.float32)
+    del parts
     sources, starts = np.unique(src, return_index=True)
     offsets = np.concatenate([starts, [len(src)]]).astype(np.int64)
     tl = (col_rank[tg // n] * n + tg % n).astype(np.uint32)
@@ -60,8 +75,7 @@ def _worker(rank, size, port, cfg, paths, steps, budget_s, q, raster_path=None):
     dist.init_process_group("gloo", rank=rank, world_size=size)
     try:
         row_off, tgt, dly, wgt = (np.load(p, mmap_mode="r") for p in paths)
-        net = shard_net(cfg, np.asarray(row_off), np.asarray(tgt), np.asarray(dly),
-                        np.asarray(wgt), rank, size)
+        net = shard_net(cfg, np.asarray(row_off), tgt, dly, wgt, rank, size)
         sim = O.ShardSim(cfg, net, rank, size)
         has = np.zeros(cfg.grid.n_neurons, np.uint8)
         has[net.sources.astype(np.int64)] = 1

@@ -30,6 +30,9 @@ def main():
     res = run_b200(cfg, 1, net=net)
     gpu_s = time.perf_counter() - t0
     row_off, tgt, w, d = net.host_csr()
+    del net
+    import torch
+    torch.cuda.empty_cache()
     k = min(len(os.sched_getaffinity(0)), 16)
     from paper_1803_08833_b200.partition import map_columns_to_workers
     while k > 1:
@@ -39,14 +42,14 @@ def main():
         except ValueError:
             k -= 1
     t1 = time.perf_counter()
-    ref = run_oracle_mp(cfg, row_off, tgt.astype(np.int64), d, w, k, cfg.n_steps, 1e9,
+    ref = run_oracle_mp(cfg, row_off, np.asarray(tgt, dtype=np.int32), d, w, k, cfg.n_steps, 1e9,
                         collect_raster=True)
     cpu_s = time.perf_counter() - t1
     same_g = bool(np.array_equal(res.raster_gids, ref["raster_gids"]))
     same_t = bool(np.array_equal(res.raster_times.view(np.uint64),
                                  ref["raster_times"].view(np.uint64)))
     out = dict(config=idx, grid=f"{cfg.grid.nx}x{cfg.grid.ny}", steps=cfg.n_steps,
-               synapses=int(net.n_synapses), spikes_gpu=int(res.n_spikes),
+               synapses=int(res.recurrent_synapses), spikes_gpu=int(res.n_spikes),
                spikes_oracle=int(len(ref["raster_gids"])), raster_gids_equal=same_g,
                raster_times_bit_equal=same_t,
                recurrent_events=[int(res.recurrent_events), ref["recurrent_events"]],
