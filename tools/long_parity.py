@@ -2,7 +2,10 @@
 oracle (numpy port of the reference loop, pinned to the reference's own
 fixtures) on the same connectivity, over the config's whole duration.
 
-    python tools/long_parity.py [CONFIG] [DURATION_S]
+    python tools/long_parity.py [CONFIG] [DURATION_S] [SHARDS]
+
+SHARDS > 1 runs the multi-shard path (distributed.run_local_shards: W column
+blocks with their own generator, spike exchange by device copies) on one GPU.
 
 Writes gpurun_out/long_parity_config<N>.json (committed under profiles/)."""
 import json
@@ -23,11 +26,16 @@ from oracle.mp_runner import run_oracle_mp  # noqa: E402
 
 def main():
     idx = int(sys.argv[1]) if len(sys.argv) > 1 else 1
-    dur = float(sys.argv[2]) if len(sys.argv) > 2 else None
+    dur = float(sys.argv[2]) if len(sys.argv) > 2 and float(sys.argv[2]) > 0 else None
+    shards = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     cfg = baseline_config(idx, "calibrated", duration_s=dur)
     net = build_b200(cfg)
     t0 = time.perf_counter()
-    res = run_b200(cfg, 1, net=net)
+    if shards > 1:
+        from paper_1803_08833_b200.distributed import run_local_shards
+        res = run_local_shards(cfg, shards)
+    else:
+        res = run_b200(cfg, 1, net=net)
     gpu_s = time.perf_counter() - t0
     row_off, tgt, w, d = net.host_csr()
     del net
@@ -48,7 +56,7 @@ def main():
     same_g = bool(np.array_equal(res.raster_gids, ref["raster_gids"]))
     same_t = bool(np.array_equal(res.raster_times.view(np.uint64),
                                  ref["raster_times"].view(np.uint64)))
-    out = dict(config=idx, grid=f"{cfg.grid.nx}x{cfg.grid.ny}", steps=cfg.n_steps,
+    out = dict(config=idx, grid=f"{cfg.grid.nx}x{cfg.grid.ny}", steps=cfg.n_steps, gpu_shards=shards,
                synapses=int(res.recurrent_synapses), spikes_gpu=int(res.n_spikes),
                spikes_oracle=int(len(ref["raster_gids"])), raster_gids_equal=same_g,
                raster_times_bit_equal=same_t,
@@ -59,7 +67,8 @@ def main():
                mean_rate_hz=res.mean_rate_hz)
     print(json.dumps(out))
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", f"long_parity_config{idx}.json"), "w") as fh:
+    name = f"long_parity_config{idx}" + (f"_{shards}shards" if shards > 1 else "")
+    with open(os.path.join(ROOT, "gpurun_out", name + ".json"), "w") as fh:
         json.dump(out, fh, indent=1)
     ok = same_g and same_t and out["recurrent_events"][0] == out["recurrent_events"][1] \
         and out["external_events"][0] == out["external_events"][1]
