@@ -411,13 +411,11 @@ static size_t gen_smem(const cc_gen* g) {
 }
 
 static int gen_prep(const cc_gen* g) {
-    static const void* prepared[2] = {nullptr, nullptr};
     const size_t sm = gen_smem(g);
     if (sm > 48 * 1024) {
         cudaFuncSetAttribute(k_gen<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         cudaFuncSetAttribute(k_gen<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     }
-    (void)prepared;
     return 0;
 }
 

@@ -49,28 +49,6 @@ struct Ev {                              // one input event, 16 B
     float w;                             // recurrent weight (f32 as stored)
 };
 
-__device__ __forceinline__ bool ev_less(const Ev& a, const Ev& b) {
-    // (t, src) is unique per target except for identical external events,
-    // whose weights are equal too, so this is the reference's total order
-    // lexsort((w, src, tm, tgt)) restricted to one target (engine.py:386).
-    return a.t < b.t || (a.t == b.t && a.src < b.src);
-}
-
-// Shell sort (Ciura gaps) degenerating to insertion sort for short inputs.
-__device__ __forceinline__ void sort_events(Ev* seg, uint32_t n) {
-    const uint32_t gaps[8] = {701u, 301u, 132u, 57u, 23u, 10u, 4u, 1u};
-    for (int gi = (n > 32 ? 0 : 7); gi < 8; ++gi) {
-        const uint32_t g = gaps[gi];
-        if (g >= n) continue;
-        for (uint32_t i = g; i < n; ++i) {
-            const Ev key = seg[i];
-            uint32_t j = i;
-            while (j >= g && ev_less(key, seg[j - g])) { seg[j] = seg[j - g]; j -= g; }
-            seg[j] = key;
-        }
-    }
-}
-
 __device__ __forceinline__ long long pos_mod(long long a, long long m) {
     long long r = a % m;
     return r < 0 ? r + m : r;
@@ -747,7 +725,6 @@ __device__ __forceinline__ void plan_group(const cc_shard& sh, long long t, int 
         mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
         es += __shfl_xor_sync(0xffffffffu, es, o);
     }
-    const int ok = 1;
     if (active) {
         sh.ev_n[li] = (int32_t)n;
         sh.ev_nr[li] = (int32_t)n_r;
@@ -774,12 +751,10 @@ __device__ __forceinline__ void plan_group(const cc_shard& sh, long long t, int 
     }
     const unsigned has = __ballot_sync(0xffffffffu, nn > 0);
     int ni = 0;
-    uint32_t my_item = 0, my_tot = 0;
+    uint32_t my_item = 0;
     for (int st = has ? __ffs(has) - 1 : 32; st < 32; ++ni) {
         const int en = __shfl_sync(0xffffffffu, lo, st);
-        const uint32_t tot = __shfl_sync(0xffffffffu, incl, en - 1)
-                             - __shfl_sync(0xffffffffu, excl, st);
-        if (lane == ni) { my_item = (uint32_t)st | ((uint32_t)en << 8); my_tot = tot; }
+        if (lane == ni) my_item = (uint32_t)st | ((uint32_t)en << 8);
         st = en;
     }
     const unsigned long long pt3 = gtimer();
@@ -945,7 +920,6 @@ k_stage(const cc_shard sh) {
         uint16_t* Epv = B.prov;
         uint8_t* Eo = B.own;
         uint8_t* Eq = B.owns;
-        unsigned long long spill_at = 0;
         if (rtot > (uint32_t)NEURON_WCAP) {
             // a single neuron larger than the shared buffer: stage in global scratch
             unsigned long long at = 0;
@@ -960,7 +934,6 @@ k_stage(const cc_shard sh) {
             ok = __shfl_sync(0xffffffffu, ok, 0);
             at = __shfl_sync(0xffffffffu, at, 0);
             if (!ok) continue;
-            spill_at = at;
             // spill layout: 3 words of 8 B per event (t, src|w, keep|perm|own)
             double* base = reinterpret_cast<double*>(sh.scratch) + at * 3;
             const uint32_t cap = rtot;
