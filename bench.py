@@ -108,6 +108,9 @@ def workload(args):
     cfg = baseline_config(args.config, "calibrated", kernel=args.kernel,
                           duration_s=(args.warmup + args.steps) / 1000.0, seed=args.seed,
                           drive_hz=args.drive)
+    if getattr(args, "grid", None):
+        nx, ny = (int(v) for v in args.grid.lower().split("x"))
+        cfg = replace(cfg, grid=replace(cfg.grid, nx=nx, ny=ny))
     n = n_ranks(args)
     if n > 1 and args.scaling == "weak":
         # per-GPU work fixed: the BASELINE grid once per GPU, tiled (the column
@@ -263,6 +266,8 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak = the config's grid once per GPU (default), "
                          "strong = the config's grid split over the GPUs")
+    ap.add_argument("--grid", default=None,
+                    help="override the config's grid, e.g. 48x24 (one GPU's block of config 4)")
     ap.add_argument("--exchange", action="store_true",
                     help="run the multi-GPU (exchange-mode) path even on one rank")
     args = ap.parse_args()
