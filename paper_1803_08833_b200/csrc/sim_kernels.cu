@@ -397,9 +397,10 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < CC_UPD_NBUF; ++j) issue();
+    // (each lane copies into and reads only its own slots, and cp.async waits
+    // are per thread: no warp barrier inside the loop)
     for (uint32_t b0 = 0; b0 < nmax; ++b0) {
         asm volatile("cp.async.wait_group %0;" ::"n"(CC_UPD_NBUF - 1) : "memory");
-        __syncwarp();
         const double2* my = sb + bi * BS;
         bi = bi + 1 == CC_UPD_NBUF ? 0 : bi + 1;
         const uint32_t e = min(n, b0 + 1u);
@@ -465,7 +466,6 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
             }
         }
 #if CC_UPD_PIPE
-        __syncwarp();                            // buffer consumed
         issue();
 #endif
     }
