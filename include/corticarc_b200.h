@@ -184,7 +184,8 @@ typedef struct cc_shard {
     cc_ctl* ctl;
     /* [128] counters, each on its own 128 B line (away from the work-item
      * claims in ctl): [0] next step's delay>=2 units claimed by k_stage's idle
-     * warps, [32] k_stage warps out of work items, [64] k_stage grid barrier */
+     * warps, [32] k_stage warps out of work items, [64] k_stage grid barrier,
+     * [96] k_stage work-item claims */
     uint32_t* tailc;
     /* [n_local] or NULL: with direct_log, neurons with a destination shard
      * other than this one also go to the exchange out-list (cc_pack_aer) */

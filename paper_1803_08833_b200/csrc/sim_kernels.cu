@@ -30,6 +30,9 @@
 #ifndef CC_STATIC_FIRST
 #define CC_STATIC_FIRST 1     // k_stage: each warp's first item by its index
 #endif
+#ifndef CC_CLAIM_OWN_LINE
+#define CC_CLAIM_OWN_LINE 1  // k_stage item claims on their own L2 line (tailc[96])
+#endif
 #ifndef CC_TAIL_STOP
 #define CC_TAIL_STOP 10
 #endif
@@ -882,7 +885,11 @@ k_stage(const cc_shard sh) {
             first = false;
         } else {
             if (lane == 0)
+#if CC_CLAIM_OWN_LINE
+                item = atomicAdd(&sh.tailc[96], 1u) + (CC_STATIC_FIRST ? n_stage_warps : 0u);
+#else
                 item = atomicAdd(&ctl->round_next, 1u) + (CC_STATIC_FIRST ? n_stage_warps : 0u);
+#endif
             item = __shfl_sync(0xffffffffu, item, 0);
         }
         if (item >= n_items) break;
@@ -1327,6 +1334,7 @@ k_deliver(const cc_shard sh) {
         ctl->stream_used = 0ull;
         ctl->n_rounds = 0u;
         ctl->round_next = 0u;
+        sh.tailc[96] = 0u;                     // k_stage's item claims (own L2 line)
 #pragma unroll
         for (int c = 0; c < CC_ITEM_CLASSES; ++c) ctl->cls_n[c] = 0u;
     }
