@@ -182,10 +182,10 @@ typedef struct cc_shard {
     double* probe_out;      /* [steps][n_probe][5] V c last refr V_end         */
     int64_t probe_steps;    /* rows in probe_out                               */
     cc_ctl* ctl;
-    /* [128] counters, each on its own 128 B line (away from the work-item
+    /* [256] counters, each on its own 128 B line (away from the work-item
      * claims in ctl): [0] next step's delay>=2 units claimed by k_stage's idle
      * warps, [32] k_stage warps out of work items, [64] k_stage grid barrier,
-     * [96] k_stage work-item claims */
+     * [96] k_stage work-item claims, [128] its ordered-input record cursor */
     uint32_t* tailc;
     /* [n_local] or NULL: with direct_log, neurons with a destination shard
      * other than this one also go to the exchange out-list (cc_pack_aer) */

@@ -1117,7 +1117,11 @@ k_stage(const cc_shard sh) {
         //      with t and w as one ordered record per input
         unsigned long long rbase = 0;
         if (lane == 0 && rtot) {
+#if CC_CLAIM_OWN_LINE
+            rbase = atomicAdd(&sh.tailc[128], rtot);     // own L2 line
+#else
             rbase = atomicAdd(&ctl->stream_used, (unsigned long long)rtot);
+#endif
             // evrec_cap covers a step's expected list capacity + overflow + drive
             if (rbase + rtot > (unsigned long long)sh.evrec_cap) cc_raise(ctl, CC_ERR_EVREC, t);
         }
@@ -1228,6 +1232,7 @@ k_stage(const cc_shard sh) {
         if (atomicAdd(&ctl->done_stage, 1u) == gridDim.x - 1) {
             ctl->done_stage = 0;
             sh.tailc[32] = 0u;
+            ctl->stream_used = sh.tailc[128];  // records used this step (diagnostics)
             sh.ovf_cnt[t & 1] = 0;             // step t's inputs fully consumed
             __threadfence();
             *(volatile long long*)&ctl->t = t + 1;
@@ -1332,6 +1337,7 @@ k_deliver(const cc_shard sh) {
         sh.log_len[pos_mod(t, L)] = 0ull;
         ctl->scratch_used = 0ull;
         ctl->stream_used = 0ull;
+        sh.tailc[128] = 0u;                    // k_stage's ordered-input record cursor
         ctl->n_rounds = 0u;
         ctl->round_next = 0u;
         sh.tailc[96] = 0u;                     // k_stage's item claims (own L2 line)

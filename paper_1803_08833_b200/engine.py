@@ -216,7 +216,7 @@ class Simulator:
                            device=dev),
 
             ctl=T.zeros(C.sizeof(_lib.Ctl) // 8, dtype=i64, device=dev),
-            tailc=T.zeros(128, dtype=i32, device=dev),
+            tailc=T.zeros(256, dtype=i32, device=dev),
         )
         self.probes = None if probes is None else np.asarray(probes, np.int64)
         n_probe = 0 if self.probes is None else len(self.probes)
