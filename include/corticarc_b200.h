@@ -108,6 +108,8 @@ typedef struct cc_shard {
     int32_t direct_log;     /* 1: neuron kernel logs its spikes itself (0: out-list only) */
     int32_t debug_skip;     /* timing experiments only: bit mask of k_neuron stages to skip */
     int32_t plan_in_stage;  /* set by cc_neuron_step: k_stage runs the planning itself */
+    int32_t del_lps_log2;   /* delivery: log2 lanes per spike (3: 4 spikes per warp unit, 4: 2) */
+    int32_t pad32_;
     uint64_t h2_ext;        /* splitmix chain prefix for EXTERNAL (rng.py:85-86)      */
     uint64_t h2_time;       /* ... for EXTERNAL_TIME                                  */
     uint64_t h2_init;       /* ... for INIT_STATE                                     */

@@ -69,6 +69,7 @@ class Shard(C.Structure):
         ("scratch_cap", C.c_int64), ("n_rows", C.c_int64),
         ("out_cap", C.c_int32), ("ext_budget", C.c_int32), ("n_probe", C.c_int32),
         ("direct_log", C.c_int32), ("debug_skip", C.c_int32), ("plan_in_stage", C.c_int32),
+        ("del_lps_log2", C.c_int32), ("pad32_", C.c_int32),
         ("h2_ext", C.c_uint64), ("h2_time", C.c_uint64), ("h2_init", C.c_uint64),
         ("dt", C.c_double), ("ext_weight", C.c_double), ("ext_thresh", C.c_double),
         ("pop", Pop * 2),

@@ -491,11 +491,9 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
 #ifndef CC_DEL_U
 #define CC_DEL_U 8          // synapses per lane per pass
 #endif
-#ifndef CC_DEL_SPU
-#define CC_DEL_SPU 4
-#endif
-constexpr int DEL_SPU = CC_DEL_SPU;         // spikes per unit
-constexpr int DEL_LPS = 32 / DEL_SPU;       // lanes per spike
+// Lanes per spike: 8 (4 spikes per unit) or 16 (2 per unit), chosen per shard
+// by the host (sh.del_lps_log2); the k_stage tail and k_deliver share it.
+__device__ __forceinline__ int del_lps(const cc_shard& sh) { return 1 << sh.del_lps_log2; }
 constexpr int DEL_DMAX = 256;               // d_max <= 255 (uint8 delays)
 
 // Input lists of arrival step t: two sets (t & 1), so that step t+1's
@@ -529,7 +527,7 @@ __device__ __forceinline__ void unit_prefix(const cc_shard& sh, long long ta, in
             if (k < nk)
                 n = (unsigned)min(sh.log_ctr[pos_mod(ta - unit_delay(k, sh.d_max), sh.log_slots)],
                                   (unsigned long long)sh.spk_cap);
-            const unsigned units = (n + DEL_SPU - 1) / DEL_SPU;
+            const unsigned units = (n + (32u >> sh.del_lps_log2) - 1) >> (5 - sh.del_lps_log2);
             unsigned tot;
             const unsigned ex = warp_excl_scan(units, tot);
             if (k < nk) { s_n[k] = n; s_pre[k] = carry + ex; }
@@ -547,7 +545,7 @@ __device__ __forceinline__ void unit_desc(const cc_shard& sh, long long ta, cons
                                           const unsigned* s_pre, unsigned u, int& kc,
                                           uint64_t& st, uint32_t& ln, uint32_t& rf) {
     while (s_pre[kc + 1] <= u) ++kc;
-    const unsigned idx = (u - s_pre[kc]) * DEL_SPU + ((threadIdx.x & 31) / DEL_LPS);
+    const unsigned idx = ((u - s_pre[kc]) << (5 - sh.del_lps_log2)) + ((threadIdx.x & 31) >> sh.del_lps_log2);
     st = 0; ln = 0; rf = 0;
     if (idx < s_n[kc]) {
         const int d = unit_delay(kc, sh.d_max);
@@ -569,10 +567,11 @@ __device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
 template <int U>
 __device__ __forceinline__ void load_pass(const cc_shard& sh, uint64_t st, uint32_t ln, int p,
                                           int* tg, float* w) {
-    const int sl = threadIdx.x % DEL_LPS;
+    const int lps = del_lps(sh);
+    const int sl = threadIdx.x & (lps - 1);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const uint32_t j = (uint32_t)(p * DEL_LPS * U + u * DEL_LPS + sl);
+        const uint32_t j = (uint32_t)((p * U + u) * lps + sl);
         tg[u] = -1;
         if (j < ln) {
             tg[u] = __ldg(sh.syn_tgt + st + j);
@@ -1204,9 +1203,9 @@ k_stage(const cc_shard sh) {
             uint64_t st;
             uint32_t ln, rf;
             unit_desc(sh, t + 1, a_n, a_pre, u, kc, st, ln, rf);
-            if (lane % DEL_LPS == 0) tail_ev += ln;      // one lane per spike
+            if ((lane & (del_lps(sh) - 1)) == 0) tail_ev += ln;      // one lane per spike
             const uint32_t lmax = warp_max_u32(ln);
-            for (int p = 0; (uint32_t)(p * DEL_LPS * UT) < lmax; ++p) {
+            for (int p = 0; (uint32_t)(p * del_lps(sh) * UT) < lmax; ++p) {
                 int tg[UT];
                 float w[UT];
                 load_pass<UT>(sh, st, ln, p, tg, w);
@@ -1357,7 +1356,7 @@ k_deliver(const cc_shard sh) {
     const unsigned nw = (gridDim.x * blockDim.x) >> 5;
     const unsigned long long dbg_t1 = gtimer();
     constexpr int U = CC_DEL_U;
-    constexpr int SPAN = DEL_LPS * U;                        // synapses per spike per pass
+    const int SPAN = del_lps(sh) * U;                        // synapses per spike per pass
     int kc = 0;
     unsigned u = c0 + wid;
     uint64_t st = 0, stn = 0;
@@ -1370,7 +1369,7 @@ k_deliver(const cc_shard sh) {
     int tg[U];
     float w[U];
     if (u < n_units) load_pass<U>(sh, st, ln, 0, tg, w);
-    const bool cnt_lane = lane % DEL_LPS == 0;               // one lane per spike counts
+    const bool cnt_lane = (lane & (del_lps(sh) - 1)) == 0;   // one lane per spike counts
     unsigned long long my_ev = (u < n_units && cnt_lane) ? ln : 0u;
     while (u < n_units) {
         // next pass of this unit, else the first pass of the warp's next unit

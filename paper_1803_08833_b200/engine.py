@@ -31,6 +31,8 @@ __all__ = ["RunResult", "Simulator", "run_b200", "raster_checksum", "estimate_wo
 
 MASK64 = (1 << 64) - 1
 DOMAIN = 0x636F727469636172
+# shards of at least this many neurons deliver with 16 lanes per spike (see Shard setup)
+DEL_WIDE_NEURONS = 2_000_000
 P_INIT_STATE, P_EXTERNAL, P_EXTERNAL_TIME = 4, 5, 7
 
 
@@ -233,6 +235,13 @@ class Simulator:
         sh.n_groups, sh.bin_pad = n_groups, bin_pad
         sh.debug_skip = int(os.environ.get("CC_DEBUG_SKIP", "0"))   # timing experiments only
         sh.spk_cap, sh.seg_stride = spk_cap, seg_stride
+        # delivery lanes per spike: 16 on shards of >= 2 M neurons (config 3 gaussian: k_deliver
+        # 448 -> 367 us, step -3.3 %), 8 below (configs 1, 2 and the config-4 GPU block: 16 lanes are ~1 % slower);
+        # CC_DEL_LPS overrides for experiments (profiles/r01l_delivery_sweep.md)
+        lps = int(os.environ.get("CC_DEL_LPS", "0")) or (16 if n_local >= DEL_WIDE_NEURONS else 8)
+        if lps not in (8, 16):
+            raise ValueError(f"CC_DEL_LPS must be 8 or 16, got {lps}")
+        sh.del_lps_log2 = lps.bit_length() - 1
         sh.ovf_cap, sh.raster_cap = ovf_cap, raster_cap
         sh.scratch_cap, sh.n_rows = scratch_cap, grid.n_neurons
         sh.evrec_cap = evrec_cap

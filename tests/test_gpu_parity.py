@@ -233,6 +233,21 @@ def test_tail_delivery_off_same_run(cuda, name, monkeypatch):
     assert np.array_equal(t.view(np.uint64), arr["raster_times"].view(np.uint64))
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["config0_cal", "tiny_gauss_long", "tiny_exp"])
+@pytest.mark.parametrize("lps", ["8", "16"])
+@pytest.mark.parametrize("tail", ["0", "4096"])
+def test_delivery_lanes_per_spike_same_run(cuda, name, lps, tail, monkeypatch):
+    """Delivery with 8 or 16 lanes per spike (the shard's del_lps_log2; 16 is
+    the default on shards of >= 2 M neurons), with and without the k_stage tail:
+    the same reference raster and event counts."""
+    from paper_1803_08833_b200.engine import run_b200
+    cfg, meta, arr = golden_run(name)
+    monkeypatch.setenv("CC_DEL_LPS", lps)
+    monkeypatch.setenv("CC_DEBUG_SKIP", tail)
+    _assert_same_run(run_b200(cfg, 1), meta, arr)
+
+
 @pytest.mark.parametrize("name", ["config0_cal", "tiny_exp"])
 def test_planning_inside_k_stage_same_run(cuda, name, monkeypatch):
     """The planning pass run by k_stage itself behind a grid barrier (chosen
