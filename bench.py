@@ -102,22 +102,33 @@ def weak_tiling(n: int):
     return n // b, b
 
 
-def workload(args):
-    from dataclasses import replace
-    from paper_1803_08833_b200.presets import baseline_config
-    cfg = baseline_config(args.config, "calibrated", kernel=args.kernel,
-                          duration_s=(args.warmup + args.steps) / 1000.0, seed=args.seed,
-                          drive_hz=args.drive)
+def resolve_defaults(args) -> None:
+    """N = 1: BASELINE config 1 (the single-B200 config); N > 1: BASELINE
+    config 2 split over the GPUs (the config BASELINE states at 1/2/4/8)."""
+    if args.config is None:
+        args.config = 1 if n_ranks(args) == 1 else 2
+
+
+def workload_grid(args, nx: int, ny: int):
     if getattr(args, "grid", None):
         nx, ny = (int(v) for v in args.grid.lower().split("x"))
-        cfg = replace(cfg, grid=replace(cfg.grid, nx=nx, ny=ny))
     n = n_ranks(args)
     if n > 1 and args.scaling == "weak":
         # per-GPU work fixed: the BASELINE grid once per GPU, tiled (the column
         # partition hands each rank one block of about the single-GPU size)
         a, b = weak_tiling(n)
-        cfg = replace(cfg, grid=replace(cfg.grid, nx=cfg.grid.nx * a, ny=cfg.grid.ny * b))
-    return cfg
+        nx, ny = nx * a, ny * b
+    return nx, ny
+
+
+def workload(args):
+    from dataclasses import replace
+    from paper_1803_08833_b200.presets import baseline_config
+    cfg = baseline_config(args.config, args.regime, kernel=args.kernel,
+                          duration_s=(args.warmup + args.steps) / 1000.0, seed=args.seed,
+                          drive_hz=args.drive)
+    nx, ny = workload_grid(args, cfg.grid.nx, cfg.grid.ny)
+    return replace(cfg, grid=replace(cfg.grid, nx=nx, ny=ny))
 
 
 def scaling_of(args) -> str:
@@ -161,48 +172,47 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
-def reference_workers(cfg) -> int:
-    """Largest k <= host threads that tiles the grid (engine.run_multiprocess)."""
-    from paper_1803_08833_b200.partition import map_columns_to_workers
-    for k in range(min(host_threads(), cfg.grid.n_columns), 0, -1):
-        try:
-            map_columns_to_workers(cfg.grid, k)
-            return k
-        except ValueError:
-            continue
-    return 1
-
-
 def run_reference_arm(args):
-    import torch
+    """The reference's CPU implementation of the path, timed on the host's
+    cores: the numpy oracle of the reference loop (a restatement pinned to the
+    reference's own outputs, tests/golden) on k processes with the
+    reference's counters-then-payloads exchange over gloo, on connectivity the
+    oracle generates on the same k processes.  This process imports nothing
+    from the product package (no CUDA library is loaded).  W + K steps from
+    t = 0 are run and the last K are timed, like the GPU arm."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_1803_08833_b200.network import build_b200
-    cfg = workload(args)
-    if not torch.cuda.is_available():
-        emit({"impl": "reference", "unavailable": "no CUDA device to build the "
-                                                  "shared connectivity"})
-        return
-    net = build_b200(cfg)
-    from oracle.mp_runner import run_oracle_mp
-    row_off, tgt_local, w, d = net.host_csr()
-    tgt_global = tgt_local.astype(np.int64)            # one shard: local index == gid
-    k = reference_workers(cfg)
-    budget = float(os.environ.get("CC_REF_BUDGET_S", "120"))
-    del net
-    torch.cuda.empty_cache()
-    r = run_oracle_mp(cfg, row_off, tgt_global, d, w, k, args.warmup + args.steps, budget)
-    ms = r["wall_s"] * 1000.0 / max(1, r["steps"])
+    from oracle.configs import baseline_config as oracle_config
+    from oracle.mp_runner import build_global_csr, run_oracle_mp, tiles
+    W, K = args.warmup, args.steps
+    probe = oracle_config(args.config, args.regime, kernel=args.kernel)
+    nx, ny = workload_grid(args, probe.grid.nx, probe.grid.ny)
+    cfg = oracle_config(args.config, args.regime, kernel=args.kernel,
+                        duration_s=(W + K) / 1000.0, seed=args.seed, drive_hz=args.drive,
+                        grid=f"{nx}x{ny}")
+    k = next(k for k in range(min(host_threads(), cfg.grid.n_columns), 0, -1)
+             if tiles(cfg.grid, k))
+    budget = float(os.environ.get("CC_REF_BUDGET_S", "150"))
+    row_off, tgt, dly, wgt, gen_s = build_global_csr(cfg, k)
+    r = run_oracle_mp(cfg, row_off, tgt, dly, wgt, k, W + K, budget, warmup=W)
+    steps_t = max(1, r["timed_steps"])
+    ms = r["timed_wall_s"] * 1000.0 / steps_t
     sample = (f"oracle/mp_runner.py: numpy oracle of the reference loop on {k} processes "
-              f"(gloo exchange), config {cfg.grid.nx}x{cfg.grid.ny}, steps 0..{r['steps'] - 1} "
-              f"from t=0, {r['events']} events in {r['wall_s']:.1f} s")
+              f"(gloo exchange, counters then payloads), config {cfg.grid.nx}x{cfg.grid.ny}, "
+              f"connectivity generated by the oracle on {k} processes ({len(wgt)} synapses, "
+              f"{gen_s:.0f} s); steps 0..{r['steps'] - 1} from t=0 run, the last {steps_t} "
+              f"timed ({r['timed_events']} events in {r['timed_wall_s']:.1f} s)"
+              + ("; stopped by the time budget" if r["steps"] < W + K else ""))
     line = {
         "metric": "synaptic events/s (recurrent + external)", "value": r["value"],
-        "unit": "events/s", "n_gpus": args.gpus, "steps": r["steps"], "warmup": 0,
+        "unit": "events/s", "n_gpus": args.gpus, "steps": steps_t, "warmup": W,
         "ms_per_step": ms, "higher_is_better": True, "scaling": scaling_of(args),
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, same connectivity)",
-        "config": config_block(cfg, None, args) | {"synapses": int(len(w))}, "impl": "reference",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based RNG; connectivity and drive bit-exact with "
+                "the reference streams)",
+        "config": config_block(cfg, None, args) | {"synapses": int(len(wgt))},
+        "impl": "reference",
         "cpu_baseline": {"value": r["value"], "unit": "events/s", "cores": k, "kind": "port",
                          "sample": sample},
         "e2e": {"value": r["value"], "unit": "events/s", "h2d_bytes_per_step": 0,
@@ -216,7 +226,8 @@ def run_reference_arm(args):
 def config_block(cfg, net, args):
     return {"workload": f"BASELINE config {args.config}: {cfg.grid.nx}x{cfg.grid.ny} columns x "
                         f"{cfg.grid.neurons_per_column} LIF+SFA neurons, {cfg.kernel.kind} "
-                        f"lateral decay, calibrated drive",
+                        f"lateral decay, {args.regime} operating point",
+            "regime": args.regime,
             "grid": f"{cfg.grid.nx}x{cfg.grid.ny}", "neurons": cfg.grid.n_neurons,
             "synapses": int(net.n_synapses) if net is not None else None,
             "kernel": cfg.kernel.kind, "drive_hz": cfg.external.rate_per_synapse_hz,
@@ -254,7 +265,11 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=None,
+                    help="BASELINE config (default: 1 on one GPU, 2 on N > 1 GPUs)")
+    ap.add_argument("--regime", default="calibrated", choices=["calibrated", "literal", "stress"])
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: spike exchange (peer stores, or the NCCL slots baseline)")
     ap.add_argument("--kernel", default=None)
     ap.add_argument("--drive", type=float, default=None)
     ap.add_argument("--seed", type=int, default=1)
@@ -263,15 +278,16 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--instrument-steps", type=int, default=200)
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N > 1: weak = the config's grid once per GPU (default), "
-                         "strong = the config's grid split over the GPUs")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N > 1: strong = the config's grid split over the GPUs (default), "
+                         "weak = the config's grid once per GPU")
     ap.add_argument("--grid", default=None,
                     help="override the config's grid, e.g. 48x24 (one GPU's block of config 4)")
     ap.add_argument("--exchange", action="store_true",
-                    help="run the multi-GPU (exchange-mode) path even on one rank")
+                    help="one GPU, own spikes routed through the peer exchange (loopback)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    resolve_defaults(args)
     if args.impl == "reference":
         return run_reference_arm(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -294,13 +310,20 @@ def bench_single(args):
     torch.cuda.set_device(dev)
     cfg = workload(args)
     net = build_b200(cfg)
-    K, W, CH = args.steps, args.warmup, min(args.chunk, args.steps)
+    K, W = args.steps, args.warmup
+    # timed: steps W .. W+K-1 (like the reference arm), as K / CH replays of a
+    # CH-step graph; CH divides K and fits in the warm-up, whose last CH steps
+    # are one untimed replay of that same graph (graph upload and first-launch
+    # costs stay outside the timed region)
+    CH = max(d for d in range(1, min(args.chunk, W, K) + 1) if K % d == 0)
     sim = Simulator(cfg, net, chunk=CH, raster_steps=K + CH, bin_cap=args.bin_cap)
-    sim.advance(W)                                         # warm-up (eager + graphs)
-    c0 = sim.check()
+    sim.advance(W - CH)                                    # warm-up (eager + graphs)
+    sim.check()
     g_main = sim.capture(CH)
-    rem = K % CH
-    g_rem = sim.capture(rem) if rem else None
+    g_main.replay()
+    torch.cuda.synchronize(dev)
+    sim.t += CH
+    c0 = sim.check(collect_raster=False)
     stream = torch.cuda.current_stream(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = Clocks(0)
@@ -309,8 +332,6 @@ def bench_single(args):
     ev0.record(stream)
     for _ in range(K // CH):
         g_main.replay()
-    if g_rem is not None:
-        g_rem.replay()
     ev1.record(stream)
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
@@ -427,7 +448,7 @@ def bench_single(args):
                          "spilled_neuron_steps": int(c1.spilled_total),
                          "bin_cap": sim.shard.bin_cap},
     }
-    del sim, g_main, g_rem
+    del sim, g_main
     torch.cuda.empty_cache()
     if not args.no_e2e:
         res = run_b200(cfg, 1, net=net)

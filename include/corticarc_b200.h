@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 23
+#define CC_ABI_VERSION 24
 
 /* Work items are queued in this many size classes, largest first. */
 /* Input lists per 32-neuron group (events of delay d go to sub-list
@@ -45,6 +45,8 @@ extern "C" {
 #define CC_ERR_GEN            0x80u  /* generator: row larger than planned          */
 #define CC_ERR_EVREC          0x100u /* ordered-input record buffer full (one step) */
 #define CC_ERR_GRIDSYNC       0x200u /* k_stage grid barrier timed out              */
+#define CC_ERR_XWAIT          0x400u /* peer exchange: a source's step flag did not arrive in time */
+#define CC_ERR_XCAP           0x800u /* peer exchange: destination region full     */
 
 /* Constants of one neuron population (model.py:44-86, NeuronBlock
  * per-neuron arrays model.py:243-267).  k1 = tau_c - tau_m and
@@ -84,7 +86,25 @@ typedef struct cc_ctl {
     unsigned int cls_n[CC_ITEM_CLASSES];  /* work items queued per size class  */
     unsigned long long del_events;        /* recurrent events deposited by cc_deliver */
     unsigned long long tail_events;       /* ... by cc_neuron_step's idle warps (next step) */
+    unsigned long long x_sent;            /* AER records pushed to peer shards */
+    unsigned long long x_recv;            /* AER records received (all sources) */
 } cc_ctl;
+
+/* Peer exchange over NVLink (one process per GPU of one node; DESIGN.md
+ * section 6).  Every rank owns one receive window (cudaMalloc'd by
+ * cc_xwin_alloc, mapped into the other ranks with CUDA IPC) holding, per step
+ * parity and per source rank, a region of AER records {gid, t lo, t hi, 0}
+ * (uint4) and one flag word ((step + 1) << 32 | record count).  An entry
+ * describes one such region: on the send side (xdst[d]) the region of THIS
+ * rank in rank d's window, as mapped here; on the receive side (xsrc[s]) the
+ * region of rank s in this rank's own window.  cap is the exact worst case:
+ * the neurons of the source that have >= 1 synapse on the destination. */
+typedef struct cc_xpeer {
+    uint64_t rec[2];        /* region base (uint4 records) per step parity; 0 = no link */
+    uint64_t flag[2];       /* flag word per step parity                         */
+    uint32_t cap;           /* records per region                               */
+    uint32_t pad;
+} cc_xpeer;
 
 /* One shard's device state.  Layout documented in DESIGN.md section 3. */
 typedef struct cc_shard {
@@ -192,6 +212,19 @@ typedef struct cc_shard {
     /* [n_local] or NULL: with direct_log, neurons with a destination shard
      * other than this one also go to the exchange out-list (cc_pack_aer) */
     const uint8_t* remote;
+
+    /* peer exchange (NULL xdst: none).  k_stage pushes every spike of a
+     * neuron with xmask bit d set into xdst[d]'s region (NVLink stores) and its
+     * last block publishes the per-destination counts in the flag words;
+     * cc_exchange_ingest waits for every linked source's flag of the step and
+     * logs the received spikes (deliver_spikes, network.py:325-379). */
+    int32_t n_ranks;        /* entries in xdst / xsrc (<= 32)                   */
+    int32_t rank;           /* this shard's rank                                */
+    const uint32_t* xmask;  /* [n_local] destination ranks of each neuron (bit d) */
+    const cc_xpeer* xdst;   /* [n_ranks] send side (device memory)              */
+    const cc_xpeer* xsrc;   /* [n_ranks] receive side (device memory)           */
+    uint32_t* xcnt;         /* [32] records pushed per destination this step (zero between steps) */
+    int64_t xwait_ns;       /* give up waiting for a source's flag after this long (CC_ERR_XWAIT) */
 } cc_shard;
 
 /* ---------------------------------------------------------------- misc */
@@ -200,6 +233,7 @@ const char* cc_last_error(void);
 /* sizeof(cc_shard) and sizeof(cc_ctl) as compiled, so hosts can verify layout. */
 int64_t cc_sizeof_shard(void);
 int64_t cc_sizeof_ctl(void);
+int64_t cc_sizeof_xpeer(void);
 
 /* CUDA-event timers usable inside captured CUDA graphs (records use
  * cudaEventRecordExternal): per-kernel durations of graph replays. */
@@ -257,6 +291,25 @@ int cc_pack_aer(const cc_shard* sh, const uint32_t* dest_mask_by_local, int32_t 
  * spikes of step ctl->t - 1 that have rows on this shard. */
 int cc_ingest_aer(const cc_shard* sh, const int64_t* recv, int32_t n_src, int32_t cap,
                   void* stream);
+
+/* Peer exchange, receive half (capturable; one launch per step after
+ * cc_neuron_step): wait until every linked source rank has published its
+ * flag for step ctl->t - 1 (acquire, system scope; CC_ERR_XWAIT after
+ * sh->xwait_ns), then log its records that have rows on this shard.  With
+ * every rank's step kernels finished before the launch (host-synchronised
+ * mode, ranks sharing one GPU) the wait returns at once.  Replaces the
+ * receive half of deliver_spikes (network.py:360-378) + rows_for
+ * (network.py:135-141); the send half is fused into cc_neuron_step. */
+int cc_exchange_ingest(const cc_shard* sh, void* stream);
+
+/* Receive windows for the peer exchange: cc_xwin_alloc cudaMallocs `bytes`
+ * (zeroed) on the current device and returns the pointer and its 64-byte CUDA
+ * IPC handle; cc_xwin_open maps another process's window (peer access enabled
+ * lazily); cc_xwin_close / cc_xwin_free release them. */
+int cc_xwin_alloc(int64_t bytes, void** ptr, uint8_t* handle64);
+int cc_xwin_open(const uint8_t* handle64, void** ptr);
+int cc_xwin_close(void* ptr);
+int cc_xwin_free(void* ptr);
 
 /* CC_SUBLISTS as compiled (hosts size bin_cnt / bin_rec / grp_sub with it). */
 int32_t cc_sublists(void);

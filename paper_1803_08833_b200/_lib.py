@@ -10,12 +10,12 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-__all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "check", "EngineError", "ERR_BITS",
+__all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "XPeer", "check", "EngineError", "ERR_BITS",
            "LIB_PATH"]
 
 LIB_PATH = os.environ.get("CC_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 23
+ABI_VERSION = 24
 ITEM_CLASSES = 8
 CNT_STRIDE_MAX = 64          # bin_cnt words per group allocated (CC_CNT_STRIDE <= this)
 
@@ -30,6 +30,8 @@ ERR_BITS = {
     0x80: "generator row larger than planned",
     0x100: "ordered-input record buffer full (inputs of one step)",
     0x200: "k_stage grid barrier timed out (blocks not co-resident)",
+    0x400: "peer exchange: a source rank's spikes of the step did not arrive in time",
+    0x800: "peer exchange: destination region full",
 }
 
 
@@ -54,7 +56,14 @@ class Ctl(C.Structure):
         ("stream_used", C.c_ulonglong), ("done_stage", C.c_uint), ("n_rounds", C.c_uint),
         ("round_next", C.c_uint), ("pad1", C.c_uint), ("cls_n", C.c_uint * 8),
         ("del_events", C.c_ulonglong), ("tail_events", C.c_ulonglong),
+        ("x_sent", C.c_ulonglong), ("x_recv", C.c_ulonglong),
     ]
+
+
+class XPeer(C.Structure):
+    """cc_xpeer: one source/destination region of the peer exchange."""
+    _fields_ = [("rec", C.c_uint64 * 2), ("flag", C.c_uint64 * 2), ("cap", C.c_uint32),
+                ("pad", C.c_uint32)]
 
 
 _P = C.c_void_p
@@ -86,6 +95,8 @@ class Shard(C.Structure):
         ("grp_done", _P), ("rounds", _P), ("round_cap", C.c_int64),
         ("probe_map", _P), ("probe_out", _P),
         ("probe_steps", C.c_int64), ("ctl", _P), ("tailc", _P), ("remote", _P),
+        ("n_ranks", C.c_int32), ("rank", C.c_int32), ("xmask", _P), ("xdst", _P), ("xsrc", _P),
+        ("xcnt", _P), ("xwait_ns", C.c_int64),
     ]
 
 
@@ -109,6 +120,7 @@ _SIGS = {
     "cc_sizeof_shard": (C.c_int64, []),
     "cc_sizeof_ctl": (C.c_int64, []),
     "cc_sizeof_gen": (C.c_int64, []),
+    "cc_sizeof_xpeer": (C.c_int64, []),
     "cc_timer_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
     "cc_timer_record": (C.c_int, [C.c_void_p, C.c_int32, _P]),
     "cc_timer_elapsed_ms": (C.c_float, [C.c_void_p, C.c_int32, C.c_int32]),
@@ -125,6 +137,11 @@ _SIGS = {
                               C.c_int64, _P, _P]),
     "cc_gen_warps": (C.c_int64, []),
     "cc_build_dseg": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]),
+    "cc_exchange_ingest": (C.c_int, [C.POINTER(Shard), _P]),
+    "cc_xwin_alloc": (C.c_int, [C.c_int64, C.POINTER(C.c_void_p), C.c_char_p]),
+    "cc_xwin_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "cc_xwin_close": (C.c_int, [_P]),
+    "cc_xwin_free": (C.c_int, [_P]),
     "cc_sublists": (C.c_int32, []),
     "cc_kernels_per_step": (C.c_int32, [C.c_int32]),
     "cc_csr_checksum": (C.c_int, [_P, _P, C.c_int64, _P, _P, _P, C.c_int32, C.c_int32, _P, _P]),
@@ -149,7 +166,8 @@ def load_library(path: str = LIB_PATH):
         fn.restype, fn.argtypes = res, args
     if L.cc_abi_version() != ABI_VERSION:
         raise ImportError(f"ABI mismatch: library {L.cc_abi_version()} != {ABI_VERSION}")
-    for name, st in (("cc_sizeof_shard", Shard), ("cc_sizeof_ctl", Ctl), ("cc_sizeof_gen", Gen)):
+    for name, st in (("cc_sizeof_shard", Shard), ("cc_sizeof_ctl", Ctl), ("cc_sizeof_gen", Gen),
+                     ("cc_sizeof_xpeer", XPeer)):
         if getattr(L, name)() != C.sizeof(st):
             raise ImportError(f"struct layout mismatch for {name}: "
                               f"{getattr(L, name)()} != {C.sizeof(st)}")

@@ -165,6 +165,73 @@ __device__ __forceinline__ void log_spike(const cc_shard& sh, long long t, uint3
     for (int j = 0; j < sh.seg_stride / 8; ++j) dst[j] = src[j];
 }
 
+// Warp-wide log_spike for received spikes (every lane calls; `valid` lanes
+// carry a spike): one reservation atomic per warp instead of one per spike.
+__device__ __forceinline__ void log_spike_warp(const cc_shard& sh, long long t, bool valid,
+                                               uint32_t gid, double te) {
+    const int lane = threadIdx.x & 31;
+    int64_t r0 = 0, len = 0;
+    if (valid) {
+        r0 = sh.row_off[gid];
+        len = sh.row_off[gid + 1] - r0;
+    }
+    const bool has = valid && len > 0;
+    const unsigned b = __ballot_sync(0xffffffffu, has);
+    if (!b) return;
+    unsigned long long lsum = has ? (unsigned long long)len : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    const int e = (int)pos_mod(t, sh.log_slots);
+    const int leader = __ffs(b) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) {
+        base = atomicAdd(&sh.log_ctr[e], (unsigned long long)__popc(b));
+        atomicAdd(&sh.log_len[e], lsum);
+    }
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (!has) return;
+    const unsigned long long idx = base + (unsigned long long)__popc(b & ((1u << lane) - 1u));
+    if (idx >= (unsigned long long)sh.spk_cap) {
+        cc_raise(sh.ctl, CC_ERR_SPIKE_LOG, t);
+        return;
+    }
+    const uint32_t ref = (uint32_t)(e * sh.spk_cap + idx);
+    sh.log_t[ref] = te;
+    sh.log_gid[ref] = gid;
+    sh.log_r0[ref] = r0;
+    const uint4* src = reinterpret_cast<const uint4*>(sh.dseg + (size_t)gid * sh.seg_stride);
+    uint4* dst = reinterpret_cast<uint4*>(sh.log_dseg + (size_t)ref * sh.seg_stride);
+    for (int j = 0; j < sh.seg_stride / 8; ++j) dst[j] = src[j];
+}
+
+// System-scope release / acquire of the peer exchange's flag words.
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Peer exchange, send half: push one spike into the region of every
+// destination rank in mask m (NVLink stores into the peer's window).
+__device__ __forceinline__ void x_push(const cc_shard& sh, long long t, uint32_t m, uint32_t gid,
+                                       double te) {
+    const unsigned long long tb = (unsigned long long)__double_as_longlong(te);
+    while (m) {
+        const int d = __ffs(m) - 1;
+        m &= m - 1;
+        const cc_xpeer& X = sh.xdst[d];
+        const unsigned o = atomicAdd(&sh.xcnt[d], 1u);
+        if (o < X.cap)
+            reinterpret_cast<uint4*>(X.rec[t & 1])[o] =
+                make_uint4(gid, (uint32_t)tb, (uint32_t)(tb >> 32), 0u);
+        else
+            cc_raise(sh.ctl, CC_ERR_XCAP, t);
+    }
+}
+
 __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, int t_mod_l) {
     const uint32_t ref = (uint32_t)rec >> 5;                 // low 5 bits: lane in group
     const int e = (int)(ref >> (31 - __clz(sh.spk_cap)));      // spk_cap is a power of two
@@ -454,7 +521,11 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
                 stale = true;
                 ++my_spikes;
                 if (sh.direct_log) log_spike(sh, t, gid, tj);
-                if (!sh.direct_log || (sh.remote && sh.remote[li])) {   // to other shards
+                if (sh.xdst) {                               // peer exchange: push now
+                    const uint32_t xm = sh.xmask[li];
+                    if (xm) x_push(sh, t, xm, gid, tj);
+                }
+                if ((!sh.direct_log && !sh.xdst) || (sh.remote && sh.remote[li])) {   // out-list
                     const unsigned o = atomicAdd(&ctl->out_n, 1u);
                     if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = tj; }
                     else cc_raise(ctl, CC_ERR_OUTLIST, t);
@@ -818,6 +889,29 @@ __global__ void __launch_bounds__(128)
 k_plan(const cc_shard sh) {
     const long long t = *(volatile long long*)&sh.ctl->t;
     plan_group(sh, t, (blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+}
+
+// Peer exchange: publish step t's per-destination record counts (last block
+// of k_stage; every other block's pushes are ordered before by its system
+// fence and the completion counter).  Every linked destination gets a flag
+// every step, also with no records, so that all ranks advance in lockstep
+// and a region is never rewritten before its receiver consumed it (the
+// regions alternate by step parity).  Runs also after a device error (with
+// the counts as they stand) so that peers never wait in vain.
+__device__ __noinline__ void x_publish(const cc_xpeer* xdst, uint32_t* xcnt, int n_ranks,
+                                      cc_ctl* ctl, long long t) {
+    __threadfence_system();
+    unsigned long long sent = 0;
+    for (int d = 0; d < n_ranks; ++d) {
+        const cc_xpeer& X = xdst[d];
+        if (!X.flag[0]) continue;
+        const uint32_t c = min(*(volatile uint32_t*)&xcnt[d], X.cap);
+        xcnt[d] = 0u;
+        sent += c;
+        st_release_sys(reinterpret_cast<unsigned long long*>(X.flag[t & 1]),
+                       ((unsigned long long)(t + 1) << 32) | c);
+    }
+    if (sent) ctl->x_sent += sent;
 }
 
 // Phase A proper: persistent warps claim work items from the queue.
@@ -1227,12 +1321,15 @@ k_stage(const cc_shard sh) {
     __syncthreads();
     if (threadIdx.x == 0) {
         if (blk_s) atomicAdd(&ctl->n_spikes, (unsigned long long)blk_s);
-        __threadfence();
+        // (peer exchange: the block's pushes to other GPUs are ordered before
+        // its completion, which the last block's release publishes)
+        if (sh.xdst) __threadfence_system(); else __threadfence();
         if (atomicAdd(&ctl->done_stage, 1u) == gridDim.x - 1) {
             ctl->done_stage = 0;
             sh.tailc[32] = 0u;
             ctl->stream_used = sh.tailc[128];  // records used this step (diagnostics)
             sh.ovf_cnt[t & 1] = 0;             // step t's inputs fully consumed
+            if (sh.xdst) x_publish(sh.xdst, sh.xcnt, sh.n_ranks, ctl, t);
             __threadfence();
             *(volatile long long*)&ctl->t = t + 1;
         }
@@ -1471,8 +1568,79 @@ __global__ void k_ingest(const cc_shard sh, const uint32_t* in_gid, const double
                          const int32_t* in_n) {
     const long long t = *(volatile long long*)&sh.ctl->t - 1;
     const int n = *in_n;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        log_spike(sh, t, in_gid[i], in_t[i]);
+    const int lane = threadIdx.x & 31;
+    const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int b = w0 * 32; b < n; b += nw * 32) {
+        const int i = b + lane;
+        const bool v = i < n;
+        log_spike_warp(sh, t, v, v ? in_gid[i] : 0u, v ? in_t[i] : 0.0);
+    }
+}
+
+// Peer exchange, receive half: wait for every linked source's flag of step
+// ctl->t - 1 (acquire, system scope), then log its records.
+__global__ void __launch_bounds__(256) k_xingest(const cc_shard sh) {
+    cc_ctl* ctl = sh.ctl;
+    const long long t = *(volatile long long*)&ctl->t - 1;
+    // a failed rank stops receiving (its k_stage keeps publishing, so that its
+    // peers never wait for it; the hosts agree on the failure per chunk)
+    if (*(volatile unsigned*)&ctl->error_bits) return;
+    __shared__ uint32_t s_pre[33];
+    __shared__ const uint4* s_rec[32];
+    if (threadIdx.x < 32) {
+        const int s = threadIdx.x;
+        uint32_t c = 0;
+        const uint4* rec = nullptr;
+        if (s < sh.n_ranks) {
+            const cc_xpeer& X = sh.xsrc[s];
+            if (X.flag[0]) {
+                const unsigned long long* f =
+                    reinterpret_cast<const unsigned long long*>(X.flag[t & 1]);
+                unsigned long long v = ld_acquire_sys(f);
+                if ((long long)(v >> 32) < t + 1) {
+                    const unsigned long long t0 = gtimer();
+                    for (;;) {
+                        __nanosleep(128);
+                        v = ld_acquire_sys(f);
+                        if ((long long)(v >> 32) >= t + 1) break;
+                        if ((long long)(gtimer() - t0) > sh.xwait_ns) {
+                            cc_raise(ctl, CC_ERR_XWAIT, t);
+                            v = 0ull;
+                            break;
+                        }
+                    }
+                }
+                c = min((uint32_t)v, X.cap);
+                rec = reinterpret_cast<const uint4*>(X.rec[t & 1]);
+            }
+        }
+        uint32_t tot;
+        const uint32_t ex = warp_excl_scan(c, tot);
+        s_pre[s] = ex;
+        s_rec[s] = rec;
+        if (s == 31) s_pre[32] = tot;
+        if (s == 0 && blockIdx.x == 0 && tot) ctl->x_recv += tot;
+    }
+    __syncthreads();
+    const uint32_t total = s_pre[32];
+    const int lane = threadIdx.x & 31;
+    const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    int s = 0;
+    for (uint32_t b = w0 * 32; b < total; b += nw * 32) {
+        const uint32_t i = b + lane;
+        const bool v = i < total;
+        uint32_t gid = 0;
+        double te = 0.0;
+        if (v) {
+            while (s_pre[s + 1] <= i) ++s;
+            const uint4 r = s_rec[s][i - s_pre[s]];
+            gid = r.x;
+            te = __longlong_as_double((long long)(((unsigned long long)r.z << 32) | r.y));
+        }
+        log_spike_warp(sh, t, v, gid, te);
+    }
 }
 
 // Multi-shard send (source_masks, network.py:229-230; the counters-then-payloads
@@ -1516,11 +1684,33 @@ __global__ void k_ingest_aer(const cc_shard sh, const long long* recv, int n_src
     const long long t = *(volatile long long*)&sh.ctl->t - 1;
     if (*(volatile unsigned*)&sh.ctl->error_bits) return;
     const size_t stride = 1 + 2 * (size_t)cap;
-    for (int src = 0; src < n_src; ++src) {
-        const long long* r = recv + src * stride;
-        const int n = (int)min(r[0], (long long)cap);
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-            log_spike(sh, t, (uint32_t)r[1 + 2 * i], __longlong_as_double(r[2 + 2 * i]));
+    __shared__ uint32_t s_pre[33];
+    if (threadIdx.x < 32) {
+        const int s = threadIdx.x;
+        const uint32_t c = s < n_src ? (uint32_t)min(recv[s * stride], (long long)cap) : 0u;
+        uint32_t tot;
+        const uint32_t ex = warp_excl_scan(c, tot);
+        s_pre[s] = ex;
+        if (s == 31) s_pre[32] = tot;
+    }
+    __syncthreads();
+    const uint32_t total = s_pre[32];
+    const int lane = threadIdx.x & 31;
+    const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    int s = 0;
+    for (uint32_t b = w0 * 32; b < total; b += nw * 32) {
+        const uint32_t i = b + lane;
+        const bool v = i < total;
+        uint32_t gid = 0;
+        double te = 0.0;
+        if (v) {
+            while (s_pre[s + 1] <= i) ++s;
+            const long long* r = recv + s * stride + 1 + 2 * (size_t)(i - s_pre[s]);
+            gid = (uint32_t)r[0];
+            te = __longlong_as_double(r[1]);
+        }
+        log_spike_warp(sh, t, v, gid, te);
     }
 }
 
@@ -1675,4 +1865,12 @@ extern "C" int cc_ingest_aer(const cc_shard* sh, const int64_t* recv, int32_t n_
     k_ingest_aer<<<sm_count(), 256, 0, (cudaStream_t)stream>>>(
         *sh, reinterpret_cast<const long long*>(recv), n_src, cap);
     return cc_check_launch("k_ingest_aer");
+}
+
+extern "C" int cc_exchange_ingest(const cc_shard* sh, void* stream) {
+    if (!sh) return cc_set_error("cc_exchange_ingest: null shard");
+    if (!sh->xsrc || !sh->xdst) return cc_set_error("cc_exchange_ingest: no peer exchange set up");
+    if (sh->n_ranks < 1 || sh->n_ranks > 32) return cc_set_error("cc_exchange_ingest: 1..32 ranks");
+    k_xingest<<<sm_count(), 256, 0, (cudaStream_t)stream>>>(*sh);
+    return cc_check_launch("k_xingest");
 }

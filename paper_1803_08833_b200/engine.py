@@ -175,7 +175,8 @@ class Simulator:
         seg_stride = (D + 1 + 7) // 8 * 8
         dseg = net.delay_segments(D, seg_stride)
         raster_cap = max(1024, n_local * bound * max(self.chunk, raster_steps or 0))
-        scratch_cap = max(1 << 16, n_local * 64)     # spill staging: onset bursts
+        # spill staging for onset bursts (neuron-steps with > NEURON_WCAP inputs)
+        scratch_cap = max(1 << 16, n_local * int(os.environ.get("CC_SCRATCH_PER_NEURON", "64")))
         # ordered-input records of one step: the expected list capacity of a step,
         # the overflow list and every neuron's Poisson budget (beyond it the
         # step fails with "event staging scratch exhausted")
@@ -504,8 +505,16 @@ def run_b200(config, workers: int = 1, *, net: Optional[DeviceNetwork] = None, p
     one process per GPU (see paper_1803_08833_b200.distributed)."""
     import torch
     if workers != 1:
-        from .distributed import run_multi_gpu
-        return run_multi_gpu(config, workers)
+        from .distributed import run_multi_gpu, run_spawned
+        est = estimate_worker_bytes(config, workers)
+        if est > config.memory_budget_bytes:
+            raise MemoryBudgetError(
+                f"estimated {est / 1e9:.2f} GB per worker exceeds the "
+                f"{config.memory_budget_bytes / 1e9:.2f} GB budget")
+        transport = os.environ.get("CC_TRANSPORT", "p2p")
+        if int(os.environ.get("WORLD_SIZE", "1")) == workers:      # under torchrun
+            return run_multi_gpu(config, workers, transport=transport)
+        return run_spawned(config, workers, transport=transport, chunk=chunk)
     est = estimate_worker_bytes(config, workers)
     if est > config.memory_budget_bytes:
         raise MemoryBudgetError(

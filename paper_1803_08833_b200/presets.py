@@ -1,6 +1,6 @@
 """BASELINE.json configs 0-4 expressed as SimConfig.
 
-Two regimes per config:
+Three regimes per config:
 
 * ``literal``    - the BASELINE numbers as far as the reference can express
                    them (clipped borders, one delay law for all sources).  The
@@ -9,6 +9,8 @@ Two regimes per config:
 * ``calibrated`` - the operating point used for performance: J_inh = -2.0 mV
                    and an external drive pinned with the calibration sweep so
                    the Gaussian grids fire at ~7.5 Hz.
+* ``stress``     - the exponential grids at ~33 Hz mean rate (see STRESS below):
+                   the paper's event volume, for the delivery path.
 
 Not expressible in the reference and therefore not used: periodic borders
 (connectivity.py:11-13), 1 ms inhibitory delays (connectivity.py:410-416).
@@ -22,7 +24,7 @@ from dataclasses import replace
 from .spec import (ExternalInputSpec, GridSpec, KernelSpec, NeuronParams,
                    SimConfig, SynapseGenSpec)
 
-__all__ = ["baseline_config", "GAUSS_3SIGMA", "EXP_BASELINE", "CALIBRATED_DRIVE_HZ"]
+__all__ = ["baseline_config", "GAUSS_3SIGMA", "EXP_BASELINE", "CALIBRATED_DRIVE_HZ", "STRESS"]
 
 # Gaussian sigma=100 um truncated at 3 sigma: p(300 um) = 5.5545e-4 must stay
 # inside the stencil, hence a cutoff just below it (28 offsets).
@@ -54,20 +56,35 @@ _DURATION = {0: 1.0, 1: 1.0, 2: 2.0, 3: 1.0, 4: 1.0}
 CALIBRATED_DRIVE_HZ = {"gaussian": 40.0, "exponential": 55.0}
 CALIBRATED_J_INH = {"gaussian": (-2.0, -2.0), "exponential": (-8.0, -1.0)}   # (->exc, ->inh)
 
+# ``stress``: the exponential grids at the paper's event volume (PAPER.md:530-532
+# quotes 32-38 Hz).  The BASELINE neuron/weight model has no asynchronous state
+# there with equal inhibitory weights (every J_inh->exc = J_inh->inh in -2..-8
+# runs away at drive >= 50 Hz: tools/sweep_rates.py, profiles/operating_points_r02.md);
+# with strong inhibition onto excitatory cells and weak inhibition between
+# inhibitory cells it settles at ~33 Hz mean (excitatory ~7 Hz, inhibitory
+# ~185 Hz) with a flat population rate (CV of the per-step spike count 0.16):
+# 400 Hz drive per external synapse, J_inh->exc = -12 mV, J_inh->inh = -0.5 mV.
+# A labelled stress point for the delivery path, not a biological calibration.
+STRESS = {"gaussian": (40.0, -2.0, -2.0), "exponential": (400.0, -12.0, -0.5)}
+
 
 def baseline_config(index: int, regime: str = "calibrated", kernel: str | None = None,
                     duration_s: float | None = None, seed: int = 1,
                     drive_hz: float | None = None) -> SimConfig:
     if index not in _GRIDS:
         raise ValueError(f"no BASELINE config {index}")
-    if regime not in ("literal", "calibrated"):
+    if regime not in ("literal", "calibrated", "stress"):
         raise ValueError(f"unknown regime {regime!r}")
     if kernel is None:
         kernel = "gaussian" if index in (0, 1, 3) else "exponential"
     kspec = GAUSS_3SIGMA if kernel == "gaussian" else EXP_BASELINE
     nx, ny = _GRIDS[index]
-    j_ie, j_ii = (-1.2, -1.2) if regime == "literal" else CALIBRATED_J_INH[kernel]
-    rate = 3.0 if regime == "literal" else CALIBRATED_DRIVE_HZ[kernel]
+    if regime == "literal":
+        rate, j_ie, j_ii = 3.0, -1.2, -1.2
+    elif regime == "stress":
+        rate, j_ie, j_ii = STRESS[kernel]
+    else:
+        rate, (j_ie, j_ii) = CALIBRATED_DRIVE_HZ[kernel], CALIBRATED_J_INH[kernel]
     if drive_hz is not None:
         rate = drive_hz
     neuron = dict(tau_m=20.0, C_m=1.0, E=0.0, tau_c=300.0, g_c=0.5,

@@ -16,10 +16,12 @@ import bench  # noqa: E402
 
 
 def _args(**kw):
-    a = dict(gpus=1, steps=10, warmup=3, config=1, kernel=None, drive=None, seed=1,
-             grid=None, scaling="weak")
+    a = dict(gpus=1, steps=10, warmup=3, config=None, kernel=None, drive=None, seed=1,
+             grid=None, scaling="strong", regime="calibrated")
     a.update(kw)
-    return argparse.Namespace(**a)
+    ns = argparse.Namespace(**a)
+    bench.resolve_defaults(ns)
+    return ns
 
 
 def test_weak_tiling_series():
@@ -29,32 +31,63 @@ def test_weak_tiling_series():
         assert a * b == n and a >= b
 
 
-def test_workload_weak_and_strong(monkeypatch):
+def test_workload_defaults_and_scaling(monkeypatch):
     monkeypatch.delenv("WORLD_SIZE", raising=False)
     one = bench.workload(_args())
-    assert (one.grid.nx, one.grid.ny) == (8, 8)
+    assert (one.grid.nx, one.grid.ny) == (8, 8)          # N = 1: BASELINE config 1
     assert one.grid.n_neurons == 79360
     assert bench.scaling_of(_args()) == "strong"        # one GPU: nothing to scale
     eight = bench.workload(_args(gpus=8))
-    assert (eight.grid.nx, eight.grid.ny) == (32, 16)   # config-1 grid once per GPU
-    assert bench.scaling_of(_args(gpus=8)) == "weak"
-    strong = bench.workload(_args(gpus=8, scaling="strong"))
-    assert (strong.grid.nx, strong.grid.ny) == (8, 8)
+    assert (eight.grid.nx, eight.grid.ny) == (24, 24)   # N > 1: config 2 split over the GPUs
+    assert eight.kernel.kind == "exponential"
+    assert bench.scaling_of(_args(gpus=8)) == "strong"
+    weak = bench.workload(_args(gpus=8, config=1, scaling="weak"))
+    assert (weak.grid.nx, weak.grid.ny) == (32, 16)     # config-1 grid once per GPU
+    assert bench.scaling_of(_args(gpus=8, scaling="weak")) == "weak"
     monkeypatch.setenv("WORLD_SIZE", "4")
-    assert (bench.workload(_args()).grid.nx, bench.workload(_args()).grid.ny) == (16, 16)
-    grid = bench.workload(_args(config=4, grid="48x24"))
-    assert (grid.grid.nx, grid.grid.ny) == (96, 48)     # --grid is one GPU's block
+    assert bench.workload(_args()).grid.nx == 24
+    grid = bench.workload(_args(config=4, grid="48x24", scaling="weak"))
+    assert (grid.grid.nx, grid.grid.ny) == (96, 48)     # weak: --grid is one GPU's block
     monkeypatch.delenv("WORLD_SIZE")
     grid = bench.workload(_args(config=4, grid="48x24"))
     assert (grid.grid.nx, grid.grid.ny) == (48, 24)
+    stress = bench.workload(_args(config=2, regime="stress"))
+    assert stress.external.rate_per_synapse_hz == 400.0 and stress.genspec.j_inh_inh == -0.5
 
 
-def test_reference_workers_tile_the_grid():
+def test_reference_arm_config_is_the_gpu_arm_config(monkeypatch):
+    """The CPU reference arm builds its run description without the product
+    package (oracle/configs.py); it must describe the same workload."""
+    from oracle.configs import baseline_config as oc
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    for idx, regime in ((1, "calibrated"), (2, "calibrated"), (2, "stress"), (0, "literal")):
+        a = _args(config=idx, regime=regime)
+        g = bench.workload(a)
+        o = oc(idx, regime, duration_s=(a.warmup + a.steps) / 1000.0)
+        assert (o.grid.nx, o.grid.ny, o.grid.n_neurons) == (g.grid.nx, g.grid.ny, g.grid.n_neurons)
+        for k in ("kind", "amplitude_A", "scale", "cutoff_p", "local_p"):
+            assert getattr(o.kernel, k) == getattr(g.kernel, k), k
+        for k in ("j_exc_exc", "j_exc_inh", "j_inh_exc", "j_inh_inh", "weight_sd_frac",
+                  "delay_kind", "delay_min_ms", "delay_max_ms", "timestep_ms", "d_max_steps"):
+            assert getattr(o.genspec, k) == getattr(g.genspec, k), k
+        for k in ("tau_m", "C_m", "E", "tau_c", "g_c", "V_theta", "V_r", "tau_arp", "alpha_c"):
+            assert getattr(o.exc_params, k) == getattr(g.exc_params, k), k
+            assert getattr(o.inh_params, k) == getattr(g.inh_params, k), k
+        assert vars(o.external) == {k: getattr(g.external, k) for k in vars(o.external)}
+        assert (o.timestep_ms, o.seed, o.n_steps) == (g.timestep_ms, g.seed, g.n_steps)
+
+
+def test_reference_arm_tiling():
+    from oracle.mp_runner import tiles
     from paper_1803_08833_b200.partition import map_columns_to_workers
     cfg = bench.workload(_args())
-    k = bench.reference_workers(cfg)
-    assert 1 <= k <= min(bench.host_threads(), cfg.grid.n_columns)
-    map_columns_to_workers(cfg.grid, k)                 # raises if k does not tile
+    for k in range(1, 33):
+        try:
+            map_columns_to_workers(cfg.grid, k)
+            ok = True
+        except ValueError:
+            ok = False
+        assert tiles(cfg.grid, k) == ok, k
 
 
 def _run_bench(*argv, timeout=600, env=None):
@@ -67,10 +100,24 @@ def _run_bench(*argv, timeout=600, env=None):
     return json.loads(lines[0])
 
 
-@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="CPU-only fallback line")
-def test_reference_arm_without_gpu_prints_unavailable():
-    line = _run_bench("--impl", "reference", "--steps", "1", "--warmup", "3")
-    assert line["impl"] == "reference" and "unavailable" in line
+def test_reference_arm_runs_without_the_product_package():
+    """--impl reference on a tiny workload: one JSON line from the CPU oracle
+    (W + K steps, last K timed), and the product package never imported."""
+    code = ("import sys, runpy; sys.argv = ['bench.py', '--impl', 'reference', '--config', '0', "
+            "'--steps', '4', '--warmup', '3', '--grid', '2x1']; "
+            "import bench; bench.main(); "
+            "bad = [m for m in sys.modules if m.startswith('paper_1803_08833_b200')]; "
+            "assert not bad, bad")
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       timeout=600, cwd=ROOT, env=dict(os.environ, CC_REF_BUDGET_S="120"))
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, p.stdout
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["steps"] == 4 and line["warmup"] == 3
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
 
 
 @pytest.mark.gpu
@@ -97,3 +144,5 @@ def test_bench_line_contract():
     assert c["kind"] == "port" and c["cores"] == 1 and c["value"] > 0
     assert line["gpu_launches"] >= 3 * 20               # k_deliver, k_plan, k_stage per step
     assert line["clocks"]["sm_mhz"] > 0
+    # the device-timed value replays warm graphs: not below the end-to-end rate
+    assert line["value"] >= 0.9 * e["value"]

@@ -535,19 +535,21 @@ def test_partition_invariance_flat_ingest(cuda):
 
 
 def test_exchange_mode_single_rank_matches_reference(cuda):
-    """The multi-GPU code path (spike out-list -> cc_pack_aer -> NCCL
-    all-to-all in CUDA graphs -> cc_ingest_aer) on a one-rank NCCL group
-    reproduces the reference raster."""
+    """The NCCL slots transport (spike out-list -> cc_pack_aer -> NCCL
+    all-to-all captured in CUDA graphs -> cc_ingest_aer) on a one-rank NCCL
+    group, every spike routed through the exchange (loopback), reproduces the
+    reference raster."""
     import os
-    import torch
     import torch.distributed as dist
     from paper_1803_08833_b200.distributed import DistributedSimulator
     cfg, meta, arr = golden_run("tiny_gauss")
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29517")
-    dist.init_process_group("nccl", rank=0, world_size=1)
+    dist.init_process_group("gloo", rank=0, world_size=1)
     try:
-        ds = DistributedSimulator(cfg, 0, 1, chunk=25, force_exchange=True)
+        ng = dist.new_group(backend="nccl")
+        ds = DistributedSimulator(cfg, 0, 1, chunk=25, transport="nccl", nccl_group=ng,
+                                  loopback=True)
         ds.advance(cfg.n_steps)
         g, t = ds.sim.raster()
         c = ds.sim.ctl()

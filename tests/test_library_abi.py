@@ -35,6 +35,7 @@ def test_abi_and_layout():
     assert L.cc_sizeof_shard() == C.sizeof(_lib.Shard)
     assert L.cc_sizeof_ctl() == C.sizeof(_lib.Ctl)
     assert L.cc_sizeof_gen() == C.sizeof(_lib.Gen)
+    assert L.cc_sizeof_xpeer() == C.sizeof(_lib.XPeer) == 40
 
 
 def test_product_path_refuses_cpu():
