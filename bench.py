@@ -3,24 +3,33 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 A "step" is one simulated 1 ms step of the whole network (k_deliver + k_neuron
-for every shard).  Workload (N=1): BASELINE config 1 - 8x8 grid of
+for every shard).  Workload: N = 1, BASELINE config 1 - 8x8 grid of
 1240-neuron columns (79,360 LIF+SFA neurons, ~95 M synapses), Gaussian
-lateral decay, calibrated operating point (presets.py).  Connectivity and
+lateral decay, calibrated operating point (presets.py); N > 1 (torchrun),
+BASELINE config 2 (24x24 exponential, 1.39 G synapses) split over the GPUs
+(strong scaling; --scaling weak tiles config 1 once per GPU).  Connectivity and
 drive are generated on the device from the seed (bit-exact with the
 reference's streams); timing excludes construction like the reference's
 normalized cost (metrics.py:114-123).
 
-value      = (recurrent + external events in K timed steps) / device time of
-             the K steps (CUDA events around CUDA-graph replays, one sync).
-e2e        = same metric through the public API run_b200(config) wall clock
-             (host loop, per-chunk counter checks and raster device->host copies).
+value      = (recurrent + external events in steps W .. W+K-1) / device time of
+             those K steps (CUDA events around warm CUDA-graph replays, one sync).
+e2e        = same metric, same steps, through the public step API: wall clock of
+             Simulator.advance(K) after advance(W) (the loop run_b200 runs:
+             pipelined chunk graphs, per-chunk counter / error checks, raster
+             device->host copies).  Recurrent events count at expansion
+             (engine.py:366), so a window that includes the onset's first steps
+             counts the burst's whole fan-out early; both numbers exclude them.
 roofline   = k_deliver against measured HBM bandwidth, 17 B per recurrent
              event; per-kernel times from event-record nodes
              in instrumented graph replays of the same workload: one as timed
              (kernel shares), one with k_stage's tail delivery switched off so
              that k_deliver deposits every arrival (the roofline line).
-cpu_baseline / --impl reference = the CPU oracle (numpy port of the
-             reference loop) on the same connectivity, 1 core, bounded sample.
+cpu_baseline = the CPU oracle (numpy port of the reference loop) on the same
+             connectivity, 1 core, bounded sample.
+--impl reference = the oracle on all host cores (oracle/mp_runner.py), steps
+             W .. W+K-1 of a run from t = 0 timed; imports nothing from the
+             product package.
 """
 
 from __future__ import annotations
@@ -303,7 +312,7 @@ def main():
 def bench_single(args):
     import torch
     from paper_1803_08833_b200 import _lib
-    from paper_1803_08833_b200.engine import Simulator, run_b200
+    from paper_1803_08833_b200.engine import Simulator
     from paper_1803_08833_b200.network import build_b200
     L = _lib.lib()
     dev = torch.device("cuda:0")
@@ -320,15 +329,16 @@ def bench_single(args):
     sim.advance(W - CH)                                    # warm-up (eager + graphs)
     sim.check()
     g_main = sim.capture(CH)
+    # the clock sampler starts (and settles) before the warm replay, so that
+    # nothing but graph replays sits between the warm-up and the timed region
+    clocks = Clocks(0)
+    time.sleep(0.3)
     g_main.replay()
     torch.cuda.synchronize(dev)
     sim.t += CH
     c0 = sim.check(collect_raster=False)
     stream = torch.cuda.current_stream(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = Clocks(0)
-    time.sleep(0.3)
-    torch.cuda.synchronize(dev)
     ev0.record(stream)
     for _ in range(K // CH):
         g_main.replay()
@@ -346,16 +356,16 @@ def bench_single(args):
     # instrumented replays: per-kernel durations from event-record nodes.
     # (a) as timed (k_stage's idle warps deliver most of the next step's
     #     delay>=2 events): kernel shares;
-    # (b) with that tail delivery switched off (debug_skip 4096), so k_deliver
+    # (b) with that tail delivery switched off (flags 4096), so k_deliver
     #     deposits every arrival: the delivery kernel's roofline.
     NI = min(args.instrument_steps, 1000)
 
     def instrumented(debug: int):
         timer = C.c_void_p()
         _lib.check(L.cc_timer_create(3 * NI, C.byref(timer)))
-        sim.shard.debug_skip = debug
+        sim.shard.flags = debug
         g_t = sim.capture(NI, timer=timer)
-        sim.shard.debug_skip = 0
+        sim.shard.flags = 0
         ca = sim.check(collect_raster=False)
         g_t.replay()
         torch.cuda.synchronize(dev)
@@ -451,14 +461,29 @@ def bench_single(args):
     del sim, g_main
     torch.cuda.empty_cache()
     if not args.no_e2e:
-        res = run_b200(cfg, 1, net=net)
-        ev = res.recurrent_events + res.external_events
-        line["e2e"] = {"value": ev / res.sim_seconds_wall, "unit": "events/s",
+        # end to end through the public step API over the same steps as value:
+        # a fresh Simulator (run_b200's), W untimed steps, then the wall clock of
+        # advance(K) - pipelined chunk graphs, per-chunk counter checks, error
+        # checks and the raster's device->host copies (the expansion-time event
+        # count of the onset's first steps stays out of both numbers)
+        sim2 = Simulator(cfg, net, chunk=min(args.chunk, K), raster_steps=K)
+        sim2.advance(W)
+        ca = sim2.check()
+        torch.cuda.synchronize(dev)
+        w0 = time.perf_counter()
+        sim2.advance(K)
+        wall = time.perf_counter() - w0
+        cb = sim2.ctl()
+        ev = (cb.rec_events + cb.ext_events) - (ca.rec_events + ca.ext_events)
+        n_sp = cb.n_spikes - ca.n_spikes
+        n_chunks = math.ceil(K / sim2.chunk)
+        line["e2e"] = {"value": ev / wall, "unit": "events/s",
                        "h2d_bytes_per_step": 0,
-                       "d2h_bytes_per_step": (12 * res.n_spikes + 128 * math.ceil(
-                           cfg.n_steps / 100)) / cfg.n_steps,
-                       "api": "paper_1803_08833_b200.run_b200(config, 1) sim_seconds_wall",
-                       "steps": cfg.n_steps}
+                       "d2h_bytes_per_step": (12 * n_sp + C.sizeof(_lib.Ctl) * n_chunks) / K,
+                       "api": "paper_1803_08833_b200.Simulator.advance(K) wall after advance(W) "
+                              "(the step loop of run_b200)",
+                       "steps": K, "warmup": W}
+        del sim2
     if not args.no_cpu:
         cb = cpu_oracle_sample(cfg, net, float(os.environ.get("CC_CPU_BUDGET_S", "20")), 10 ** 9)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}

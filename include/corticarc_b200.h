@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 24
+#define CC_ABI_VERSION 25
 
 /* Work items are queued in this many size classes, largest first. */
 /* Input lists per 32-neuron group (events of delay d go to sub-list
@@ -33,6 +33,16 @@ extern "C" {
 #endif
 #define CC_CNT_STRIDE_MAX 64
 #define CC_ITEM_CLASSES 8
+
+/* cc_shard.flags: measurement / test modes.  NO_TAIL_DELIVERY: k_stage's idle
+ * warps do not deliver the next step's delay >= 2 events, so cc_deliver
+ * deposits every arrival (bench.py's delivery roofline); PLAN_SEPARATE /
+ * PLAN_FUSED force the planning pass into its own kernel / into k_stage
+ * (tests; by default it is chosen by shard size).  Bits 32 / 256 / 512 / 1024
+ * / 2048 are timing probes of builds with -DCC_TIMING_PROBES=1 (tools/). */
+#define CC_FLAG_NO_TAIL_DELIVERY 0x1000
+#define CC_FLAG_PLAN_SEPARATE    0x4000
+#define CC_FLAG_PLAN_FUSED       0x8000
 
 /* error bits raised by kernels into cc_ctl.error_bits */
 #define CC_ERR_SPIKE_LOG      0x01u  /* more spikes in one step than log capacity   */
@@ -126,7 +136,7 @@ typedef struct cc_shard {
     int32_t ext_budget;     /* m = ceil(lam + 12 sqrt(lam)) + 20; 0 = no drive */
     int32_t n_probe;
     int32_t direct_log;     /* 1: neuron kernel logs its spikes itself (0: out-list only) */
-    int32_t debug_skip;     /* timing experiments only: bit mask of k_neuron stages to skip */
+    int32_t flags;          /* CC_FLAG_* mode bits (0 in production runs)       */
     int32_t plan_in_stage;  /* set by cc_neuron_step: k_stage runs the planning itself */
     int32_t del_lps_log2;   /* delivery: log2 lanes per spike (3: 4 spikes per warp unit, 4: 2) */
     int32_t pad32_;

@@ -277,6 +277,12 @@ def main():
                      probes=np.arange(0, 4960, 77)[:64]),
         ],
     }
+    # 64-neuron probe traces over half a second of BASELINE config 0 (the north
+    # star's "membrane-potential trace of 64 probed neurons" criterion)
+    jobs["probes_long"] = lambda: [
+        gold_run("config0_cal_0p5", presets.baseline_config(0, "calibrated", duration_s=0.5),
+                 probes=np.arange(0, 4960, 77)[:64]),
+    ]
     if a.big:
         jobs["big"] = lambda: [
             gold_run("config0_literal", presets.baseline_config(0, "literal"), workers=4),

@@ -7,7 +7,9 @@ Public surface (mirrors corticarc's names where they exist):
     SimConfig, MemoryBudgetError          run description (spec.py)
     build_b200, import_csr, export_csr    network build on the GPU, reference-format
                                           CSR in and out (network.py)
-    run_b200, Simulator, RunResult        simulate (engine.py)
+    run_b200, Simulator, RunResult        simulate (engine.py); workers > 1 runs one
+                                          process per worker (distributed.py)
+    write_raster                          the reference's raster file format
     runner                                the `runner(config, workers)` seam of
                                           metrics.scaling_harness / calibration_sweep
     baseline_config                       BASELINE.json configs 0-4 (presets.py)
@@ -23,7 +25,7 @@ __all__ = [
     "GridSpec", "KernelSpec", "SynapseGenSpec", "NeuronParams", "ExternalInputSpec",
     "SimConfig", "MemoryBudgetError", "baseline_config", "build_b200", "import_csr",
     "export_csr",
-    "run_b200", "Simulator", "RunResult", "runner", "__version__",
+    "run_b200", "Simulator", "RunResult", "runner", "write_raster", "__version__",
 ]
 
 
@@ -32,7 +34,7 @@ def __getattr__(name):
     if name in ("build_b200", "import_csr", "export_csr", "DeviceNetwork"):
         from . import network
         return getattr(network, name)
-    if name in ("run_b200", "Simulator", "RunResult"):
+    if name in ("run_b200", "Simulator", "RunResult", "write_raster"):
         from . import engine
         return getattr(engine, name)
     if name == "runner":

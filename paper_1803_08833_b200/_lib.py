@@ -15,7 +15,7 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "XPeer", "check", "EngineError",
 
 LIB_PATH = os.environ.get("CC_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 24
+ABI_VERSION = 25
 ITEM_CLASSES = 8
 CNT_STRIDE_MAX = 64          # bin_cnt words per group allocated (CC_CNT_STRIDE <= this)
 
@@ -77,7 +77,7 @@ class Shard(C.Structure):
         ("ovf_cap", C.c_int64), ("pad64_", C.c_int64), ("raster_cap", C.c_int64),
         ("scratch_cap", C.c_int64), ("n_rows", C.c_int64),
         ("out_cap", C.c_int32), ("ext_budget", C.c_int32), ("n_probe", C.c_int32),
-        ("direct_log", C.c_int32), ("debug_skip", C.c_int32), ("plan_in_stage", C.c_int32),
+        ("direct_log", C.c_int32), ("flags", C.c_int32), ("plan_in_stage", C.c_int32),
         ("del_lps_log2", C.c_int32), ("pad32_", C.c_int32),
         ("h2_ext", C.c_uint64), ("h2_time", C.c_uint64), ("h2_init", C.c_uint64),
         ("dt", C.c_double), ("ext_weight", C.c_double), ("ext_thresh", C.c_double),

@@ -42,6 +42,9 @@
 #ifndef CC_EVREC_STREAM
 #define CC_EVREC_STREAM 0
 #endif
+#ifndef CC_TIMING_PROBES
+#define CC_TIMING_PROBES 0   // timestamp / skip probes of the tools/*_timeline.py variants
+#endif
 
 namespace {
 
@@ -214,6 +217,13 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     return v;
 }
 
+// Set by any thread of a k_stage block that pushed a spike to a peer this
+// step: only those blocks need the system-scope fence before retiring.
+__device__ __forceinline__ int& x_pushed_block() {
+    __shared__ int flag;
+    return flag;
+}
+
 // Peer exchange, send half: push one spike into the region of every
 // destination rank in mask m (NVLink stores into the peer's window).
 __device__ __forceinline__ void x_push(const cc_shard& sh, long long t, uint32_t m, uint32_t gid,
@@ -223,6 +233,7 @@ __device__ __forceinline__ void x_push(const cc_shard& sh, long long t, uint32_t
         const int d = __ffs(m) - 1;
         m &= m - 1;
         const cc_xpeer& X = sh.xdst[d];
+        x_pushed_block() = 1;
         const unsigned o = atomicAdd(&sh.xcnt[d], 1u);
         if (o < X.cap)
             reinterpret_cast<uint4*>(X.rec[t & 1])[o] =
@@ -338,12 +349,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 
-// debug_skip & 32 (timing experiments only): per work item, 8 timestamps
+// Timing probes (tools/*_timeline.py; compiled only with -DCC_TIMING_PROBES=1):
+// flags & 32: per work item of k_stage, 8 timestamps
 // {claim, gathered, sorted, factors, updated, sm, rtot, warp} written to the
 // tail of the scratch buffer.
 #define CC_DBG(slot_i, val)                                                              \
     do {                                                                                 \
-        if ((sh.debug_skip & 32) && lane == 0 && item < 65536u) {                        \
+        if (CC_TIMING_PROBES && (sh.flags & 32) && lane == 0 && item < 65536u) {          \
             unsigned long long* d_ = reinterpret_cast<unsigned long long*>(sh.scratch)    \
                                      + (size_t)sh.scratch_cap * 7 - (size_t)(item + 1) * 8; \
             d_[slot_i] = (val);                                                          \
@@ -675,7 +687,7 @@ __device__ __forceinline__ void deposit_pass(const cc_shard& sh, const ListSet& 
         const int end = after ? __ffs(after) - 1 : 32;
         got[k] = 0u;
         if (tg[k] >= 0 && lane == lead[k]) {
-            if (sh.debug_skip & 1024) got[k] = 0u;       // timing experiment: no reservation
+            if (CC_TIMING_PROBES && (sh.flags & 1024)) got[k] = 0u;   // probe: no reservation
             else got[k] = atomicAdd(&S.cnt[((size_t)key[k] * NSUB + sub) * CC_CNT_STRIDE],
                                     (unsigned)(end - lead[k]));
         }
@@ -685,7 +697,7 @@ __device__ __forceinline__ void deposit_pass(const cc_shard& sh, const ListSet& 
         pos[k] = __shfl_sync(0xffffffffu, got[k], lead[k]) + (unsigned)(lane - lead[k]);
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-        if (tg[k] < 0 || (sh.debug_skip & 2048)) continue;  // 2048: timing, no deposit
+        if (tg[k] < 0 || (CC_TIMING_PROBES && (sh.flags & 2048))) continue;  // probe: no deposit
         const uint32_t lig = (uint32_t)tg[k] & 31u;
         if (pos[k] < (unsigned)K) {
             S.rec[((size_t)key[k] * NSUB + sub) * KS + pos[k]] =
@@ -874,7 +886,7 @@ __device__ __forceinline__ void plan_group(const cc_shard& sh, long long t, int 
             r[1] = my_item;
         }
     }
-    if ((sh.debug_skip & 512) && lane == 0 && gvalid) {
+    if (CC_TIMING_PROBES && (sh.flags & 512) && lane == 0 && gvalid) {
         unsigned long long* d_ = reinterpret_cast<unsigned long long*>(sh.scratch)
                                  + (size_t)sh.scratch_cap * 7 - (size_t)(group + 1) * 8;
         unsigned smid_;
@@ -926,6 +938,7 @@ k_stage(const cc_shard sh) {
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     StageBuf B = carve(nsm + wib * stage_warp_bytes());
+    if (threadIdx.x == 0) x_pushed_block() = 0;       // (published by the barriers below)
     const int t_mod_l = (int)pos_mod(t, sh.log_slots);
     const uint32_t K = (uint32_t)sh.bin_cap;
     const double t0 = (double)t * sh.dt;
@@ -955,7 +968,7 @@ k_stage(const cc_shard sh) {
     // logged): offered to the warps that run out of work items
     __shared__ unsigned a_n[DEL_DMAX], a_pre[DEL_DMAX + 1];
     const int D = sh.d_max;
-    const bool tail_deliver = D > 1 && !(sh.debug_skip & 4096);
+    const bool tail_deliver = D > 1 && !(sh.flags & CC_FLAG_NO_TAIL_DELIVERY);
     if (tail_deliver) unit_prefix(sh, t + 1, D - 1, a_n, a_pre);
     // queued items per size class (k_plan is complete); claimed largest first
     __shared__ unsigned cls_n[CC_ITEM_CLASSES];
@@ -1323,7 +1336,7 @@ k_stage(const cc_shard sh) {
         if (blk_s) atomicAdd(&ctl->n_spikes, (unsigned long long)blk_s);
         // (peer exchange: the block's pushes to other GPUs are ordered before
         // its completion, which the last block's release publishes)
-        if (sh.xdst) __threadfence_system(); else __threadfence();
+        if (sh.xdst && x_pushed_block()) __threadfence_system(); else __threadfence();
         if (atomicAdd(&ctl->done_stage, 1u) == gridDim.x - 1) {
             ctl->done_stage = 0;
             sh.tailc[32] = 0u;
@@ -1494,7 +1507,7 @@ k_deliver(const cc_shard sh) {
         for (int k = 0; k < U; ++k) { tg[k] = tg2[k]; w[k] = w2[k]; }
         u = u2; p = p2; st = st2; ln = ln2; rf = rf2; lmax = lmax2; kcur = k2;
     }
-    if ((sh.debug_skip & 256) && lane == 0) {
+    if (CC_TIMING_PROBES && (sh.flags & 256) && lane == 0) {
         unsigned long long* d_ = reinterpret_cast<unsigned long long*>(sh.scratch)
                                  + (size_t)sh.scratch_cap * 7 - 65536ull * 8 - (size_t)(wid + 1) * 4;
         unsigned smid_;
@@ -1519,7 +1532,7 @@ k_deliver(const cc_shard sh) {
         am_last = atomicAdd(&ctl->done_deliver, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if ((sh.debug_skip & 256) && threadIdx.x == 0) {
+    if (CC_TIMING_PROBES && (sh.flags & 256) && threadIdx.x == 0) {
         unsigned long long* d_ = reinterpret_cast<unsigned long long*>(sh.scratch)
                                  + (size_t)sh.scratch_cap * 7 - 65536ull * 8 - 65536ull * 4 - (size_t)(blockIdx.x + 1);
         d_[0] = gtimer();
@@ -1807,9 +1820,8 @@ extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
     const int groups = (sh->n_local + 31) / 32;
     const size_t smem = stage_warp_bytes() * STAGE_WARPS;
     if (const int rc = cc_prepare()) return rc;
-    // debug_skip bits 16384 / 32768 force the separate / fused planning (tests)
-    const bool fused = (sh->debug_skip & 32768) ||
-                       (!(sh->debug_skip & 16384) && groups > stage_blocks * STAGE_WARPS);
+    const bool fused = (sh->flags & CC_FLAG_PLAN_FUSED) ||
+                       (!(sh->flags & CC_FLAG_PLAN_SEPARATE) && groups > stage_blocks * STAGE_WARPS);
     if (!fused) {
         k_plan<<<(groups + 3) / 4, 128, 0, (cudaStream_t)stream>>>(*sh);
         if (const int rc = cc_check_launch("k_plan")) return rc;
@@ -1871,6 +1883,8 @@ extern "C" int cc_exchange_ingest(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_exchange_ingest: null shard");
     if (!sh->xsrc || !sh->xdst) return cc_set_error("cc_exchange_ingest: no peer exchange set up");
     if (sh->n_ranks < 1 || sh->n_ranks > 32) return cc_set_error("cc_exchange_ingest: 1..32 ranks");
-    k_xingest<<<sm_count(), 256, 0, (cudaStream_t)stream>>>(*sh);
+    // (a step's received spikes are few: a handful of blocks, each waiting on
+    // the flags itself, log them)
+    k_xingest<<<sm_count() / 4, 256, 0, (cudaStream_t)stream>>>(*sh);
     return cc_check_launch("k_xingest");
 }

@@ -32,8 +32,8 @@ Transports of the per-step exchange (DistributedSimulator):
           the same kernels run eagerly with a host barrier between the push and
           the ingest ("host" sync), so no kernel ever waits on another process's.
   "nccl"  baseline: cc_pack_aer into one fixed-size slot per destination, an
-          NCCL all-to-all of the slots (self excluded) captured in the chunk
-          graphs, cc_ingest_aer.  Slots are sized for the largest exact per-pair
+          NCCL all-to-all of the slots (equal splits; the self slot is empty and
+          copied locally) captured in the chunk graphs, cc_ingest_aer.  Slots are sized for the largest exact per-pair
           worst case, agreed by all ranks.
   "gloo"  the slots transport with the all-to-all on the host over gloo (eager;
           ranks may share a GPU): tests the pack / ingest kernels across real
@@ -429,7 +429,9 @@ class DistributedSimulator:
         def parts(buf):
             return [buf[d] if d != skip else buf[d][:0] for d in range(self.size)]
         if self.transport == "nccl":
-            dist.all_to_all(parts(self.recv), parts(self.send), group=self.nccl_group)
+            # equal splits over all slots (capturable); the self slot is empty
+            # unless loopback, and NCCL copies it locally
+            dist.all_to_all_single(self.recv, self.send, group=self.nccl_group)
             return
         # gloo: host staging (eager); gloo has all_to_all_single only
         self._send_h.copy_(self.send)
@@ -805,7 +807,7 @@ def run_spawned(config, workers: int, transport: str = "p2p", chunk: int = 100,
              for r in range(workers)]
     for p in procs:
         p.start()
-    pieces, err, err_at = [], None, 0.0
+    pieces, err, err_at, errs = [], None, 0.0, []
     deadline = time.time() + timeout
     received = 0
     try:
@@ -827,10 +829,15 @@ def run_spawned(config, workers: int, transport: str = "p2p", chunk: int = 100,
             received += 1
             if kind == "ok":
                 pieces.append(val)
-            elif err is None:
-                err, err_at = val, time.time()
+            else:
+                errs.append((r, val))
+                if err is None:
+                    err, err_at = val, time.time()
         if err is not None:
-            raise err
+            # the failing rank's own error over the ones of the ranks that
+            # stopped with it (agree_errors)
+            own = [e for _, e in errs if "stopped with it" not in str(e)]
+            raise (own or [err])[0]
     finally:
         for p in procs:
             p.join(timeout=0.5 if err is not None else 30)

@@ -27,7 +27,8 @@ from .geometry import grid_totals
 from .network import DeviceNetwork, build_b200
 from .spec import MemoryBudgetError
 
-__all__ = ["RunResult", "Simulator", "run_b200", "raster_checksum", "estimate_worker_bytes"]
+__all__ = ["RunResult", "Simulator", "run_b200", "raster_checksum", "estimate_worker_bytes",
+           "write_raster"]
 
 MASK64 = (1 << 64) - 1
 DOMAIN = 0x636F727469636172
@@ -62,6 +63,16 @@ def raster_checksum(gids, times) -> int:
             z = (z ^ (z >> u(27))) * u(0x94D049BB133111EB)
             return z ^ (z >> u(31))
         return int(np.sum(sm(lo ^ sm(hi)), dtype=u))
+
+
+def write_raster(path, gids, times_ms) -> None:
+    """`time_ms<TAB>neuron_gid` lines in ascending (time, gid) order - the
+    reference's raster file format (engine.py:531-536), byte for byte."""
+    gids = np.asarray(gids)
+    times_ms = np.asarray(times_ms, dtype=np.float64)
+    order = np.lexsort((gids, times_ms))
+    with open(path, "w") as fh:
+        fh.writelines(f"{t:.9f}\t{int(g)}\n" for t, g in zip(times_ms[order], gids[order]))
 
 
 def estimate_worker_bytes(config, workers: int) -> int:
@@ -175,8 +186,12 @@ class Simulator:
         seg_stride = (D + 1 + 7) // 8 * 8
         dseg = net.delay_segments(D, seg_stride)
         raster_cap = max(1024, n_local * bound * max(self.chunk, raster_steps or 0))
-        # spill staging for onset bursts (neuron-steps with > NEURON_WCAP inputs)
-        scratch_cap = max(1 << 16, n_local * int(os.environ.get("CC_SCRATCH_PER_NEURON", "64")))
+        # spill staging for onset bursts (neuron-steps with > NEURON_WCAP inputs, all
+        # of one step): the synchronous onset grows with the drive, so strongly
+        # driven runs (>= 10 drive events per neuron-step) get 4x the headroom
+        lam0 = cfg.external.mean_per_step(cfg.timestep_ms)
+        per_neuron = int(os.environ.get("CC_SCRATCH_PER_NEURON", "0")) or (256 if lam0 >= 10 else 64)
+        scratch_cap = max(1 << 16, n_local * per_neuron)
         # ordered-input records of one step: the expected list capacity of a step,
         # the overflow list and every neuron's Poisson budget (beyond it the
         # step fails with "event staging scratch exhausted")
@@ -234,7 +249,7 @@ class Simulator:
         sh.n_local, sh.n_col, sh.n_exc_col = n_local, n, grid.n_excitatory_per_column
         sh.d_max, sh.bin_cap, sh.log_slots = D, bin_cap, D + 1
         sh.n_groups, sh.bin_pad = n_groups, bin_pad
-        sh.debug_skip = int(os.environ.get("CC_DEBUG_SKIP", "0"))   # timing experiments only
+        sh.flags = int(os.environ.get("CC_FLAGS", "0"))    # CC_FLAG_* (measurement / tests)
         sh.spk_cap, sh.seg_stride = spk_cap, seg_stride
         # delivery lanes per spike: 16 on shards of >= 2 M neurons (config 3 gaussian: k_deliver
         # 448 -> 367 us, step -3.3 %), 8 below (configs 1, 2 and the config-4 GPU block: 16 lanes are ~1 % slower);

@@ -112,7 +112,7 @@ def test_generator_config0_checksum(cuda, regime):
 
 # ------------------------------------------------------------ full runs
 RUNS = ["tiny_gauss", "tiny_exp", "tiny_gauss_long", "tiny_quiet", "config0_literal_0p2",
-        "config0_cal_0p1"]
+        "config0_cal_0p1", "config0_cal_0p5"]       # 0p1 / 0p5: 64 probe traces, 0.1 / 0.5 s
 
 
 def _assert_same_run(res, meta, arr):
@@ -220,10 +220,10 @@ def test_tail_delivery_off_same_run(cuda, name, monkeypatch):
     from paper_1803_08833_b200.engine import Simulator, run_b200
     from paper_1803_08833_b200.network import build_b200
     cfg, meta, arr = golden_run(name)
-    monkeypatch.setenv("CC_DEBUG_SKIP", "4096")
+    monkeypatch.setenv("CC_FLAGS", "4096")
     res = run_b200(cfg, 1)
     _assert_same_run(res, meta, arr)
-    monkeypatch.delenv("CC_DEBUG_SKIP")
+    monkeypatch.delenv("CC_FLAGS")
     sim = Simulator(cfg, build_b200(cfg))
     sim.advance(cfg.n_steps)
     c = sim.ctl()
@@ -244,7 +244,7 @@ def test_delivery_lanes_per_spike_same_run(cuda, name, lps, tail, monkeypatch):
     from paper_1803_08833_b200.engine import run_b200
     cfg, meta, arr = golden_run(name)
     monkeypatch.setenv("CC_DEL_LPS", lps)
-    monkeypatch.setenv("CC_DEBUG_SKIP", tail)
+    monkeypatch.setenv("CC_FLAGS", tail)
     _assert_same_run(run_b200(cfg, 1), meta, arr)
 
 
@@ -255,7 +255,7 @@ def test_planning_inside_k_stage_same_run(cuda, name, monkeypatch):
     debug bit 32768) reproduces the reference run."""
     from paper_1803_08833_b200.engine import run_b200
     cfg, meta, arr = golden_run(name)
-    monkeypatch.setenv("CC_DEBUG_SKIP", "32768")
+    monkeypatch.setenv("CC_FLAGS", "32768")
     _assert_same_run(run_b200(cfg, 1), meta, arr)
 
 
@@ -271,7 +271,7 @@ def test_planning_modes_agree_at_scale(cuda, monkeypatch):
     cfg = replace(cfg, grid=S.GridSpec(nx=10, ny=10, neurons_per_column=1240))
     net = build_b200(cfg)
     a = run_b200(cfg, 1, net=net)
-    monkeypatch.setenv("CC_DEBUG_SKIP", "16384")
+    monkeypatch.setenv("CC_FLAGS", "16384")
     b = run_b200(cfg, 1, net=net)
     assert a.n_spikes > 1000
     assert a.raster_checksum == b.raster_checksum and a.n_spikes == b.n_spikes

@@ -1,4 +1,5 @@
-"""Per-warp timeline of k_deliver (debug_skip bit 256)."""
+"""[needs a library built with -DCC_TIMING_PROBES=1, selected with CC_LIB_PATH]
+Per-warp timeline of k_deliver (flags bit 256)."""
 import ctypes as C
 import os
 import sys
@@ -21,12 +22,12 @@ st = torch.cuda.current_stream().cuda_stream
 nw = 148 * 2 * 8
 extra = int(os.environ.get("DBG", "0"))
 for rep in range(3):
-    sim.shard.debug_skip = 256 | extra
+    sim.shard.flags = 256 | extra
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     _lib.check(L.cc_deliver(C.byref(sim.shard), st))
     e1.record()
-    sim.shard.debug_skip = 0
+    sim.shard.flags = 0
     _lib.check(L.cc_neuron_step(C.byref(sim.shard), st))
     torch.cuda.synchronize()
     raw = sim.buf["scratch"].view(torch.int64).reshape(-1)

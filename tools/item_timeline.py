@@ -1,4 +1,5 @@
-"""Per-work-item timeline of k_stage (debug_skip bit 32)."""
+"""[needs a library built with -DCC_TIMING_PROBES=1, selected with CC_LIB_PATH]
+Per-work-item timeline of k_stage (flags bit 32)."""
 import ctypes as C
 import os
 import sys
@@ -20,9 +21,9 @@ L = sim.L
 st = torch.cuda.current_stream().cuda_stream
 for rep in range(2):
     _lib.check(L.cc_deliver(C.byref(sim.shard), st))
-    sim.shard.debug_skip = 32
+    sim.shard.flags = 32
     _lib.check(L.cc_neuron_step(C.byref(sim.shard), st))
-    sim.shard.debug_skip = 0
+    sim.shard.flags = 0
     torch.cuda.synchronize()
     ni = int(sim.ctl().n_rounds)
     raw = sim.buf["scratch"].view(torch.int64).reshape(-1)

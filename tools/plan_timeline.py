@@ -1,4 +1,5 @@
-"""Per-group timeline of k_plan (debug_skip bit 512): start, records counted,
+"""[needs a library built with -DCC_TIMING_PROBES=1, selected with CC_LIB_PATH]
+Per-group timeline of k_plan (flags bit 512): start, records counted,
 Poisson done, items split, items queued."""
 import ctypes as C
 import os
@@ -22,9 +23,9 @@ st = torch.cuda.current_stream().cuda_stream
 ng = sim.shard.n_groups
 for rep in range(3):
     _lib.check(L.cc_deliver(C.byref(sim.shard), st))
-    sim.shard.debug_skip = 512
+    sim.shard.flags = 512
     _lib.check(L.cc_neuron_step(C.byref(sim.shard), st))
-    sim.shard.debug_skip = 0
+    sim.shard.flags = 0
     torch.cuda.synchronize()
     raw = sim.buf["scratch"].view(torch.int64).reshape(-1)
     tail = raw[raw.numel() - ng * 8:].cpu().numpy().reshape(ng, 8)[::-1].astype(np.int64)

@@ -1,5 +1,6 @@
-"""Per-stage cost of k_neuron: time one step from an identical restored
-snapshot with stages masked out (debug_skip), averaged over several steps."""
+"""[needs a library built with -DCC_TIMING_PROBES=1, selected with CC_LIB_PATH]
+Per-stage cost of k_neuron: time one step from an identical restored
+snapshot with stages masked out (flags), averaged over several steps."""
 import ctypes as C
 import os
 import sys
@@ -28,7 +29,7 @@ for rep in range(5):
     for name, mask in variants.items():
         for k, v in snap.items():
             sim.buf[k].copy_(v)
-        sim.shard.debug_skip = mask
+        sim.shard.flags = mask
         torch.cuda.synchronize()
         e0.record()
         _lib.check(L.cc_deliver(C.byref(sim.shard), st))

@@ -1,4 +1,5 @@
-"""Per-warp timeline of k_stage (debug_skip bit 32): where does a warp spend time?"""
+"""[needs a library built with -DCC_TIMING_PROBES=1, selected with CC_LIB_PATH]
+Per-warp timeline of k_stage (flags bit 32): where does a warp spend time?"""
 import ctypes as C
 import os
 import sys
@@ -21,9 +22,9 @@ st = torch.cuda.current_stream().cuda_stream
 nw = (sim.n_local + 31) // 32
 for rep in range(3):
     _lib.check(L.cc_deliver(C.byref(sim.shard), st))
-    sim.shard.debug_skip = 32 | 8
+    sim.shard.flags = 32 | 8
     _lib.check(L.cc_neuron_step(C.byref(sim.shard), st))
-    sim.shard.debug_skip = 0
+    sim.shard.flags = 0
     torch.cuda.synchronize()
     raw = sim.buf["scratch"].view(torch.int64).view(-1)
     tail = raw[raw.numel() - nw * 16:].cpu().numpy().reshape(nw, 16)[::-1]
