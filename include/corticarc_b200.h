@@ -381,6 +381,9 @@ int cc_csr_checksum(const int64_t* row_off, const uint32_t* src_gid, int64_t n_s
  * counter_uniforms(seed, purpose, a, b, k) of rng.py:74-90. */
 int cc_test_philox(uint64_t seed, uint64_t purpose, uint64_t a, int64_t n,
                    int32_t kind, double* out, void* stream);
+/* The neuron update's exponentials on n arguments: kind 0 fexp (table-driven
+ * e^x), 1 fexpm1, 2 / 3 libdevice exp / expm1 for comparison. */
+int cc_test_math(int32_t kind, const double* x, double* out, int64_t n, void* stream);
 int cc_test_counter_uniforms(uint64_t seed, uint64_t purpose, const uint64_t* a,
                              uint64_t b, const uint64_t* k, int64_t n, double* out,
                              void* stream);

@@ -147,6 +147,7 @@ _SIGS = {
     "cc_csr_checksum": (C.c_int, [_P, _P, C.c_int64, _P, _P, _P, C.c_int32, C.c_int32, _P, _P]),
     "cc_test_philox": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_int32,
                                  _P, _P]),
+    "cc_test_math": (C.c_int, [C.c_int32, _P, _P, C.c_int64, _P]),
     "cc_test_counter_uniforms": (C.c_int, [C.c_uint64, C.c_uint64, _P, C.c_uint64, _P,
                                            C.c_int64, _P, _P]),
 }

@@ -71,6 +71,71 @@ __device__ __forceinline__ double div_rn(double a, double b, double rb) {
     return __fma_rn(r, rb, q0);
 }
 
+// Exponentials of the decay factors (np.exp / np.expm1 in _voltage_decay,
+// model.py:131-138, and advance, model.py:280).  The reference's values come
+// from numpy's SIMD routines, within 1 ulp of the exact result; any <= 1 ulp
+// implementation reproduces its rasters.  These
+// are shorter than libdevice's degree-11 polynomials on the hot path:
+//   fexp    e^x = 2^(k/32) e^r, k = rint(32 x / ln2), |r| <= ln2/64; 2^(j/32) from
+//           a table as hi + lo (the hi part correctly rounded), e^r - 1 by a
+//           degree-6 Taylor polynomial (truncation < 0.03 ulp); 0.6 % of results
+//           differ from the correctly rounded value by 1 ulp (np.exp: 5.6 %),
+//           none by more (tools/micro/fexp.c, 1e7 arguments; tests/test_gpu_parity.py)
+//   fexpm1  |x| <= 1/16: x + x^2 (1/2! + x/3! + ... + x^10/12!)
+// Outside their ranges both fall back to libdevice.  The table lives in
+// shared memory (k_stage copies it at entry).
+__constant__ double2 c_exp2_tab[32] = {
+    {0x1.0000000000000p+0, 0x0.0p+0}, {0x1.059b0d3158574p+0, 0x1.d73e2a475b465p-55},
+    {0x1.0b5586cf9890fp+0, 0x1.8a62e4adc610bp-54}, {0x1.11301d0125b51p+0, -0x1.6c51039449b3ap-54},
+    {0x1.172b83c7d517bp+0, -0x1.19041b9d78a76p-55}, {0x1.1d4873168b9aap+0, 0x1.e016e00a2643cp-54},
+    {0x1.2387a6e756238p+0, 0x1.9b07eb6c70573p-54}, {0x1.29e9df51fdee1p+0, 0x1.612e8afad1255p-55},
+    {0x1.306fe0a31b715p+0, 0x1.6f46ad23182e4p-55}, {0x1.371a7373aa9cbp+0, -0x1.63aeabf42eae2p-54},
+    {0x1.3dea64c123422p+0, 0x1.ada0911f09ebcp-55}, {0x1.44e086061892dp+0, 0x1.89b7a04ef80d0p-59},
+    {0x1.4bfdad5362a27p+0, 0x1.d4397afec42e2p-56}, {0x1.5342b569d4f82p+0, -0x1.07abe1db13cadp-55},
+    {0x1.5ab07dd485429p+0, 0x1.6324c054647adp-54}, {0x1.6247eb03a5585p+0, -0x1.383c17e40b497p-54},
+    {0x1.6a09e667f3bcdp+0, -0x1.bdd3413b26456p-54}, {0x1.71f75e8ec5f74p+0, -0x1.16e4786887a99p-55},
+    {0x1.7a11473eb0187p+0, -0x1.41577ee04992fp-55}, {0x1.82589994cce13p+0, -0x1.d4c1dd41532d8p-54},
+    {0x1.8ace5422aa0dbp+0, 0x1.6e9f156864b27p-54}, {0x1.93737b0cdc5e5p+0, -0x1.75fc781b57ebcp-57},
+    {0x1.9c49182a3f090p+0, 0x1.c7c46b071f2bep-56}, {0x1.a5503b23e255dp+0, -0x1.d2f6edb8d41e1p-54},
+    {0x1.ae89f995ad3adp+0, 0x1.7a1cd345dcc81p-54}, {0x1.b7f76f2fb5e47p+0, -0x1.5584f7e54ac3bp-56},
+    {0x1.c199bdd85529cp+0, 0x1.11065895048ddp-55}, {0x1.cb720dcef9069p+0, 0x1.503cbd1e949dbp-56},
+    {0x1.d5818dcfba487p+0, 0x1.2ed02d75b3707p-55}, {0x1.dfc97337b9b5fp+0, -0x1.1a5cd4f184b5cp-54},
+    {0x1.ea4afa2a490dap+0, -0x1.e9c23179c2893p-54}, {0x1.f50765b6e4540p+0, 0x1.9d3e12dd8a18bp-54}};
+
+__device__ __forceinline__ double fexp(double x, const double2* xt) {
+    if (!(x > -700.0 && x < 700.0)) return exp(x);             // NaN / extreme: libdevice
+    const double sh = 6755399441055744.0;                      // 1.5 * 2^52
+    const double kd = __fma_rn(x, 0x1.71547652b82fep+5, sh);            // 32 / ln2
+    const int k = __double2loint(kd);
+    const double kf = __dsub_rn(kd, sh);
+    double r = __fma_rn(kf, -0x1.62e42fefa39efp-6, x);                   // ln2/32 (hi)
+    r = __fma_rn(kf, -0x1.abc9e3b39803fp-61, r);                          // ln2/32 (lo)
+    double p = __fma_rn(r, 1.0 / 720.0, 1.0 / 120.0);
+    p = __fma_rn(r, p, 1.0 / 24.0);
+    p = __fma_rn(r, p, 1.0 / 6.0);
+    p = __fma_rn(r, p, 0.5);
+    p = __fma_rn(r, p, 1.0);
+    p = __dmul_rn(p, r);                                       // e^r - 1
+    const double2 t = xt[k & 31];
+    const double y = __dadd_rn(t.x, __fma_rn(t.x, p, t.y));
+    return __hiloint2double(__double2hiint(y) + ((k >> 5) << 20), __double2loint(y));
+}
+
+__device__ __forceinline__ double fexpm1(double x) {
+    if (!(fabs(x) <= 0.0625)) return expm1(x);
+    double p = __fma_rn(x, 1.0 / 479001600.0, 1.0 / 39916800.0);
+    p = __fma_rn(x, p, 1.0 / 3628800.0);
+    p = __fma_rn(x, p, 1.0 / 362880.0);
+    p = __fma_rn(x, p, 1.0 / 40320.0);
+    p = __fma_rn(x, p, 1.0 / 5040.0);
+    p = __fma_rn(x, p, 1.0 / 720.0);
+    p = __fma_rn(x, p, 1.0 / 120.0);
+    p = __fma_rn(x, p, 1.0 / 24.0);
+    p = __fma_rn(x, p, 1.0 / 6.0);
+    p = __fma_rn(x, p, 0.5);
+    return __fma_rn(__dmul_rn(x, x), p, x);
+}
+
 // Free evolution of one neuron to time te (NeuronBlock.advance,
 // model.py:272-287 with _voltage_decay, model.py:116-143).
 struct NState { double V, c, last, ru; };
@@ -322,21 +387,22 @@ __device__ __forceinline__ StageBuf carve(char* p) {
 
 // decay factors of one event (the dt-dependent part of _voltage_decay)
 __device__ __forceinline__ void decay_factors(const cc_pop& P, double dt, bool with_c,
-                                              double& em, double& ec, double& f) {
+                                              double& em, double& ec, double& f,
+                                              const double2* xt) {
     ec = 1.0;
     f = 0.0;
     if (dt == 0.0) {            // exp(-0/tau) == 1, x == 0 -> f = 0 * 1: exact shortcut
         em = 1.0;
         return;
     }
-    em = exp(-div_rn(dt, P.tau_m, P.r_tau_m));
+    em = fexp(-div_rn(dt, P.tau_m, P.r_tau_m), xt);
     if (with_c) {
-        ec = exp(-div_rn(dt, P.tau_c, P.r_tau_c));
+        ec = fexp(-div_rn(dt, P.tau_c, P.r_tau_c), xt);
         const double x = div_rn(dt * P.k1, P.k2, P.r_k2);
         if (x == 0.0)
             f = dt * em;
         else if (fabs(x) <= 1.0)
-            f = dt * em * expm1(x) / x;
+            f = dt * em * fexpm1(x) / x;
         else
             f = dt * (ec - em) / x;
     }
@@ -372,15 +438,15 @@ __device__ __forceinline__ int neuron_pop(const cc_shard& sh, uint32_t gid) {
 // (valid unless stale, like em0, ec0, f0).
 __device__ __forceinline__ bool slow_step(NState& s, const cc_pop& P, double tj, bool stale,
                                        bool cflag, double em0, double ec0, double f0,
-                                       double ecr0, double w) {
+                                       double ecr0, double w, const double2* xt) {
     const double ff = fmin(fmax(s.last, s.ru), tj);
     double cs = s.c;
     if (ff != s.last && cs != 0.0) {                  // leaving / inside a refractory window
-        if (stale) cs = cs * exp(-div_rn(ff - s.last, P.tau_c, P.r_tau_c));
+        if (stale) cs = cs * fexp(-div_rn(ff - s.last, P.tau_c, P.r_tau_c), xt);
         else cs = cs * ecr0;
     }
     double emj = em0, ecj = ec0, fj = f0;
-    if (stale) decay_factors(P, tj - ff, cs != 0.0, emj, ecj, fj);
+    if (stale) decay_factors(P, tj - ff, cs != 0.0, emj, ecj, fj, xt);
     else if (!cflag) { ecj = 1.0; fj = 0.0; }
     // model.py:116-143 and 272-287, reference op order
     const double Vs = (s.last < s.ru) ? P.V_r : s.V;
@@ -432,7 +498,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 
 __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long long t,
-                                             double2* S, uint32_t& my_spikes) {
+                                             double2* S, uint32_t& my_spikes,
+                                             const double2* xt) {
     cc_ctl* ctl = sh.ctl;
     const int lane = threadIdx.x & 31;
     const int li = li0 + lane;
@@ -524,7 +591,7 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
                 const double V = Vt + wv;
                 if (V > P->V_theta) spike = true; else s.V = V;
             } else {
-                spike = slow_step(s, *P, tj, stale, cflag, em, ec, f, ecr, wv);
+                spike = slow_step(s, *P, tj, stale, cflag, em, ec, f, ecr, wv, xt);
             }
             if (spike) {                             // strict threshold crossed
                 s.V = P->V_r;
@@ -939,6 +1006,8 @@ k_stage(const cc_shard sh) {
     const int wib = threadIdx.x >> 5;
     StageBuf B = carve(nsm + wib * stage_warp_bytes());
     if (threadIdx.x == 0) x_pushed_block() = 0;       // (published by the barriers below)
+    __shared__ double2 s_xt[32];                      // 2^(j/32) table of fexp
+    if (threadIdx.x < 32) s_xt[threadIdx.x] = c_exp2_tab[threadIdx.x];
     const int t_mod_l = (int)pos_mod(t, sh.log_slots);
     const uint32_t K = (uint32_t)sh.bin_cap;
     const double t0 = (double)t * sh.dt;
@@ -1246,9 +1315,10 @@ k_stage(const cc_shard sh) {
                 const double ff = fmin(fmax(last, ru), te);
                 double em, ec, f;
                 const cc_pop& P = sh.pop[fl & 1u];
-                decay_factors(P, te - ff, (fl & 2u) != 0, em, ec, f);
+                decay_factors(P, te - ff, (fl & 2u) != 0, em, ec, f, s_xt);
                 // fatigue decay over the refractory part of the gap (slow_step)
-                const double ecr = (ff != last && (fl & 2u)) ? exp(-div_rn(ff - last, P.tau_c, P.r_tau_c)) : 1.0;
+                const double ecr = (ff != last && (fl & 2u))
+                                       ? fexp(-div_rn(ff - last, P.tau_c, P.r_tau_c), s_xt) : 1.0;
                 const double wv = (Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
 #if CC_EVREC_STREAM
                 __stcs(R + 3 * p, make_double2(te, wv));
@@ -1273,7 +1343,7 @@ k_stage(const cc_shard sh) {
             __threadfence();
             if (lane == 0) sh.grp_done[group] = 0u;
             update_group(sh, li0, t, reinterpret_cast<double2*>(nsm + wib * stage_warp_bytes()),
-                         my_spikes);
+                         my_spikes, s_xt);
         }
         {
             unsigned smid_;
@@ -1727,6 +1797,18 @@ __global__ void k_ingest_aer(const cc_shard sh, const long long* recv, int n_src
     }
 }
 
+// Test probe of the decay-factor exponentials (tests/test_gpu_parity.py).
+__global__ void k_test_math(int kind, const double* x, double* out, int64_t n) {
+    __shared__ double2 xt[32];
+    if (threadIdx.x < 32) xt[threadIdx.x] = c_exp2_tab[threadIdx.x];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = x[i];
+        out[i] = kind == 0 ? fexp(v, xt) : kind == 1 ? fexpm1(v) : kind == 2 ? exp(v) : expm1(v);
+    }
+}
+
 __global__ void k_init_state(const cc_shard sh) {
     const int li = blockIdx.x * blockDim.x + threadIdx.x;
     if (li >= sh.n_local) return;
@@ -1887,4 +1969,11 @@ extern "C" int cc_exchange_ingest(const cc_shard* sh, void* stream) {
     // the flags itself, log them)
     k_xingest<<<sm_count() / 4, 256, 0, (cudaStream_t)stream>>>(*sh);
     return cc_check_launch("k_xingest");
+}
+
+extern "C" int cc_test_math(int32_t kind, const double* x, double* out, int64_t n, void* stream) {
+    if (kind < 0 || kind > 3) return cc_set_error("cc_test_math: kind 0..3");
+    if (n <= 0) return 0;
+    k_test_math<<<sm_count() * 4, 256, 0, (cudaStream_t)stream>>>(kind, x, out, n);
+    return cc_check_launch("k_test_math");
 }
