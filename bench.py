@@ -312,20 +312,38 @@ def main():
 def bench_single(args):
     import torch
     from paper_1803_08833_b200 import _lib
-    from paper_1803_08833_b200.engine import Simulator
     from paper_1803_08833_b200.network import build_b200
-    L = _lib.lib()
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
     cfg = workload(args)
     net = build_b200(cfg)
+    capacity = {}
+    while True:
+        try:
+            return _bench_single(args, cfg, net, capacity)
+        except _lib.EngineError as err:
+            # an expectation-sized buffer overflowed (onset burst of a strongly
+            # driven config): measure again from t = 0 with it doubled
+            capacity = _lib.grow_capacity(err, dict(ovf=1, scratch=1, evrec=1, **capacity))
+            if capacity is None:
+                raise
+            torch.cuda.empty_cache()
+
+
+def _bench_single(args, cfg, net, capacity):
+    import torch
+    from paper_1803_08833_b200 import _lib
+    from paper_1803_08833_b200.engine import Simulator
+    L = _lib.lib()
+    dev = torch.device("cuda:0")
     K, W = args.steps, args.warmup
     # timed: steps W .. W+K-1 (like the reference arm), as K / CH replays of a
     # CH-step graph; CH divides K and fits in the warm-up, whose last CH steps
     # are one untimed replay of that same graph (graph upload and first-launch
     # costs stay outside the timed region)
     CH = max(d for d in range(1, min(args.chunk, W, K) + 1) if K % d == 0)
-    sim = Simulator(cfg, net, chunk=CH, raster_steps=K + CH, bin_cap=args.bin_cap)
+    sim = Simulator(cfg, net, chunk=CH, raster_steps=K + CH, bin_cap=args.bin_cap,
+                    capacity=capacity)
     sim.advance(W - CH)                                    # warm-up (eager + graphs)
     sim.check()
     g_main = sim.capture(CH)
@@ -414,6 +432,7 @@ def bench_single(args):
         "instrumented_steps": NI,
         "instrumented_ms_per_step": (del_ms + neu_ms) / NI,
     }
+    dsegb = int(sum(x.numel() * x.element_size() for x in net.dseg_cache.values()))
     line = {
         "metric": "synaptic events/s (recurrent + external)",
         "value": value, "unit": "events/s", "n_gpus": 1, "steps": K, "warmup": W,
@@ -453,6 +472,18 @@ def bench_single(args):
         "clocks": clk,
         "construction_s": net.construction_seconds,
         "bytes_per_synapse_steady": net.steady_bytes / max(1, net.n_synapses),
+        "capacity": dict(sim.capacity),
+        "memory": {"csr_bytes": int(net.steady_bytes),
+                   "delay_segment_table_bytes": int(sum(x.numel() * x.element_size()
+                                                        for x in net.dseg_cache.values())),
+                   "simulation_buffer_bytes": int(sim.device_bytes),
+                   "device_bytes_total": int(net.steady_bytes + sim.device_bytes + dsegb),
+                   "bytes_per_synapse_total": (net.steady_bytes + sim.device_bytes + dsegb)
+                   / max(1, net.n_synapses),
+                   "torch_max_allocated_bytes": int(torch.cuda.max_memory_allocated(dev)),
+                   "what": "CSR (9 B/synapse + row index) and every simulation buffer of the "
+                           "shard (input lists, ordered-input records, spill staging, spike "
+                           "log, state), as allocated; paper's memory study: PAPER.md:698-710"},
         "device_stats": {"max_bin": int(c1.max_bin), "max_events": int(c1.max_events),
                          "overflow_records": int(c1.ovf_total),
                          "spilled_neuron_steps": int(c1.spilled_total),
@@ -466,7 +497,7 @@ def bench_single(args):
         # advance(K) - pipelined chunk graphs, per-chunk counter checks, error
         # checks and the raster's device->host copies (the expansion-time event
         # count of the onset's first steps stays out of both numbers)
-        sim2 = Simulator(cfg, net, chunk=min(args.chunk, K), raster_steps=K)
+        sim2 = Simulator(cfg, net, chunk=min(args.chunk, K), raster_steps=K, capacity=capacity)
         sim2.advance(W)
         ca = sim2.check()
         torch.cuda.synchronize(dev)

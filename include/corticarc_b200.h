@@ -57,6 +57,8 @@ extern "C" {
 #define CC_ERR_GRIDSYNC       0x200u /* k_stage grid barrier timed out              */
 #define CC_ERR_XWAIT          0x400u /* peer exchange: a source's step flag did not arrive in time */
 #define CC_ERR_XCAP           0x800u /* peer exchange: destination region full     */
+#define CC_ERR_CHECK          0x1000u/* checked build (CC_CHECKS): a bounds / protocol assertion
+                                        failed; error_step holds its source line    */
 
 /* Constants of one neuron population (model.py:44-86, NeuronBlock
  * per-neuron arrays model.py:243-267).  k1 = tau_c - tau_m and

@@ -32,11 +32,20 @@ ERR_BITS = {
     0x200: "k_stage grid barrier timed out (blocks not co-resident)",
     0x400: "peer exchange: a source rank's spikes of the step did not arrive in time",
     0x800: "peer exchange: destination region full",
+    0x1000: "checked build: bounds / protocol assertion failed (error step = source line)",
 }
 
 
 class EngineError(RuntimeError):
-    """A device-side capacity or protocol violation, naming the step."""
+    """A device-side capacity or protocol violation, naming the step; .bits
+    holds the cc_ctl.error_bits when it came from the device."""
+
+    def __init__(self, msg: str = "", bits: int = 0):
+        super().__init__(msg)
+        self.bits = int(bits)
+
+    def __reduce__(self):                     # picklable across worker processes
+        return (EngineError, (str(self), self.bits))
 
 
 class Pop(C.Structure):
@@ -194,6 +203,36 @@ def check(rc: int, what: str = "") -> None:
     if rc != 0:
         msg = _lib.cc_last_error().decode() if _lib is not None else "?"
         raise EngineError(f"{what}: {msg}" if what else msg)
+
+
+# buffers sized by expectation (run_b200 re-runs with more capacity): overflow
+# list, spill staging, ordered-input records
+CAPACITY_BITS = 0x04 | 0x08 | 0x100
+
+
+def capacity_error(err: "EngineError") -> bool:
+    """True when an EngineError is only a capacity overflow of the
+    expectation-sized buffers (no other error bit set)."""
+    bits = getattr(err, "bits", 0)
+    return bool(bits) and not (bits & ~CAPACITY_BITS)
+
+
+_GROW = {0x04: "ovf", 0x08: "scratch", 0x100: "evrec"}
+
+
+def grow_capacity(err: "EngineError", capacity: dict, limit: int = 32):
+    """The capacity multipliers for a re-run after `err`: the overflowed
+    buffers doubled, or None if err is not (only) such an overflow or a
+    buffer is already at `limit`."""
+    if not capacity_error(err):
+        return None
+    out = dict(capacity)
+    for bit, key in _GROW.items():
+        if err.bits & bit:
+            if out.get(key, 1) >= limit:
+                return None
+            out[key] = out.get(key, 1) * 2
+    return out
 
 
 def decode_errors(bits: int) -> str:

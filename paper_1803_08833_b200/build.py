@@ -68,10 +68,16 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
 SPILL_VARIANT = os.path.join(PKG, "libcorticarc_b200_w4.so")
 
 
+# Bounds and protocol assertions compiled in (CC_CHK in cc_common.cuh): the
+# parity tests run small cases through it in place of compute-sanitizer.
+CHECKED_VARIANT = os.path.join(PKG, "libcorticarc_b200_chk.so")
+
+
 def build_test_variants(force: bool = False) -> None:
-    if force or not os.path.exists(SPILL_VARIANT) or \
-            os.path.getmtime(SPILL_VARIANT) < os.path.getmtime(LIB):
-        build(force=True, out=SPILL_VARIANT, defines=("CC_NEURON_WCAP=4", "CC_UPD_PIPE=0"))
+    for path, defines in ((SPILL_VARIANT, ("CC_NEURON_WCAP=4", "CC_UPD_PIPE=0")),
+                          (CHECKED_VARIANT, ("CC_CHECKS=1",))):
+        if force or not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(LIB):
+            build(force=True, out=path, defines=defines)
 
 
 if __name__ == "__main__":

@@ -137,3 +137,25 @@ __device__ __forceinline__ void cc_raise(cc_ctl* ctl, unsigned bits, long long t
     atomicOr(&ctl->error_bits, bits);
     atomicMin(&ctl->error_step, t);
 }
+
+// Bounds and protocol assertions of the checked build (-DCC_CHECKS=1,
+// libcorticarc_b200_chk.so, run by tests/test_gpu_parity.py in place of a
+// compute-sanitizer pass): a failed check prints its source line and raises
+// CC_ERR_CHECK with the line as the error "step".  Compiled away otherwise.
+#ifndef CC_CHECKS
+#define CC_CHECKS 0
+#endif
+#if CC_CHECKS
+#include <cstdio>
+static __device__ __noinline__ void cc_check_fail(cc_ctl* ctl, const char* file, int line,
+                                                  const char* what) {
+    printf("cc check failed: %s:%d: %s\n", file, line, what);
+    cc_raise(ctl, CC_ERR_CHECK, (long long)line);
+}
+#define CC_CHK(ctl, cond)                                                  \
+    do {                                                                   \
+        if (!(cond)) cc_check_fail((ctl), __FILE__, __LINE__, #cond);      \
+    } while (0)
+#else
+#define CC_CHK(ctl, cond) do { } while (0)
+#endif

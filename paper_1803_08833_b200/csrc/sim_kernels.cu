@@ -214,6 +214,7 @@ struct SubMap {
 // delivered in step t + d).  len == 0: no synapse on this shard.
 __device__ __forceinline__ void log_spike(const cc_shard& sh, long long t, uint32_t gid,
                                           double te) {
+    CC_CHK(sh.ctl, gid < (uint32_t)sh.n_rows);
     const int64_t r0 = sh.row_off[gid];
     const int64_t len = sh.row_off[gid + 1] - r0;
     if (len == 0) return;
@@ -240,6 +241,7 @@ __device__ __forceinline__ void log_spike_warp(const cc_shard& sh, long long t, 
     const int lane = threadIdx.x & 31;
     int64_t r0 = 0, len = 0;
     if (valid) {
+        CC_CHK(sh.ctl, gid < (uint32_t)sh.n_rows);
         r0 = sh.row_off[gid];
         len = sh.row_off[gid + 1] - r0;
     }
@@ -297,6 +299,7 @@ __device__ __forceinline__ void x_push(const cc_shard& sh, long long t, uint32_t
     while (m) {
         const int d = __ffs(m) - 1;
         m &= m - 1;
+        CC_CHK(sh.ctl, d < sh.n_ranks && sh.xdst[d].flag[0] != 0);
         const cc_xpeer& X = sh.xdst[d];
         x_pushed_block() = 1;
         const unsigned o = atomicAdd(&sh.xcnt[d], 1u);
@@ -310,7 +313,9 @@ __device__ __forceinline__ void x_push(const cc_shard& sh, long long t, uint32_t
 
 __device__ __forceinline__ Ev make_rec_event(const cc_shard& sh, uint64_t rec, int t_mod_l) {
     const uint32_t ref = (uint32_t)rec >> 5;                 // low 5 bits: lane in group
+    CC_CHK(sh.ctl, ref < (uint32_t)(sh.log_slots * sh.spk_cap));
     const int e = (int)(ref >> (31 - __clz(sh.spk_cap)));      // spk_cap is a power of two
+    CC_CHK(sh.ctl, (ref & (sh.spk_cap - 1)) < sh.log_ctr[e]);   // a logged entry
     int d = t_mod_l - e;
     if (d <= 0) d += sh.log_slots;
     Ev ev;
@@ -505,6 +510,7 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
     const int li = li0 + lane;
     const uint32_t n = li < sh.n_local ? (uint32_t)sh.ev_n[li] : 0u;
     const uint32_t off = n ? (uint32_t)__ldcg(&sh.ev_off[li]) : 0u;
+    CC_CHK(sh.ctl, (unsigned long long)off + n <= (unsigned long long)sh.evrec_cap);
     uint32_t nmax = n;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
@@ -699,6 +705,7 @@ __device__ __forceinline__ void unit_desc(const cc_shard& sh, long long ta, cons
     st = 0; ln = 0; rf = 0;
     if (idx < s_n[kc]) {
         const int d = unit_delay(kc, sh.d_max);
+        CC_CHK(sh.ctl, d >= 1 && d <= sh.d_max && idx < (unsigned)sh.spk_cap);
         const int e = (int)pos_mod(ta - d, sh.log_slots);
         rf = (uint32_t)(e * sh.spk_cap + idx);
         const uint16_t* ds = sh.log_dseg + (size_t)rf * sh.seg_stride;
@@ -724,8 +731,10 @@ __device__ __forceinline__ void load_pass(const cc_shard& sh, uint64_t st, uint3
         const uint32_t j = (uint32_t)((p * U + u) * lps + sl);
         tg[u] = -1;
         if (j < ln) {
+            CC_CHK(sh.ctl, st + j < (uint64_t)sh.row_off[sh.n_rows]);
             tg[u] = __ldg(sh.syn_tgt + st + j);
             w[u] = __ldg(sh.syn_w + st + j);
+            CC_CHK(sh.ctl, tg[u] >= 0 && tg[u] < sh.n_local);
         }
     }
 }
@@ -747,6 +756,7 @@ __device__ __forceinline__ void deposit_pass(const cc_shard& sh, const ListSet& 
 #pragma unroll
     for (int k = 0; k < U; ++k) {
         key[k] = tg[k] >= 0 ? (unsigned)(tg[k] >> 5) : 0xffffffffu;
+        CC_CHK(sh.ctl, tg[k] < 0 || key[k] < (unsigned)sh.n_groups);
         const unsigned prev = __shfl_up_sync(0xffffffffu, key[k], 1);
         const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || key[k] != prev);
         lead[k] = 31 - __clz(heads & upto);
@@ -1161,6 +1171,7 @@ k_stage(const cc_shard sh) {
                     const int L = (int)((uint32_t)rec[u] & 31u);
                     if (L < l0 || L >= l1) continue;
                     const int dst = B.seg[L] + (int)atomicAdd(&B.hist[L], 1u);
+                    CC_CHK(ctl, dst >= B.seg[L] && dst < B.seg[L + 1] && dst < (int)rtot);
                     const Ev ev = make_rec_event(sh, rec[u], t_mod_l);
                     Et[dst] = ev.t; Es[dst] = ev.src; Ew[dst] = ev.w;
                     Eo[dst] = (uint8_t)L;
@@ -1225,6 +1236,7 @@ k_stage(const cc_shard sh) {
                 const int b = min(max(__double2int_rz((Et[e] - t0) * B.bsc[o]), 0),
                                   (int)(ck >> 16) - 1);
                 const uint32_t key = (ck & 0xffffu) + (uint32_t)b;
+                CC_CHK(ctl, key < nbt && nbt <= (uint32_t)HCAP);
                 Ek[e] = (key << 16) | atomicAdd(&B.hist[key], 1u);
             }
             __syncwarp();
@@ -1718,6 +1730,7 @@ __global__ void __launch_bounds__(256) k_xingest(const cc_shard sh) {
         double te = 0.0;
         if (v) {
             while (s_pre[s + 1] <= i) ++s;
+            CC_CHK(ctl, s < sh.n_ranks && s_rec[s] != nullptr && i - s_pre[s] < sh.xsrc[s].cap);
             const uint4 r = s_rec[s][i - s_pre[s]];
             gid = r.x;
             te = __longlong_as_double((long long)(((unsigned long long)r.z << 32) | r.y));

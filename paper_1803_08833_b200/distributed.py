@@ -501,7 +501,7 @@ class DistributedSimulator:
                 msg = (f"rank {arank} failed at step {astep} "
                        f"({_lib.decode_errors(abits)}); rank {self.rank} stopped with it")
             self.error = msg
-            raise _lib.EngineError(msg)
+            raise _lib.EngineError(msg, abits)
         self.sim.check(collect_raster)
 
     def advance(self, n_steps: int, collect_raster: bool = True) -> None:

@@ -148,7 +148,8 @@ class Simulator:
                  bin_cap: Optional[int] = None, chunk: int = 100,
                  use_graphs: bool = True, direct_log: Optional[bool] = None,
                  remote=None,
-                 raster_steps: Optional[int] = None, substeps: bool = False, device=None):
+                 raster_steps: Optional[int] = None, substeps: bool = False, device=None,
+                 capacity=None):
         import torch
         self.L = _lib.lib()
         self.torch = torch
@@ -180,24 +181,26 @@ class Simulator:
         spk_cap = 1 << (spk_cap - 1).bit_length()     # power of two: ref -> slot is a shift
         if spk_cap * (D + 1) >= 2 ** 32:
             raise MemoryBudgetError("spike log references exceed 32 bits")
-        ovf_cap = max(4096, n_local * 8)
+        # capacity = {"ovf", "scratch", "evrec"} multipliers of the buffers sized
+        # by expectation rather than by a hard bound (overflow list, spill staging,
+        # ordered-input records): run_b200 re-runs from t = 0 with the one that
+        # overflowed doubled (onset bursts fail within the first steps)
+        self.capacity = cap = dict(ovf=1, scratch=1, evrec=1, **(capacity or {}))
+        ovf_cap = max(4096, n_local * 8) * cap["ovf"]
         if spk_cap * (D + 1) >= 2 ** 27:
             raise MemoryBudgetError("spike log references exceed the 27 bits of a ring record")
         seg_stride = (D + 1 + 7) // 8 * 8
         dseg = net.delay_segments(D, seg_stride)
         raster_cap = max(1024, n_local * bound * max(self.chunk, raster_steps or 0))
-        # spill staging for onset bursts (neuron-steps with > NEURON_WCAP inputs, all
-        # of one step): the synchronous onset grows with the drive, so strongly
-        # driven runs (>= 10 drive events per neuron-step) get 4x the headroom
-        lam0 = cfg.external.mean_per_step(cfg.timestep_ms)
-        per_neuron = int(os.environ.get("CC_SCRATCH_PER_NEURON", "0")) or (256 if lam0 >= 10 else 64)
-        scratch_cap = max(1 << 16, n_local * per_neuron)
+        # spill staging (neuron-steps with > NEURON_WCAP inputs, all of one step)
+        per_neuron = int(os.environ.get("CC_SCRATCH_PER_NEURON", "64"))
+        scratch_cap = max(1 << 16, n_local * per_neuron) * cap["scratch"]
         # ordered-input records of one step: the expected list capacity of a step,
         # the overflow list and every neuron's Poisson budget (beyond it the
         # step fails with "event staging scratch exhausted")
         lam = cfg.external.mean_per_step(cfg.timestep_ms)
         ext_m = int(math.ceil(lam + 12.0 * math.sqrt(lam))) + 20 if lam > 0 else 0
-        evrec_cap = n_groups * step_cap + ovf_cap + n_local * ext_m
+        evrec_cap = (n_groups * step_cap + n_local * ext_m) * cap["evrec"] + ovf_cap
         self.buf = dict(
             gid=T.from_numpy(gids.astype(np.uint32).view(np.int32)).to(dev),
             state=T.zeros((n_local, 4), dtype=f64, device=dev),
@@ -346,7 +349,8 @@ class Simulator:
         self.torch.cuda.synchronize(self.dev)
         c = self.ctl()
         if c.error_bits:
-            raise _lib.EngineError(f"step {c.error_step}: {_lib.decode_errors(c.error_bits)}")
+            raise _lib.EngineError(f"step {c.error_step}: {_lib.decode_errors(c.error_bits)}",
+                                   int(c.error_bits))
         if c.raster_n:
             n = int(c.raster_n)
             if collect_raster:
@@ -471,7 +475,8 @@ class Simulator:
         cs.synchronize()
         c = _lib.Ctl.from_buffer_copy(self._snap_host[i].numpy().tobytes())
         if c.error_bits:
-            raise _lib.EngineError(f"step {c.error_step}: {_lib.decode_errors(c.error_bits)}")
+            raise _lib.EngineError(f"step {c.error_step}: {_lib.decode_errors(c.error_bits)}",
+                                   int(c.error_bits))
         n = int(c.raster_n)
         if n and collect_raster:
             rg, rt = self._rasters[i]
@@ -539,11 +544,26 @@ def run_b200(config, workers: int = 1, *, net: Optional[DeviceNetwork] = None, p
     if net is None:
         net = build_b200(config, device=device)
     n_steps = config.n_steps if steps is None else steps
-    sim = Simulator(config, net, probes=probes, probe_steps=n_steps, bin_cap=bin_cap,
-                    chunk=chunk, use_graphs=use_graphs, substeps=True, device=device)
-    torch.cuda.synchronize(sim.dev)
-    t0 = time.perf_counter()
-    sim.advance(n_steps)
+    capacity = None
+    while True:
+        sim = Simulator(config, net, probes=probes, probe_steps=n_steps, bin_cap=bin_cap,
+                        chunk=chunk, use_graphs=use_graphs, substeps=True, device=device,
+                        capacity=capacity)
+        torch.cuda.synchronize(sim.dev)
+        t0 = time.perf_counter()
+        try:
+            sim.advance(n_steps, collect_raster=getattr(config, "record_raster", True))
+        except _lib.EngineError as err:
+            # an expectation-sized buffer overflowed (e.g. a synchronous onset
+            # burst): the run is deterministic, so re-run it from t = 0 with that
+            # buffer doubled (up to 32x); hard bounds and protocol errors raise
+            capacity = _lib.grow_capacity(err, sim.capacity)
+            if capacity is None:
+                raise
+            del sim
+            torch.cuda.empty_cache()
+            continue
+        break
     wall = time.perf_counter() - t0
     c = sim.ctl()
     g, t = sim.raster()
@@ -559,4 +579,5 @@ def run_b200(config, workers: int = 1, *, net: Optional[DeviceNetwork] = None, p
         probe_state=ps, probe_v_end=pv,
         device_stats=dict(max_bin=int(c.max_bin), max_events=int(c.max_events),
                           spilled=int(c.spilled_total), overflow=int(c.ovf_total),
-                          bin_cap=sim.shard.bin_cap, device_bytes=sim.device_bytes))
+                          bin_cap=sim.shard.bin_cap, device_bytes=sim.device_bytes,
+                          capacity=dict(sim.capacity)))

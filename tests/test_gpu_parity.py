@@ -664,9 +664,76 @@ def test_decay_exponentials_within_one_ulp(cuda):
         ref = np.array([(math.exp if kind == 0 else math.expm1)(v) for v in x])
         d = np.abs(got.view(np.int64) - ref.view(np.int64))
         assert d.max() <= 1, (kind, x[np.argmax(d)])
-        frac = float(np.mean(d != 0))
-        if kind == 0:
-            npd = float(np.mean(np.exp(x).view(np.int64) != ref.view(np.int64)))
-            assert frac <= max(0.02, npd), (frac, npd)
-        else:
-            assert frac <= 0.02, frac
+        # (fexpm1's own range |x| <= 1/16; beyond it libdevice's expm1 answers)
+        m = np.ones(len(x), bool) if kind == 0 else np.abs(x) <= 0.0625
+        frac = float(np.mean(d[m] != 0))
+        npf = (np.exp if kind == 0 else np.expm1)(x[m])
+        npd = float(np.mean(npf.view(np.int64) != ref[m].view(np.int64)))
+        assert frac <= max(0.02, npd), (kind, frac, npd)
+
+
+_CHECKED_RUNS = """
+import json, os, sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, {root!r} + "/tests")
+import numpy as np
+from conftest import golden_run
+from paper_1803_08833_b200 import _lib
+from paper_1803_08833_b200.engine import run_b200
+from paper_1803_08833_b200.distributed import run_local_shards
+assert _lib.LIB_PATH.endswith("_chk.so")
+out = {{}}
+def same(r, meta, arr):
+    return bool(np.array_equal(r.raster_gids, arr["raster_gids"].astype(np.uint64))
+                and r.raster_checksum == meta["raster_checksum"]
+                and r.recurrent_events == meta["recurrent_events"]
+                and r.external_events == meta["external_events"])
+for name in ("tiny_gauss", "tiny_exp", "config0_cal_0p1"):
+    cfg, meta, arr = golden_run(name)
+    probes = arr["probe_ids"] if "probe_ids" in arr.files else None
+    out[name] = same(run_b200(cfg, 1, probes=probes, chunk=13), meta, arr)
+cfg, meta, arr = golden_run("tiny_gauss_long")
+for flags in ("4096", "32768"):
+    os.environ["CC_FLAGS"] = flags
+    out["tiny_gauss_long/" + flags] = same(run_b200(cfg, 1), meta, arr)
+os.environ["CC_FLAGS"] = "0"
+out["overflow"] = same(run_b200(cfg, 1, bin_cap=2), meta, arr)
+cfg, meta, arr = golden_run("tiny_gauss")
+out["p2p_local_3"] = same(run_local_shards(cfg, 3, transport="p2p"), meta, arr)
+out["slots_local_4"] = same(run_local_shards(cfg, 4), meta, arr)
+# a planted bad access is caught: the CSR row bound shrunk below the gids in use
+print("NEGATIVE_CASE", flush=True)
+from paper_1803_08833_b200.engine import Simulator
+from paper_1803_08833_b200.network import build_b200
+sim = Simulator(cfg, build_b200(cfg), use_graphs=False)
+sim.shard.n_rows = 10
+try:
+    sim.advance(cfg.n_steps)
+    out["negative"] = False
+except _lib.EngineError as err:
+    out["negative"] = "checked build" in str(err)
+print(json.dumps(out))
+"""
+
+
+def test_checked_build_bounds_and_protocol(cuda):
+    """The checked build (libcorticarc_b200_chk.so: bounds and protocol
+    assertions on CSR, spike-log, list, staging, record and exchange indices)
+    runs the golden cases through every delivery / planning / overflow /
+    exchange path with no failed check and the reference's results.  (Stands
+    in for compute-sanitizer, which is closed on this GPU pool.)"""
+    import json
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    lib = os.path.join(ROOT, "paper_1803_08833_b200", "libcorticarc_b200_chk.so")
+    assert os.path.exists(lib), "run __graft_entry__.build() (builds the test variants)"
+    r = subprocess.run([sys.executable, "-c", _CHECKED_RUNS.format(root=ROOT)],
+                       env={**os.environ, "CC_LIB_PATH": lib}, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-3000:])
+    before, _, after = r.stdout.partition("NEGATIVE_CASE")
+    assert "cc check failed" not in before, before[-2000:]
+    assert "cc check failed" in after            # the planted bad access is reported
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert all(out.values()), out

@@ -57,3 +57,22 @@ def test_library_is_sm100a():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_capacity_retry_policy():
+    """Only overflows of the expectation-sized buffers trigger a re-run, each
+    doubling the buffer that overflowed, up to a limit; EngineError keeps its
+    bits across processes (pickling)."""
+    import pickle
+    from paper_1803_08833_b200 import _lib
+    cap = dict(ovf=1, scratch=1, evrec=1)
+    e = _lib.EngineError("step 3: event staging scratch exhausted", 0x08)
+    assert _lib.capacity_error(e)
+    assert _lib.grow_capacity(e, cap) == dict(ovf=1, scratch=2, evrec=1)
+    both = _lib.EngineError("x", 0x08 | 0x100)
+    assert _lib.grow_capacity(both, cap) == dict(ovf=1, scratch=2, evrec=2)
+    assert _lib.grow_capacity(e, dict(cap, scratch=32)) is None          # at the limit
+    for bits in (0x01, 0x20, 0x08 | 0x20, 0x400, 0x1000, 0):
+        assert _lib.grow_capacity(_lib.EngineError("x", bits), cap) is None
+    back = pickle.loads(pickle.dumps(e))
+    assert isinstance(back, _lib.EngineError) and back.bits == 0x08 and str(back) == str(e)
