@@ -409,8 +409,10 @@ def _bench_single(args, cfg, net, capacity):
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            prof_d = json.load(open(prof)).get(f"config{args.config}", {})
-            traffic = prof_d.get("k_deliver", {}).get("dram_bytes_per_launch")
+            key = f"config{args.config}" + ("" if args.regime == "calibrated" else f"_{args.regime}")
+            prof_d = json.load(open(prof)).get(key, {})
+            # the roofline kernel is replay (b)'s k_deliver: its ncu DRAM bytes
+            traffic = prof_d.get("k_deliver_b", {}).get("dram_bytes_per_launch")
             stage_ncu = prof_d.get("k_stage", {})
         except Exception:
             traffic = None
@@ -448,6 +450,9 @@ def _bench_single(args, cfg, net, capacity):
                      "units": "events k_deliver deposited x 17 B / its average launch time, "
                               "replay (b) with every arrival delivered by k_deliver",
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                     "traffic_source": "profiles/ncu_summary.json: dram__bytes_read.sum + "
+                                       "dram__bytes_write.sum of one replay-(b) k_deliver "
+                                       "launch (ncu --set full)",
                      "peak_source": peak_src,
                      "bytes_per_event": BYTES_PER_EVENT},
         "dominant_kernel": {

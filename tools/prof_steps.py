@@ -29,8 +29,19 @@ if a.grid:
     nx, ny = (int(v) for v in a.grid.split("x"))
     cfg = replace(cfg, grid=replace(cfg.grid, nx=nx, ny=ny))
 net = build_b200(cfg)
-sim = Simulator(cfg, net, chunk=100)
-sim.advance(a.warmup)
+from paper_1803_08833_b200 import _lib  # noqa: E402
+capacity = None
+while True:                      # onset bursts: grow the overflowed buffer (run_b200's policy)
+    sim = Simulator(cfg, net, chunk=100, capacity=capacity)
+    try:
+        sim.advance(a.warmup)
+        break
+    except _lib.EngineError as err:
+        capacity = _lib.grow_capacity(err, sim.capacity)
+        if capacity is None:
+            raise
+        del sim
+        torch.cuda.empty_cache()
 sim.shard.flags = a.flags
 s = torch.cuda.current_stream().cuda_stream
 torch.cuda.synchronize()
