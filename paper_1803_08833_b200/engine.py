@@ -185,7 +185,7 @@ class Simulator:
         # by expectation rather than by a hard bound (overflow list, spill staging,
         # ordered-input records): run_b200 re-runs from t = 0 with the one that
         # overflowed doubled (onset bursts fail within the first steps)
-        self.capacity = cap = dict(ovf=1, scratch=1, evrec=1, **(capacity or {}))
+        self.capacity = cap = {"ovf": 1, "scratch": 1, "evrec": 1, **(capacity or {})}
         ovf_cap = max(4096, n_local * 8) * cap["ovf"]
         if spk_cap * (D + 1) >= 2 ** 27:
             raise MemoryBudgetError("spike log references exceed the 27 bits of a ring record")
