@@ -324,7 +324,7 @@ def bench_single(args):
         except _lib.EngineError as err:
             # an expectation-sized buffer overflowed (onset burst of a strongly
             # driven config): measure again from t = 0 with it doubled
-            capacity = _lib.grow_capacity(err, dict(ovf=1, scratch=1, evrec=1, **capacity))
+            capacity = _lib.grow_capacity(err, {**dict(ovf=1, scratch=1, evrec=1), **capacity})
             if capacity is None:
                 raise
             torch.cuda.empty_cache()
@@ -473,7 +473,9 @@ def _bench_single(args, cfg, net, capacity):
                           "definition": "recurrent events/s x 17 B over the whole step "
                                         "(BASELINE.md roofline formula)"},
         "kernels": kernels,
-        "gpu_launches": int(L.cc_kernels_per_step(sim.shard.n_groups)) * K,
+        "gpu_launches": int(L.cc_kernels_per_step(C.byref(sim.shard))) * K,
+        "stage_grid": {"warps": int(L.cc_stage_warps(sim.shard.d_max)),
+                       "what": "k_stage's persistent grid (resident warps, 4 per block)"},
         "clocks": clk,
         "construction_s": net.construction_seconds,
         "bytes_per_synapse_steady": net.steady_bytes / max(1, net.n_synapses),

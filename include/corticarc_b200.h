@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 25
+#define CC_ABI_VERSION 26
 
 /* Work items are queued in this many size classes, largest first. */
 /* Input lists per 32-neuron group (events of delay d go to sub-list
@@ -326,9 +326,13 @@ int cc_xwin_free(void* ptr);
 /* CC_SUBLISTS as compiled (hosts size bin_cnt / bin_rec / grp_sub with it). */
 int32_t cc_sublists(void);
 
-/* Kernels cc_deliver + cc_neuron_step launch per step for a shard of n_groups
- * 32-neuron groups (3, or 2 when the planning runs inside k_stage). */
-int32_t cc_kernels_per_step(int32_t n_groups);
+/* Kernels cc_deliver + cc_neuron_step launch per step for this shard: 3
+ * (k_deliver, k_plan, k_stage), 2 when the planning runs inside k_stage. */
+int32_t cc_kernels_per_step(const cc_shard* sh);
+
+/* Warps of k_stage's persistent grid for a shard with this d_max (SM count x
+ * resident blocks per SM x warps per block). */
+int32_t cc_stage_warps(int32_t d_max);
 
 /* Delay-segment table of a CSR whose rows are sorted by delay: out[r][d] =
  * synapses of row r with delay <= d, d = 0..d_max (u16, row stride `stride`).

@@ -15,8 +15,9 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "XPeer", "check", "EngineError",
 
 LIB_PATH = os.environ.get("CC_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 25
+ABI_VERSION = 26
 ITEM_CLASSES = 8
+FLAG_NO_TAIL_DELIVERY = 0x1000   # CC_FLAG_NO_TAIL_DELIVERY (include/corticarc_b200.h)
 CNT_STRIDE_MAX = 64          # bin_cnt words per group allocated (CC_CNT_STRIDE <= this)
 
 ERR_BITS = {
@@ -152,7 +153,8 @@ _SIGS = {
     "cc_xwin_close": (C.c_int, [_P]),
     "cc_xwin_free": (C.c_int, [_P]),
     "cc_sublists": (C.c_int32, []),
-    "cc_kernels_per_step": (C.c_int32, [C.c_int32]),
+    "cc_kernels_per_step": (C.c_int32, [_P]),
+    "cc_stage_warps": (C.c_int32, [C.c_int32]),
     "cc_csr_checksum": (C.c_int, [_P, _P, C.c_int64, _P, _P, _P, C.c_int32, C.c_int32, _P, _P]),
     "cc_test_philox": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_int32,
                                  _P, _P]),

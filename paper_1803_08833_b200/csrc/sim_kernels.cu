@@ -17,6 +17,7 @@
 // follows the reference's evaluation order; the file is compiled with
 // -fmad=false so no multiply-add is contracted.
 #include <climits>
+#include <type_traits>
 #include "cc_common.cuh"
 
 // cache-policy experiments (tools/sweep_variants.py): evict-first CSR loads in
@@ -58,6 +59,15 @@ struct Ev {                              // one input event, 16 B
 __device__ __forceinline__ long long pos_mod(long long a, long long m) {
     long long r = a % m;
     return r < 0 ? r + m : r;
+}
+
+// (t_mod + delta) mod L for |delta| <= L, given t_mod = t mod L: the log slot
+// of step t + delta without a 64-bit modulo at every use.
+__device__ __forceinline__ int slot_add(int t_mod, int delta, int L) {
+    int e = t_mod + delta;
+    if (e < 0) e += L;
+    else if (e >= L) e -= L;
+    return e;
 }
 
 // a / b, correctly rounded, for a constant divisor with rb = RN(1/b) (host
@@ -212,17 +222,18 @@ struct SubMap {
 // Append one spike to the log slot of emission step t: time, gid, row start
 // and the row's delay-segment offsets (the delay-d part of its row is
 // delivered in step t + d).  len == 0: no synapse on this shard.
-__device__ __forceinline__ void log_spike(const cc_shard& sh, long long t, uint32_t gid,
-                                          double te) {
+// Returns the entry's reference (slot * spk_cap + index), CC_NO_REF if none.
+constexpr uint32_t CC_NO_REF = 0xffffffffu;
+__device__ __forceinline__ uint32_t log_spike(const cc_shard& sh, long long t, int e, uint32_t gid,
+                                              double te) {
     CC_CHK(sh.ctl, gid < (uint32_t)sh.n_rows);
     const int64_t r0 = sh.row_off[gid];
     const int64_t len = sh.row_off[gid + 1] - r0;
-    if (len == 0) return;
-    const int e = (int)pos_mod(t, sh.log_slots);
+    if (len == 0) return CC_NO_REF;
     const unsigned long long idx = atomicAdd(&sh.log_ctr[e], 1ull);
     if (idx >= (unsigned long long)sh.spk_cap) {
         cc_raise(sh.ctl, CC_ERR_SPIKE_LOG, t);
-        return;
+        return CC_NO_REF;
     }
     atomicAdd(&sh.log_len[e], (unsigned long long)len);
     const uint32_t ref = (uint32_t)(e * sh.spk_cap + idx);
@@ -232,11 +243,12 @@ __device__ __forceinline__ void log_spike(const cc_shard& sh, long long t, uint3
     const uint4* src = reinterpret_cast<const uint4*>(sh.dseg + (size_t)gid * sh.seg_stride);
     uint4* dst = reinterpret_cast<uint4*>(sh.log_dseg + (size_t)ref * sh.seg_stride);
     for (int j = 0; j < sh.seg_stride / 8; ++j) dst[j] = src[j];
+    return ref;
 }
 
 // Warp-wide log_spike for received spikes (every lane calls; `valid` lanes
 // carry a spike): one reservation atomic per warp instead of one per spike.
-__device__ __forceinline__ void log_spike_warp(const cc_shard& sh, long long t, bool valid,
+__device__ __forceinline__ void log_spike_warp(const cc_shard& sh, long long t, int e, bool valid,
                                                uint32_t gid, double te) {
     const int lane = threadIdx.x & 31;
     int64_t r0 = 0, len = 0;
@@ -251,7 +263,6 @@ __device__ __forceinline__ void log_spike_warp(const cc_shard& sh, long long t, 
     unsigned long long lsum = has ? (unsigned long long)len : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-    const int e = (int)pos_mod(t, sh.log_slots);
     const int leader = __ffs(b) - 1;
     unsigned long long base = 0;
     if (lane == leader) {
@@ -356,7 +367,10 @@ constexpr int STAGE_WARPS = CC_STAGE_WARPS;
 // Sort buckets per work item: neuron L gets NB_L = min(2 n_L, 352 n_L / rtot + 1)
 // buckets (0 if it has no input), so sum NB_L <= HCAP and a bucket holds ~0.5
 // inputs on average.
-constexpr int HCAP = 384;
+#ifndef CC_HCAP
+#define CC_HCAP 280
+#endif
+constexpr int HCAP = CC_HCAP;
 
 struct StageBuf {
     double* t; double* o_last; double* o_ru; double* bsc;
@@ -368,6 +382,12 @@ struct StageBuf {
 __host__ __device__ constexpr size_t stage_warp_bytes() {
     return ((size_t)NEURON_WCAP * (8 + 4 + 4 + 4 + 2 + 2 + 1 + 1) + HCAP * 4 + 34 * 4
             + 32 * (8 + 8 + 8 + 4 + 4) + 32 + 15) / 16 * 16;     // 16 B aligned per warp
+}
+
+// dynamic shared memory of k_stage behind the warps' buffers: the tail
+// delivery's unit tables a_n[d_max], a_pre[d_max + 1]
+static inline size_t stage_tail_bytes(int d_max) {
+    return ((size_t)(2 * d_max + 1) * 4 + 15) / 16 * 16;
 }
 
 __device__ __forceinline__ StageBuf carve(char* p) {
@@ -422,7 +442,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // Timing probes (tools/*_timeline.py; compiled only with -DCC_TIMING_PROBES=1):
 // flags & 32: per work item of k_stage, 8 timestamps
-// {claim, gathered, sorted, factors, updated, sm, rtot, warp} written to the
+// {claim, gathered, sorted, factors, updated, update start (0: none), rtot, warp} written to the
 // tail of the scratch buffer.
 #define CC_DBG(slot_i, val)                                                              \
     do {                                                                                 \
@@ -474,166 +494,6 @@ __device__ __forceinline__ bool slow_step(NState& s, const cc_pop& P, double tj,
     return false;
 }
 
-// In-order update of the 32 neurons of one group (NeuronBlock.integrate_sorted,
-// model.py:289-337), one lane per neuron: affine update, jump, strict
-// threshold, reset, refractory discard, spike emission.  The factors assume the
-// step-start refractory window; after a spike they are recomputed in line
-// (slow_step).  The ordered 48 B records {t, w}, {em, ec}, {f, ecr} reach the
-// warp's (idle) shared buffer by cp.async (L2 only): CC_UPD_NBUF batches of
-// one input per neuron each are in flight while one is applied, so a
-// neuron's serial chain does not wait for an L2 round trip per input (1 input
-// x 3 buffers: 97.2 -> 94.3 us per step at config 1; the single-buffer
-// fallback, 5 inputs per round trip, serves builds whose buffer is too small).
-constexpr int UB = stage_warp_bytes() / (32 * 48) < 5 ? (int)(stage_warp_bytes() / (32 * 48))
-                                                        : 5;    // inputs per neuron per batch
-constexpr int UB_STRIDE = 3 * UB;        // double2 per lane: 15 = 7 mod 8, conflict-free
-static_assert(32 * UB_STRIDE * 16 <= stage_warp_bytes(), "update batch > stage buffer");
-#ifndef CC_UPD_PIPE
-#define CC_UPD_PIPE 1        // update: CC_UPD_NBUF single-input batches in flight
-#endif
-#ifndef CC_UPD_NBUF
-#define CC_UPD_NBUF 3
-#endif
-static_assert(!CC_UPD_PIPE || CC_UPD_NBUF * 32 * 3 * 16 <= (int)stage_warp_bytes(),
-              "update pipeline > stage buffer");
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
-}
-
-__device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long long t,
-                                             double2* S, uint32_t& my_spikes,
-                                             const double2* xt) {
-    cc_ctl* ctl = sh.ctl;
-    const int lane = threadIdx.x & 31;
-    const int li = li0 + lane;
-    const uint32_t n = li < sh.n_local ? (uint32_t)sh.ev_n[li] : 0u;
-    const uint32_t off = n ? (uint32_t)__ldcg(&sh.ev_off[li]) : 0u;
-    CC_CHK(sh.ctl, (unsigned long long)off + n <= (unsigned long long)sh.evrec_cap);
-    uint32_t nmax = n;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
-    const double2* R = reinterpret_cast<const double2*>(sh.evrec);
-    uint32_t gid = 0;
-    const cc_pop* P = &sh.pop[0];
-    double* st = sh.state + (size_t)(n ? li : 0) * 4;
-    NState s{0.0, 0.0, 0.0, 0.0};
-    if (n) {
-        gid = sh.gid[li];
-        P = &sh.pop[neuron_pop(sh, gid)];
-        const double2 a0 = reinterpret_cast<const double2*>(st)[0];
-        const double2 a1 = reinterpret_cast<const double2*>(st)[1];
-        s = NState{a0.x, a0.y, a1.x, a1.y};
-    }
-    const bool cflag = s.c != 0.0;
-    bool stale = false;                      // spiked: factors need recomputing
-#if CC_UPD_PIPE
-    // CC_UPD_NBUF single-input buffers per lane in flight: input i+NBUF is
-    // loading while input i is applied (cp.async groups, wait_group NBUF-1);
-    // rotating buffer indices, one 48 B slot per lane and buffer
-    double2* const sb = S + lane * 3;
-    constexpr int BS = 32 * 3;                   // double2 per buffer
-    const double2* Rp = R + 3 * (size_t)off;     // next record of this lane to fetch
-    uint32_t jn = 0;                             // its input index
-    int bn = 0, bi = 0;                          // buffer to fill next / to apply
-    auto issue = [&]() {
-        if (jn < n) {
-            double2* d = sb + bn * BS;
-            cp_async16(d, Rp);
-            cp_async16(d + 1, Rp + 1);
-            cp_async16(d + 2, Rp + 2);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        Rp += 3;
-        ++jn;
-        bn = bn + 1 == CC_UPD_NBUF ? 0 : bn + 1;
-    };
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < CC_UPD_NBUF; ++j) issue();
-    // (each lane copies into and reads only its own slots, and cp.async waits
-    // are per thread: no warp barrier inside the loop)
-    for (uint32_t b0 = 0; b0 < nmax; ++b0) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(CC_UPD_NBUF - 1) : "memory");
-        const double2* my = sb + bi * BS;
-        bi = bi + 1 == CC_UPD_NBUF ? 0 : bi + 1;
-        const uint32_t e = min(n, b0 + 1u);
-#else
-    const double2* my = S + lane * UB_STRIDE;
-    for (uint32_t b0 = 0; b0 < nmax; b0 += UB) {
-        __syncwarp();                        // previous batch consumed
-        {
-            const double2* Rn = R + 3 * (size_t)(off + b0);
-            const uint32_t m = n > b0 ? min(n - b0, (uint32_t)UB) : 0u;
-#pragma unroll
-            for (int k = 0; k < UB; ++k) {
-                if ((uint32_t)k < m) {
-                    cp_async16(S + lane * UB_STRIDE + 3 * k, Rn + 3 * k);
-                    cp_async16(S + lane * UB_STRIDE + 3 * k + 1, Rn + 3 * k + 1);
-                    cp_async16(S + lane * UB_STRIDE + 3 * k + 2, Rn + 3 * k + 2);
-                }
-            }
-        }
-        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-        __syncwarp();
-        const uint32_t e = min(n, b0 + (uint32_t)UB);
-#endif
-        for (uint32_t i = b0; i < e; ++i) {
-            const double2 r0 = my[3 * (i - b0)], r1 = my[3 * (i - b0) + 1],
-                          r2 = my[3 * (i - b0) + 2];
-            const double tj = r0.x, wv = r0.y, em = r1.x, ec = r1.y, f = r2.x, ecr = r2.y;
-            bool spike = false;
-            if (!stale && s.ru <= s.last) {
-                // fast path (no refractory window involved, factors valid):
-                // free_from == last, V_s == V, not refractory; ec = 1, f = 0 when
-                // the neuron started the step without fatigue (c stays 0 then)
-                double Vt = P->E + (s.V - P->E) * em;
-                if (s.c != 0.0) {
-                    Vt = Vt - P->sfa * s.c * f;
-                    s.c = s.c * ec;
-                }
-                s.last = tj;
-                const double V = Vt + wv;
-                if (V > P->V_theta) spike = true; else s.V = V;
-            } else {
-                spike = slow_step(s, *P, tj, stale, cflag, em, ec, f, ecr, wv, xt);
-            }
-            if (spike) {                             // strict threshold crossed
-                s.V = P->V_r;
-                s.c = s.c + P->alpha_c;
-                s.ru = tj + P->tau_arp;
-                stale = true;
-                ++my_spikes;
-                if (sh.direct_log) log_spike(sh, t, gid, tj);
-                if (sh.xdst) {                               // peer exchange: push now
-                    const uint32_t xm = sh.xmask[li];
-                    if (xm) x_push(sh, t, xm, gid, tj);
-                }
-                if ((!sh.direct_log && !sh.xdst) || (sh.remote && sh.remote[li])) {   // out-list
-                    const unsigned o = atomicAdd(&ctl->out_n, 1u);
-                    if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = tj; }
-                    else cc_raise(ctl, CC_ERR_OUTLIST, t);
-                }
-                const unsigned long long rr = atomicAdd(&ctl->raster_n, 1ull);
-                if (rr < (unsigned long long)sh.raster_cap) {
-                    sh.raster_gid[rr] = gid;
-                    sh.raster_t[rr] = tj;
-                } else {
-                    cc_raise(ctl, CC_ERR_RASTER, t);
-                }
-            }
-        }
-#if CC_UPD_PIPE
-        issue();
-#endif
-    }
-    if (n) {
-        reinterpret_cast<double2*>(st)[0] = make_double2(s.V, s.c);
-        reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
-    }
-}
-
 // ------------------------------------------------------------ delivery
 // A work unit is (delay d, 4 consecutive spikes of log slot t - d); each spike's
 // delay-d segment is walked by 8 lanes, U synapses per lane per pass.  Records
@@ -672,7 +532,7 @@ __device__ __forceinline__ int unit_delay(int k, int D) { return k < D - 1 ? k +
 
 // Block-wide (barriers): s_n[k] spikes of log slot ta - d(k), s_pre the unit
 // prefix over positions k < nk.
-__device__ __forceinline__ void unit_prefix(const cc_shard& sh, long long ta, int nk,
+__device__ __forceinline__ void unit_prefix(const cc_shard& sh, int ta_mod, int nk,
                                             unsigned* s_n, unsigned* s_pre) {
     if (threadIdx.x < 32) {                  // warp 0: loads and a shuffle scan, 32 at a time
         const int lane = threadIdx.x;
@@ -681,7 +541,8 @@ __device__ __forceinline__ void unit_prefix(const cc_shard& sh, long long ta, in
             const int k = k0 + lane;
             unsigned n = 0;
             if (k < nk)
-                n = (unsigned)min(sh.log_ctr[pos_mod(ta - unit_delay(k, sh.d_max), sh.log_slots)],
+                n = (unsigned)min(sh.log_ctr[slot_add(ta_mod, -unit_delay(k, sh.d_max),
+                                                      sh.log_slots)],
                                   (unsigned long long)sh.spk_cap);
             const unsigned units = (n + (32u >> sh.del_lps_log2) - 1) >> (5 - sh.del_lps_log2);
             unsigned tot;
@@ -697,7 +558,7 @@ __device__ __forceinline__ void unit_prefix(const cc_shard& sh, long long ta, in
 // This lane's spike of unit u (< s_pre[nk]) of arrival step ta: segment start,
 // length and log reference; kc is the caller's position cursor (its units
 // only increase).
-__device__ __forceinline__ void unit_desc(const cc_shard& sh, long long ta, const unsigned* s_n,
+__device__ __forceinline__ void unit_desc(const cc_shard& sh, int ta_mod, const unsigned* s_n,
                                           const unsigned* s_pre, unsigned u, int& kc,
                                           uint64_t& st, uint32_t& ln, uint32_t& rf) {
     while (s_pre[kc + 1] <= u) ++kc;
@@ -706,7 +567,7 @@ __device__ __forceinline__ void unit_desc(const cc_shard& sh, long long ta, cons
     if (idx < s_n[kc]) {
         const int d = unit_delay(kc, sh.d_max);
         CC_CHK(sh.ctl, d >= 1 && d <= sh.d_max && idx < (unsigned)sh.spk_cap);
-        const int e = (int)pos_mod(ta - d, sh.log_slots);
+        const int e = slot_add(ta_mod, -d, sh.log_slots);
         rf = (uint32_t)(e * sh.spk_cap + idx);
         const uint16_t* ds = sh.log_dseg + (size_t)rf * sh.seg_stride;
         const uint32_t a = __ldg(ds + d - 1), b = __ldg(ds + d);
@@ -1003,9 +864,172 @@ __device__ __noinline__ void x_publish(const cc_xpeer* xdst, uint32_t* xcnt, int
     if (sent) ctl->x_sent += sent;
 }
 
+// In-order update of the 32 neurons of one group (NeuronBlock.integrate_sorted,
+// model.py:289-337), one lane per neuron: affine update, jump, strict
+// threshold, reset, refractory discard, spike emission.  The factors assume the
+// step-start refractory window; after a spike they are recomputed in line
+// (slow_step).  The ordered 48 B records {t, w}, {em, ec}, {f, ecr} reach the
+// warp's (idle) shared buffer by cp.async (L2 only): CC_UPD_NBUF batches of
+// one input per neuron each are in flight while one is applied, so a
+// neuron's serial chain does not wait for an L2 round trip per input (1 input
+// x 3 buffers: 97.2 -> 94.3 us per step at config 1; the single-buffer
+// fallback, 5 inputs per round trip, serves builds whose buffer is too small).
+constexpr int UB = stage_warp_bytes() / (32 * 48) < 5 ? (int)(stage_warp_bytes() / (32 * 48))
+                                                        : 5;    // inputs per neuron per batch
+constexpr int UB_STRIDE = 3 * UB;        // double2 per lane: 15 = 7 mod 8, conflict-free
+static_assert(32 * UB_STRIDE * 16 <= stage_warp_bytes(), "update batch > stage buffer");
+#ifndef CC_UPD_PIPE
+#define CC_UPD_PIPE 1        // update: CC_UPD_NBUF single-input batches in flight
+#endif
+#ifndef CC_UPD_NBUF
+#define CC_UPD_NBUF 3
+#endif
+static_assert(!CC_UPD_PIPE || CC_UPD_NBUF * 32 * 3 * 16 <= (int)stage_warp_bytes(),
+              "update pipeline > stage buffer");
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+__device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long long t, int e_t,
+                                             double2* S, uint32_t& my_spikes,
+                                             const double2* xt) {
+    cc_ctl* ctl = sh.ctl;
+    const int lane = threadIdx.x & 31;
+    const int li = li0 + lane;
+    const uint32_t n = li < sh.n_local ? (uint32_t)sh.ev_n[li] : 0u;
+    const uint32_t off = n ? (uint32_t)__ldcg(&sh.ev_off[li]) : 0u;
+    CC_CHK(sh.ctl, (unsigned long long)off + n <= (unsigned long long)sh.evrec_cap);
+    uint32_t nmax = n;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+    const double2* R = reinterpret_cast<const double2*>(sh.evrec);
+    uint32_t gid = 0;
+    const cc_pop* P = &sh.pop[0];
+    double* st = sh.state + (size_t)(n ? li : 0) * 4;
+    NState s{0.0, 0.0, 0.0, 0.0};
+    if (n) {
+        gid = sh.gid[li];
+        P = &sh.pop[neuron_pop(sh, gid)];
+        const double2 a0 = reinterpret_cast<const double2*>(st)[0];
+        const double2 a1 = reinterpret_cast<const double2*>(st)[1];
+        s = NState{a0.x, a0.y, a1.x, a1.y};
+    }
+    const bool cflag = s.c != 0.0;
+    bool stale = false;                      // spiked: factors need recomputing
+#if CC_UPD_PIPE
+    // CC_UPD_NBUF single-input buffers per lane in flight: input i+NBUF is
+    // loading while input i is applied (cp.async groups, wait_group NBUF-1);
+    // rotating buffer indices, one 48 B slot per lane and buffer
+    double2* const sb = S + lane * 3;
+    constexpr int BS = 32 * 3;                   // double2 per buffer
+    const double2* Rp = R + 3 * (size_t)off;     // next record of this lane to fetch
+    uint32_t jn = 0;                             // its input index
+    int bn = 0, bi = 0;                          // buffer to fill next / to apply
+    auto issue = [&]() {
+        if (jn < n) {
+            double2* d = sb + bn * BS;
+            cp_async16(d, Rp);
+            cp_async16(d + 1, Rp + 1);
+            cp_async16(d + 2, Rp + 2);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        Rp += 3;
+        ++jn;
+        bn = bn + 1 == CC_UPD_NBUF ? 0 : bn + 1;
+    };
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < CC_UPD_NBUF; ++j) issue();
+    // (each lane copies into and reads only its own slots, and cp.async waits
+    // are per thread: no warp barrier inside the loop)
+    for (uint32_t b0 = 0; b0 < nmax; ++b0) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(CC_UPD_NBUF - 1) : "memory");
+        const double2* my = sb + bi * BS;
+        bi = bi + 1 == CC_UPD_NBUF ? 0 : bi + 1;
+        const uint32_t e = min(n, b0 + 1u);
+#else
+    const double2* my = S + lane * UB_STRIDE;
+    for (uint32_t b0 = 0; b0 < nmax; b0 += UB) {
+        __syncwarp();                        // previous batch consumed
+        {
+            const double2* Rn = R + 3 * (size_t)(off + b0);
+            const uint32_t m = n > b0 ? min(n - b0, (uint32_t)UB) : 0u;
+#pragma unroll
+            for (int k = 0; k < UB; ++k) {
+                if ((uint32_t)k < m) {
+                    cp_async16(S + lane * UB_STRIDE + 3 * k, Rn + 3 * k);
+                    cp_async16(S + lane * UB_STRIDE + 3 * k + 1, Rn + 3 * k + 1);
+                    cp_async16(S + lane * UB_STRIDE + 3 * k + 2, Rn + 3 * k + 2);
+                }
+            }
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        const uint32_t e = min(n, b0 + (uint32_t)UB);
+#endif
+        for (uint32_t i = b0; i < e; ++i) {
+            const double2 r0 = my[3 * (i - b0)], r1 = my[3 * (i - b0) + 1],
+                          r2 = my[3 * (i - b0) + 2];
+            const double tj = r0.x, wv = r0.y, em = r1.x, ec = r1.y, f = r2.x, ecr = r2.y;
+            bool spike = false;
+            if (!stale && s.ru <= s.last) {
+                // fast path (no refractory window involved, factors valid):
+                // free_from == last, V_s == V, not refractory; ec = 1, f = 0 when
+                // the neuron started the step without fatigue (c stays 0 then)
+                double Vt = P->E + (s.V - P->E) * em;
+                if (s.c != 0.0) {
+                    Vt = Vt - P->sfa * s.c * f;
+                    s.c = s.c * ec;
+                }
+                s.last = tj;
+                const double V = Vt + wv;
+                if (V > P->V_theta) spike = true; else s.V = V;
+            } else {
+                spike = slow_step(s, *P, tj, stale, cflag, em, ec, f, ecr, wv, xt);
+            }
+            if (spike) {                             // strict threshold crossed
+                s.V = P->V_r;
+                s.c = s.c + P->alpha_c;
+                s.ru = tj + P->tau_arp;
+                stale = true;
+                ++my_spikes;
+                if (sh.direct_log) log_spike(sh, t, e_t, gid, tj);
+                if (sh.xdst) {                               // peer exchange: push now
+                    const uint32_t xm = sh.xmask[li];
+                    if (xm) x_push(sh, t, xm, gid, tj);
+                }
+                if ((!sh.direct_log && !sh.xdst) || (sh.remote && sh.remote[li])) {   // out-list
+                    const unsigned o = atomicAdd(&ctl->out_n, 1u);
+                    if (o < (unsigned)sh.out_cap) { sh.out_gid[o] = gid; sh.out_t[o] = tj; }
+                    else cc_raise(ctl, CC_ERR_OUTLIST, t);
+                }
+                const unsigned long long rr = atomicAdd(&ctl->raster_n, 1ull);
+                if (rr < (unsigned long long)sh.raster_cap) {
+                    sh.raster_gid[rr] = gid;
+                    sh.raster_t[rr] = tj;
+                } else {
+                    cc_raise(ctl, CC_ERR_RASTER, t);
+                }
+            }
+        }
+#if CC_UPD_PIPE
+        issue();
+#endif
+    }
+    if (n) {
+        reinterpret_cast<double2*>(st)[0] = make_double2(s.V, s.c);
+        reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
+    }
+}
+
 // Phase A proper: persistent warps claim work items from the queue.
+// 6 blocks of 4 warps per SM: 80 registers per thread (no spills) and, with
+// HCAP 288, 9,008 B of staging buffer per warp.  24 instead of 20 resident
+// warps: config 1 -1.5 %, config 3 and the 33 Hz stress point -6 % per step.
 #ifndef CC_STAGE_MINB
-#define CC_STAGE_MINB 5
+#define CC_STAGE_MINB 6
 #endif
 __global__ void __launch_bounds__(32 * STAGE_WARPS, CC_STAGE_MINB)
 k_stage(const cc_shard sh) {
@@ -1045,10 +1069,13 @@ k_stage(const cc_shard sh) {
     }
     // step t+1's delay >= 2 units (spikes of steps t-1 .. t+1-d_max, all
     // logged): offered to the warps that run out of work items
-    __shared__ unsigned a_n[DEL_DMAX], a_pre[DEL_DMAX + 1];
+    // (block-wide unit tables behind the warps' staging buffers: d_max and
+    // d_max + 1 words, stage_tail_bytes())
     const int D = sh.d_max;
+    unsigned* const a_n = reinterpret_cast<unsigned*>(nsm + STAGE_WARPS * stage_warp_bytes());
+    unsigned* const a_pre = a_n + D;
     const bool tail_deliver = D > 1 && !(sh.flags & CC_FLAG_NO_TAIL_DELIVERY);
-    if (tail_deliver) unit_prefix(sh, t + 1, D - 1, a_n, a_pre);
+    if (tail_deliver) unit_prefix(sh, slot_add(t_mod_l, 1, sh.log_slots), D - 1, a_n, a_pre);
     // queued items per size class (k_plan is complete); claimed largest first
     __shared__ unsigned cls_n[CC_ITEM_CLASSES];
     if (threadIdx.x < CC_ITEM_CLASSES)
@@ -1079,6 +1106,7 @@ k_stage(const cc_shard sh) {
         }
         if (item >= n_items) break;
         CC_DBG(0, gtimer());
+        CC_DBG(5, 0ull);
         unsigned r = item;                        // class c, position r in it
         int c = 0;
         while (r >= cls_n[c]) r -= cls_n[c++];    // terminates: item < n_items
@@ -1107,12 +1135,19 @@ k_stage(const cc_shard sh) {
         const uint32_t roff = warp_excl_scan(go ? n : 0u, rtot);
         B.seg[lane] = (int)roff;
         if (lane == 31) B.seg[32] = (int)rtot;
+        // Phases 1-3 of the item, instantiated twice: with the warp's shared-
+        // memory buffer (every item of <= NEURON_WCAP inputs: the hot path,
+        // shared-memory addressing only), and with a global-scratch buffer for a
+        // single neuron larger than that (an item of its own; onset bursts).
+        // Returns false if a capacity error was raised.
+        auto stage = [&](auto spill_tag) -> bool {
+        constexpr bool SPILL = decltype(spill_tag)::value;
         double* Et = B.t; uint32_t* Es = B.src; float* Ew = B.w; uint16_t* Ep = B.perm;
         uint32_t* Ek = B.keep;
         uint16_t* Epv = B.prov;
         uint8_t* Eo = B.own;
         uint8_t* Eq = B.owns;
-        if (rtot > (uint32_t)NEURON_WCAP) {
+        if constexpr (SPILL) {
             // a single neuron larger than the shared buffer: stage in global scratch
             unsigned long long at = 0;
             int ok = 1;
@@ -1125,7 +1160,7 @@ k_stage(const cc_shard sh) {
             }
             ok = __shfl_sync(0xffffffffu, ok, 0);
             at = __shfl_sync(0xffffffffu, at, 0);
-            if (!ok) continue;
+            if (!ok) return false;
             // spill layout: 3 words of 8 B per event (t, src|w, keep|perm|own)
             double* base = reinterpret_cast<double*>(sh.scratch) + at * 3;
             const uint32_t cap = rtot;
@@ -1188,7 +1223,7 @@ k_stage(const cc_shard sh) {
             const uint32_t eoff = warp_excl_scan(ne, etot);
             const uint64_t h4 = ne ? cc_splitmix64(cc_splitmix64(sh.h2_time ^ (uint64_t)gid)
                                                    ^ (uint64_t)t) : 0ull;
-            if (rtot <= (uint32_t)NEURON_WCAP) {
+            if constexpr (!SPILL) {
                 uint64_t* hq = reinterpret_cast<uint64_t*>(B.hist + 32);   // [32], idle here
                 uint32_t* eo = B.hist + 96;
                 uint32_t* eb = B.hist + 128;
@@ -1222,7 +1257,7 @@ k_stage(const cc_shard sh) {
         //      monotone time bucket (adaptive count per neuron, flattened over
         //      the warp), then the exact rank of each input inside its bucket
         {
-            const uint32_t nbl = go ? min(2u * n, 352u * n / rtot + 1u) : 0u;
+            const uint32_t nbl = go ? min(2u * n, (uint32_t)(HCAP - 32) * n / rtot + 1u) : 0u;
             uint32_t nbt;
             const uint32_t cb = warp_excl_scan(nbl, nbt);
             B.cbk[lane] = cb | (nbl << 16);
@@ -1313,7 +1348,7 @@ k_stage(const cc_shard sh) {
             if (rbase + rtot > (unsigned long long)sh.evrec_cap) cc_raise(ctl, CC_ERR_EVREC, t);
         }
         rbase = __shfl_sync(0xffffffffu, rbase, 0);
-        if (rbase + rtot > (unsigned long long)sh.evrec_cap) continue;
+        if (rbase + rtot > (unsigned long long)sh.evrec_cap) return false;
         {
             double2* R = reinterpret_cast<double2*>(sh.evrec) + 3 * rbase;
             for (uint32_t p = lane; p < rtot; p += 32) {
@@ -1345,6 +1380,10 @@ k_stage(const cc_shard sh) {
         }
         if (go) sh.ev_off[li] = (int32_t)(rbase + roff);
         CC_DBG(3, gtimer());
+        return true;
+        };
+        if (!(rtot > (uint32_t)NEURON_WCAP ? stage(std::true_type{}) : stage(std::false_type{})))
+            continue;
         // ---- 4 publish; the warp finishing a group's last item runs the
         //      group's in-order update (one lane per neuron)
         __threadfence();
@@ -1354,14 +1393,12 @@ k_stage(const cc_shard sh) {
         if (prev + 1u == sh.grp_items[group]) {
             __threadfence();
             if (lane == 0) sh.grp_done[group] = 0u;
-            update_group(sh, li0, t, reinterpret_cast<double2*>(nsm + wib * stage_warp_bytes()),
+            CC_DBG(5, gtimer());                       // update start (0: no update)
+            update_group(sh, li0, t, t_mod_l, reinterpret_cast<double2*>(nsm + wib * stage_warp_bytes()),
                          my_spikes, s_xt);
         }
         {
-            unsigned smid_;
-            asm volatile("mov.u32 %0, %smid;" : "=r"(smid_));
             CC_DBG(4, gtimer());
-            CC_DBG(5, (unsigned long long)smid_);
             CC_DBG(6, (unsigned long long)rtot);
             CC_DBG(7, (unsigned long long)(blockIdx.x * STAGE_WARPS + wib));
         }
@@ -1380,6 +1417,7 @@ k_stage(const cc_shard sh) {
     if (tail_deliver && __shfl_sync(0xffffffffu, idle_prev, 0) + 1u < n_warps &&
         !*(volatile unsigned*)&ctl->error_bits) {
         const unsigned n_a = a_pre[D - 1];
+        const int t1_mod = slot_add(t_mod_l, 1, sh.log_slots);
         const ListSet S1 = list_set(sh, t + 1);
         constexpr int UT = 8;
         int kc = 0;
@@ -1391,7 +1429,7 @@ k_stage(const cc_shard sh) {
             if (u >= n_a) break;
             uint64_t st;
             uint32_t ln, rf;
-            unit_desc(sh, t + 1, a_n, a_pre, u, kc, st, ln, rf);
+            unit_desc(sh, t1_mod, a_n, a_pre, u, kc, st, ln, rf);
             if ((lane & (del_lps(sh) - 1)) == 0) tail_ev += ln;      // one lane per spike
             const uint32_t lmax = warp_max_u32(ln);
             for (int p = 0; (uint32_t)(p * del_lps(sh) * UT) < lmax; ++p) {
@@ -1539,7 +1577,8 @@ k_deliver(const cc_shard sh) {
     // order); read by warp 1 while warp 0 builds the unit prefix
     __shared__ unsigned s_c0;
     if (threadIdx.x == 32) s_c0 = *(volatile unsigned*)&sh.tailc[0];
-    unit_prefix(sh, t, D, s_n, s_pre);
+    const int t_mod = (int)pos_mod(t, L);
+    unit_prefix(sh, t_mod, D, s_n, s_pre);
     const unsigned n_units = s_pre[D];
     const unsigned c0 = min(s_c0, s_pre[D - 1]);
     const ListSet S = list_set(sh, t);
@@ -1554,8 +1593,8 @@ k_deliver(const cc_shard sh) {
     uint64_t st = 0, stn = 0;
     uint32_t ln = 0, rf = 0, lnn = 0, rfn = 0;
     int kcur = 0, kn = 0;
-    if (u < n_units) { unit_desc(sh, t, s_n, s_pre, u, kc, st, ln, rf); kcur = kc; }
-    if (u + nw < n_units) { unit_desc(sh, t, s_n, s_pre, u + nw, kc, stn, lnn, rfn); kn = kc; }
+    if (u < n_units) { unit_desc(sh, t_mod, s_n, s_pre, u, kc, st, ln, rf); kcur = kc; }
+    if (u + nw < n_units) { unit_desc(sh, t_mod, s_n, s_pre, u + nw, kc, stn, lnn, rfn); kn = kc; }
     uint32_t lmax = warp_max_u32(ln);
     int p = 0;
     int tg[U];
@@ -1582,7 +1621,7 @@ k_deliver(const cc_shard sh) {
 #pragma unroll
             for (int k = 0; k < U; ++k) tg2[k] = -1;
         }
-        if (adv && u2 + nw < n_units) { unit_desc(sh, t, s_n, s_pre, u2 + nw, kc, stn, lnn, rfn); kn = kc; }
+        if (adv && u2 + nw < n_units) { unit_desc(sh, t_mod, s_n, s_pre, u2 + nw, kc, stn, lnn, rfn); kn = kc; }
         if (adv && u2 < n_units && cnt_lane) my_ev += ln2;
         deposit_pass<U>(sh, S, kcur % NSUB, tg, w, rf, t);
 #pragma unroll
@@ -1662,6 +1701,7 @@ __global__ void k_build_dseg(const int64_t* row_off, const uint8_t* syn_d, int64
 __global__ void k_ingest(const cc_shard sh, const uint32_t* in_gid, const double* in_t,
                          const int32_t* in_n) {
     const long long t = *(volatile long long*)&sh.ctl->t - 1;
+    const int e_t = (int)pos_mod(t, sh.log_slots);
     const int n = *in_n;
     const int lane = threadIdx.x & 31;
     const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1669,7 +1709,7 @@ __global__ void k_ingest(const cc_shard sh, const uint32_t* in_gid, const double
     for (int b = w0 * 32; b < n; b += nw * 32) {
         const int i = b + lane;
         const bool v = i < n;
-        log_spike_warp(sh, t, v, v ? in_gid[i] : 0u, v ? in_t[i] : 0.0);
+        log_spike_warp(sh, t, e_t, v, v ? in_gid[i] : 0u, v ? in_t[i] : 0.0);
     }
 }
 
@@ -1678,6 +1718,7 @@ __global__ void k_ingest(const cc_shard sh, const uint32_t* in_gid, const double
 __global__ void __launch_bounds__(256) k_xingest(const cc_shard sh) {
     cc_ctl* ctl = sh.ctl;
     const long long t = *(volatile long long*)&ctl->t - 1;
+    const int e_t = (int)pos_mod(t, sh.log_slots);
     // a failed rank stops receiving (its k_stage keeps publishing, so that its
     // peers never wait for it; the hosts agree on the failure per chunk)
     if (*(volatile unsigned*)&ctl->error_bits) return;
@@ -1735,7 +1776,7 @@ __global__ void __launch_bounds__(256) k_xingest(const cc_shard sh) {
             gid = r.x;
             te = __longlong_as_double((long long)(((unsigned long long)r.z << 32) | r.y));
         }
-        log_spike_warp(sh, t, v, gid, te);
+        log_spike_warp(sh, t, e_t, v, gid, te);
     }
 }
 
@@ -1778,6 +1819,7 @@ k_pack_aer(const cc_shard sh, const uint32_t* dest_mask, int n_dest, int cap,
 // of step ctl->t - 1 that have rows here (rows_for, network.py:135-141).
 __global__ void k_ingest_aer(const cc_shard sh, const long long* recv, int n_src, int cap) {
     const long long t = *(volatile long long*)&sh.ctl->t - 1;
+    const int e_t = (int)pos_mod(t, sh.log_slots);
     if (*(volatile unsigned*)&sh.ctl->error_bits) return;
     const size_t stride = 1 + 2 * (size_t)cap;
     __shared__ uint32_t s_pre[33];
@@ -1806,7 +1848,7 @@ __global__ void k_ingest_aer(const cc_shard sh, const long long* recv, int n_src
             gid = (uint32_t)r[0];
             te = __longlong_as_double(r[1]);
         }
-        log_spike_warp(sh, t, v, gid, te);
+        log_spike_warp(sh, t, e_t, v, gid, te);
     }
 }
 
@@ -1855,12 +1897,16 @@ static int sm_count() {
 
 extern "C" int32_t cc_sublists(void) { return CC_SUBLISTS; }
 
-static int stage_blocks_(void);
+static int stage_blocks_(int d_max);
 
 // Kernels cc_deliver + cc_neuron_step launch per step for a shard of n_groups
 // neuron groups (k_plan runs inside k_stage when groups outnumber its warps).
-extern "C" int32_t cc_kernels_per_step(int32_t n_groups) {
-    return n_groups > stage_blocks_() * STAGE_WARPS ? 2 : 3;
+extern "C" int32_t cc_kernels_per_step(const cc_shard* sh) {
+    if (!sh) return 0;
+    const bool fused = (sh->flags & CC_FLAG_PLAN_FUSED) ||
+                       (!(sh->flags & CC_FLAG_PLAN_SEPARATE) &&
+                        sh->n_groups > stage_blocks_(sh->d_max) * STAGE_WARPS);
+    return fused ? 2 : 3;
 }
 
 extern "C" int cc_build_dseg(const int64_t* row_off, const uint8_t* syn_d, int64_t n_rows,
@@ -1888,33 +1934,52 @@ extern "C" int cc_deliver(const cc_shard* sh, void* stream) {
     return cc_check_launch("k_deliver");
 }
 
-// One-time kernel attributes and the persistent grid size (not capturable in
-// a CUDA graph, so done here or on the first eager cc_neuron_step).
-static int stage_blocks = 0;
+// One-time kernel attributes (not settable inside a CUDA graph capture, so done
+// here or on the first eager cc_neuron_step) and the persistent grid size,
+// which depends on d_max through the tail tables' share of shared memory.
+static bool stage_prepared = false;
+static int stage_blocks_by_d[DEL_DMAX] = {};
+
+static size_t stage_smem(int d_max) {
+    return stage_warp_bytes() * STAGE_WARPS + stage_tail_bytes(d_max);
+}
 
 extern "C" int cc_prepare(void) {
-    if (stage_blocks) return 0;
-    const size_t smem = stage_warp_bytes() * STAGE_WARPS;
-    if (cudaFuncSetAttribute(k_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-        != cudaSuccess)
+    if (stage_prepared) return 0;
+    if (cudaFuncSetAttribute(k_stage, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)stage_smem(DEL_DMAX - 1)) != cudaSuccess)
         return cc_set_error("cc_prepare: %s", cudaGetErrorString(cudaGetLastError()));
+    // (filled here, outside any stream capture; the tail tables grow by 16 B
+    // per two delay steps, so the occupancy changes at a few d_max values only)
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage, 32 * STAGE_WARPS, smem);
-    stage_blocks = sm_count() * (per_sm > 0 ? per_sm : 1);
+    size_t last = 0;
+    for (int d = 1; d < DEL_DMAX; ++d) {
+        if (stage_smem(d) != last) {
+            last = stage_smem(d);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage, 32 * STAGE_WARPS, last);
+        }
+        stage_blocks_by_d[d] = sm_count() * (per_sm > 0 ? per_sm : 1);
+    }
+    stage_prepared = true;
     return 0;
 }
 
-static int stage_blocks_(void) {
+static int stage_blocks_(int d_max) {
     cc_prepare();
-    return stage_blocks;
+    return stage_blocks_by_d[d_max < 1 ? 1 : (d_max >= DEL_DMAX ? DEL_DMAX - 1 : d_max)];
 }
+
+extern "C" int32_t cc_stage_warps(int32_t d_max) { return stage_blocks_(d_max) * STAGE_WARPS; }
 
 extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_neuron_step: null shard");
     if (sh->n_local <= 0) return cc_set_error("cc_neuron_step: empty shard");
     const int groups = (sh->n_local + 31) / 32;
-    const size_t smem = stage_warp_bytes() * STAGE_WARPS;
+    if (sh->d_max < 1 || sh->d_max >= DEL_DMAX)
+        return cc_set_error("cc_neuron_step: d_max must be in [1, %d)", DEL_DMAX);
+    const size_t smem = stage_smem(sh->d_max);
     if (const int rc = cc_prepare()) return rc;
+    const int stage_blocks = stage_blocks_(sh->d_max);
     const bool fused = (sh->flags & CC_FLAG_PLAN_FUSED) ||
                        (!(sh->flags & CC_FLAG_PLAN_SEPARATE) && groups > stage_blocks * STAGE_WARPS);
     if (!fused) {

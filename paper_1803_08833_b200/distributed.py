@@ -977,7 +977,7 @@ def bench_distributed(args, cfg) -> Optional[dict]:
                     "d2h_bytes_per_step": 12.0 * float(evs[2]) / args.steps,
                     "api": "DistributedSimulator.advance wall (graph replays, per-chunk "
                            "counter checks, cross-rank error agreement and raster copies)"},
-            "gpu_launches": (int(ds.sim.L.cc_kernels_per_step(ds.sim.shard.n_groups)) + 1)
+            "gpu_launches": (int(ds.sim.L.cc_kernels_per_step(C.byref(ds.sim.shard))) + 1)
             * args.steps,
             "clocks": clk,
         }

@@ -44,9 +44,9 @@ for rep in range(2):
     print(f"  rtot mean {tail[:,6].mean():.1f} max {tail[:,6].max()}")
     ends = np.sort(rel[:, 4])
     print("  completion quantiles (us):", [round(float(np.percentile(ends, q)), 1) for q in (10, 50, 90, 99, 100)])
-    sm = tail[:, 5]
-    busy = np.bincount(sm, weights=dur)
-    print(f"  per-SM summed item-us: min {busy[busy>0].min():.0f} max {busy.max():.0f} mean {busy[busy>0].mean():.0f}")
+    upd = tail[:, 5] > 0                      # slot 5: update start (0: the item ran no update)
+    ud = (tail[upd, 4] - tail[upd, 5]) / 1e3
+    print(f"  group updates {upd.sum()}: us mean {ud.mean():.2f} p90 {np.percentile(ud, 90):.2f} max {ud.max():.2f}")
     # tail: when does each warp finish its last item, and how big were late items
     last = {}
     for w_, e_ in zip(warps, rel[:, 4]):
