@@ -34,6 +34,9 @@
 #ifndef CC_CLAIM_OWN_LINE
 #define CC_CLAIM_OWN_LINE 1  // k_stage item claims on their own L2 line (tailc[96])
 #endif
+#ifndef CC_STAGE_ECR
+#define CC_STAGE_ECR 0       // 1: the refractory-gap fatigue decay staged with the factors
+#endif
 #ifndef CC_TAIL_STOP
 #define CC_TAIL_STOP 10
 #endif
@@ -207,6 +210,13 @@ struct SubMap {
 #pragma unroll
         for (int j = 0; j < NSUB; ++j) { pre[j] = x; x += __shfl_sync(0xffffffffu, cj, j); }
         pre[NSUB] = x;
+    }
+    __device__ __forceinline__ uint32_t pre_at(int j) const {      // pre[j], j not a constant
+        uint32_t v = pre[0];
+#pragma unroll
+        for (int i = 1; i <= NSUB; ++i)
+            if (j >= i) v = pre[i];
+        return v;
     }
     // record index of concatenated position r (< pre[NSUB]) in the group's region
     __device__ __forceinline__ size_t at(uint32_t r, size_t ks) const {
@@ -467,8 +477,12 @@ __device__ __forceinline__ bool slow_step(NState& s, const cc_pop& P, double tj,
     const double ff = fmin(fmax(s.last, s.ru), tj);
     double cs = s.c;
     if (ff != s.last && cs != 0.0) {                  // leaving / inside a refractory window
+#if CC_STAGE_ECR
         if (stale) cs = cs * fexp(-div_rn(ff - s.last, P.tau_c, P.r_tau_c), xt);
         else cs = cs * ecr0;
+#else
+        cs = cs * fexp(-div_rn(ff - s.last, P.tau_c, P.r_tau_c), xt);
+#endif
     }
     double emj = em0, ecj = ec0, fj = f0;
     if (stale) decay_factors(P, tj - ff, cs != 0.0, emj, ecj, fj, xt);
@@ -604,6 +618,18 @@ __device__ __forceinline__ void load_pass(const cc_shard& sh, uint64_t st, uint3
 // the same group (a segment is sorted by target, network.py:257, so a spike's
 // 8 lanes form 1-3 runs; runs are found with a shuffle and a ballot); lists
 // that are full spill to the set's overflow list.
+#ifndef CC_SUB_BY_LANE
+#define CC_SUB_BY_LANE 1     // sub-lists by target lane range (0: by delay, `sub` of the caller)
+#endif
+static_assert((NSUB & (NSUB - 1)) == 0 && NSUB <= 32, "CC_SUBLISTS must be a power of two <= 32");
+__device__ __forceinline__ unsigned list_of(int tg, int sub) {
+#if CC_SUB_BY_LANE
+    return ((unsigned)tg * NSUB) >> 5;                  // (tg >> 5) * NSUB + (tg & 31) * NSUB / 32
+#else
+    return ((unsigned)tg >> 5) * NSUB + (unsigned)sub;
+#endif
+}
+
 template <int U>
 __device__ __forceinline__ void deposit_pass(const cc_shard& sh, const ListSet& S, int sub,
                                              const int* tg, const float* w, uint32_t rf,
@@ -616,8 +642,10 @@ __device__ __forceinline__ void deposit_pass(const cc_shard& sh, const ListSet& 
     const unsigned upto = 0xffffffffu >> (31 - lane);      // bits 0..lane
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-        key[k] = tg[k] >= 0 ? (unsigned)(tg[k] >> 5) : 0xffffffffu;
-        CC_CHK(sh.ctl, tg[k] < 0 || key[k] < (unsigned)sh.n_groups);
+        // list of the target: group * NSUB + sub-list; with CC_SUB_BY_LANE the
+        // sub-list is the target's lane range (NSUB ranges of 32 / NSUB lanes)
+        key[k] = tg[k] >= 0 ? list_of(tg[k], sub) : 0xffffffffu;
+        CC_CHK(sh.ctl, tg[k] < 0 || key[k] < (unsigned)sh.n_groups * NSUB);
         const unsigned prev = __shfl_up_sync(0xffffffffu, key[k], 1);
         const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || key[k] != prev);
         lead[k] = 31 - __clz(heads & upto);
@@ -626,7 +654,7 @@ __device__ __forceinline__ void deposit_pass(const cc_shard& sh, const ListSet& 
         got[k] = 0u;
         if (tg[k] >= 0 && lane == lead[k]) {
             if (CC_TIMING_PROBES && (sh.flags & 1024)) got[k] = 0u;   // probe: no reservation
-            else got[k] = atomicAdd(&S.cnt[((size_t)key[k] * NSUB + sub) * CC_CNT_STRIDE],
+            else got[k] = atomicAdd(&S.cnt[(size_t)key[k] * CC_CNT_STRIDE],
                                     (unsigned)(end - lead[k]));
         }
     }
@@ -638,12 +666,13 @@ __device__ __forceinline__ void deposit_pass(const cc_shard& sh, const ListSet& 
         if (tg[k] < 0 || (CC_TIMING_PROBES && (sh.flags & 2048))) continue;  // probe: no deposit
         const uint32_t lig = (uint32_t)tg[k] & 31u;
         if (pos[k] < (unsigned)K) {
-            S.rec[((size_t)key[k] * NSUB + sub) * KS + pos[k]] =
+            S.rec[(size_t)key[k] * KS + pos[k]] =
                 (uint64_t)((rf << 5) | lig) | ((uint64_t)__float_as_uint(w[k]) << 32);
         } else {
             const unsigned o = atomicAdd(S.ovf_cnt, 1u);
             atomicAdd(&sh.ctl->ovf_total, 1ull);
-            if (o < (unsigned)sh.ovf_cap) S.ovf[o] = make_uint4(key[k], lig, rf, __float_as_uint(w[k]));
+            if (o < (unsigned)sh.ovf_cap)
+                S.ovf[o] = make_uint4((unsigned)tg[k] >> 5, lig, rf, __float_as_uint(w[k]));
             else cc_raise(sh.ctl, CC_ERR_OVERFLOW_BIN, t_err);
         }
     }
@@ -1031,6 +1060,9 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
 #ifndef CC_STAGE_MINB
 #define CC_STAGE_MINB 6
 #endif
+// PLAN: the planning pass runs at the start of the kernel (its own instantiation,
+// so that the separate-k_plan kernel does not carry the planning code).
+template <bool PLAN>
 __global__ void __launch_bounds__(32 * STAGE_WARPS, CC_STAGE_MINB)
 k_stage(const cc_shard sh) {
     extern __shared__ __align__(16) char nsm[];
@@ -1050,7 +1082,7 @@ k_stage(const cc_shard sh) {
     // grid-wide barrier: the persistent grid is co-resident (cooperative launch).
     // Chosen by cc_neuron_step when there are more groups than warps: k_plan's
     // separate, 48-warps-per-SM grid is faster for a single round (config 1).
-    if (sh.plan_in_stage) {
+    if constexpr (PLAN) {
         const int rounds = (sh.n_groups + (int)(gridDim.x * STAGE_WARPS) - 1)
                            / (int)(gridDim.x * STAGE_WARPS);
         for (int r = 0; r < rounds; ++r)
@@ -1187,16 +1219,26 @@ k_stage(const cc_shard sh) {
             const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + sh.ovf_off[group];
             B.hist[lane] = 0u;                          // per-lane fill cursors
             __syncwarp();
-            for (uint32_t r0 = 0; r0 < c_all; r0 += 128) {
+            // concatenated positions [rs, re) of the list part: with sub-lists
+            // by lane range only the ones the item's lanes [l0, l1) fall into
+            uint32_t rs = 0u, re = c_list;
+#if CC_SUB_BY_LANE
+            if (NSUB > 1) {
+                rs = M.pre_at((l0 * NSUB) >> 5);
+                re = M.pre_at((((l1 - 1) * NSUB) >> 5) + 1);
+            }
+#endif
+            const uint32_t n_rd = (re - rs) + (c_all - c_list);
+            for (uint32_t r0 = 0; r0 < n_rd; r0 += 128) {
                 uint64_t rec[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const uint32_t r = r0 + u * 32 + lane;
+                    const uint32_t q0 = r0 + u * 32 + lane;
                     rec[u] = ~0ull;
-                    if (r < c_list) {
-                        rec[u] = lst[M.at(r, KS)];
-                    } else if (r < c_all) {
-                        const uint4 q = ov[r - c_list];
+                    if (q0 < re - rs) {
+                        rec[u] = lst[M.at(rs + q0, KS)];
+                    } else if (q0 < n_rd) {
+                        const uint4 q = ov[q0 - (re - rs)];
                         rec[u] = (uint64_t)((q.z << 5) | q.y) | ((uint64_t)q.w << 32);
                     }
                 }
@@ -1364,8 +1406,12 @@ k_stage(const cc_shard sh) {
                 const cc_pop& P = sh.pop[fl & 1u];
                 decay_factors(P, te - ff, (fl & 2u) != 0, em, ec, f, s_xt);
                 // fatigue decay over the refractory part of the gap (slow_step)
+#if CC_STAGE_ECR
                 const double ecr = (ff != last && (fl & 2u))
                                        ? fexp(-div_rn(ff - last, P.tau_c, P.r_tau_c), s_xt) : 1.0;
+#else
+                const double ecr = 1.0;         // (computed by slow_step when it is needed)
+#endif
                 const double wv = (Es[e] == CC_EXT_SRC) ? sh.ext_weight : (double)Ew[e];
 #if CC_EVREC_STREAM
                 __stcs(R + 3 * p, make_double2(te, wv));
@@ -1897,7 +1943,7 @@ static int sm_count() {
 
 extern "C" int32_t cc_sublists(void) { return CC_SUBLISTS; }
 
-static int stage_blocks_(int d_max);
+static int stage_blocks_(int d_max, bool fused = false);
 
 // Kernels cc_deliver + cc_neuron_step launch per step for a shard of n_groups
 // neuron groups (k_plan runs inside k_stage when groups outnumber its warps).
@@ -1938,7 +1984,7 @@ extern "C" int cc_deliver(const cc_shard* sh, void* stream) {
 // here or on the first eager cc_neuron_step) and the persistent grid size,
 // which depends on d_max through the tail tables' share of shared memory.
 static bool stage_prepared = false;
-static int stage_blocks_by_d[DEL_DMAX] = {};
+static int stage_blocks_by_d[2][DEL_DMAX] = {};        // [planning inside k_stage][d_max]
 
 static size_t stage_smem(int d_max) {
     return stage_warp_bytes() * STAGE_WARPS + stage_tail_bytes(d_max);
@@ -1946,27 +1992,33 @@ static size_t stage_smem(int d_max) {
 
 extern "C" int cc_prepare(void) {
     if (stage_prepared) return 0;
-    if (cudaFuncSetAttribute(k_stage, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(k_stage<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)stage_smem(DEL_DMAX - 1)) != cudaSuccess ||
+        cudaFuncSetAttribute(k_stage<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)stage_smem(DEL_DMAX - 1)) != cudaSuccess)
         return cc_set_error("cc_prepare: %s", cudaGetErrorString(cudaGetLastError()));
     // (filled here, outside any stream capture; the tail tables grow by 16 B
     // per two delay steps, so the occupancy changes at a few d_max values only)
-    int per_sm = 0;
+    int per_sm[2] = {0, 0};
     size_t last = 0;
     for (int d = 1; d < DEL_DMAX; ++d) {
         if (stage_smem(d) != last) {
             last = stage_smem(d);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage, 32 * STAGE_WARPS, last);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], k_stage<false>,
+                                                          32 * STAGE_WARPS, last);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], k_stage<true>,
+                                                          32 * STAGE_WARPS, last);
         }
-        stage_blocks_by_d[d] = sm_count() * (per_sm > 0 ? per_sm : 1);
+        for (int f = 0; f < 2; ++f)
+            stage_blocks_by_d[f][d] = sm_count() * (per_sm[f] > 0 ? per_sm[f] : 1);
     }
     stage_prepared = true;
     return 0;
 }
 
-static int stage_blocks_(int d_max) {
+static int stage_blocks_(int d_max, bool fused) {
     cc_prepare();
-    return stage_blocks_by_d[d_max < 1 ? 1 : (d_max >= DEL_DMAX ? DEL_DMAX - 1 : d_max)];
+    return stage_blocks_by_d[fused][d_max < 1 ? 1 : (d_max >= DEL_DMAX ? DEL_DMAX - 1 : d_max)];
 }
 
 extern "C" int32_t cc_stage_warps(int32_t d_max) { return stage_blocks_(d_max) * STAGE_WARPS; }
@@ -1979,13 +2031,14 @@ extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
         return cc_set_error("cc_neuron_step: d_max must be in [1, %d)", DEL_DMAX);
     const size_t smem = stage_smem(sh->d_max);
     if (const int rc = cc_prepare()) return rc;
-    const int stage_blocks = stage_blocks_(sh->d_max);
     const bool fused = (sh->flags & CC_FLAG_PLAN_FUSED) ||
-                       (!(sh->flags & CC_FLAG_PLAN_SEPARATE) && groups > stage_blocks * STAGE_WARPS);
+                       (!(sh->flags & CC_FLAG_PLAN_SEPARATE) &&
+                        groups > stage_blocks_(sh->d_max, false) * STAGE_WARPS);
+    const int stage_blocks = stage_blocks_(sh->d_max, fused);
     if (!fused) {
         k_plan<<<(groups + 3) / 4, 128, 0, (cudaStream_t)stream>>>(*sh);
         if (const int rc = cc_check_launch("k_plan")) return rc;
-        k_stage<<<stage_blocks, 32 * STAGE_WARPS, smem, (cudaStream_t)stream>>>(*sh);
+        k_stage<false><<<stage_blocks, 32 * STAGE_WARPS, smem, (cudaStream_t)stream>>>(*sh);
     } else {
         // cooperative: the grid barrier after the planning phase needs every
         // block resident (the launch fails instead of hanging otherwise)
@@ -2001,7 +2054,7 @@ extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
         at[0].val.cooperative = 1;
         lc.attrs = at;
         lc.numAttrs = 1;
-        cudaLaunchKernelEx(&lc, k_stage, s2);
+        cudaLaunchKernelEx(&lc, k_stage<true>, s2);
     }
     if (const int rc = cc_check_launch("k_stage")) return rc;
     if (sh->n_probe > 0) {
