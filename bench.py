@@ -474,7 +474,8 @@ def _bench_single(args, cfg, net, capacity):
                                         "(BASELINE.md roofline formula)"},
         "kernels": kernels,
         "gpu_launches": int(L.cc_kernels_per_step(C.byref(sim.shard))) * K,
-        "stage_grid": {"warps": int(L.cc_stage_warps(sim.shard.d_max)),
+        "stage_grid": {"warps": int(L.cc_stage_warps(C.byref(sim.shard))),
+                       "sublists_per_group": int(sim.shard.n_sub),
                        "what": "k_stage's persistent grid (resident warps, 4 per block)"},
         "clocks": clk,
         "construction_s": net.construction_seconds,

@@ -22,16 +22,24 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 26
+#define CC_ABI_VERSION 27
 
-/* Work items are queued in this many size classes, largest first. */
-/* Input lists per 32-neuron group (events of delay d go to sub-list
- * d % CC_SUBLISTS) and the largest stride (u32 words) between their fill
- * counters the host allocates for. */
-#ifndef CC_SUBLISTS
-#define CC_SUBLISTS 1
+/* Input sub-lists per 32-neuron group, by target lane range: sub-list j of a
+ * group holds the events of its lanes [32 j / n, 32 (j + 1) / n).  The library
+ * carries the step kernels in two variants, CC_NSUB_A (one list per group:
+ * fewest reservation atomics, best where a group's inputs fit two or three work
+ * items) and CC_NSUB_B (a work item reads only the sub-lists of its own lanes:
+ * best at high rates, where a group takes ten and more work items);
+ * cc_shard.n_sub selects one per shard.  CC_CNT_STRIDE_FOR(n): u32 words between
+ * the fill counters of consecutive lists (the host sizes bin_cnt with it). */
+#ifndef CC_NSUB_A
+#define CC_NSUB_A 1
 #endif
-#define CC_CNT_STRIDE_MAX 64
+#ifndef CC_NSUB_B
+#define CC_NSUB_B 8
+#endif
+#define CC_CNT_STRIDE_FOR(n) ((n) >= 8 ? 8 : (n) >= 4 ? 16 : (n) >= 2 ? 32 : 64)
+/* Work items are queued in this many size classes, largest first. */
 #define CC_ITEM_CLASSES 8
 
 /* cc_shard.flags: measurement / test modes.  NO_TAIL_DELIVERY: k_stage's idle
@@ -141,7 +149,7 @@ typedef struct cc_shard {
     int32_t flags;          /* CC_FLAG_* mode bits (0 in production runs)       */
     int32_t plan_in_stage;  /* set by cc_neuron_step: k_stage runs the planning itself */
     int32_t del_lps_log2;   /* delivery: log2 lanes per spike (3: 4 spikes per warp unit, 4: 2) */
-    int32_t pad32_;
+    int32_t n_sub;          /* input sub-lists per group: CC_NSUB_A or CC_NSUB_B        */
     uint64_t h2_ext;        /* splitmix chain prefix for EXTERNAL (rng.py:85-86)      */
     uint64_t h2_time;       /* ... for EXTERNAL_TIME                                  */
     uint64_t h2_init;       /* ... for INIT_STATE                                     */
@@ -171,10 +179,10 @@ typedef struct cc_shard {
     int32_t bin_pad;        /* unused records after each list: list stride is
                                bin_cap + bin_pad (staggers the list starts over
                                L2 slices / DRAM channels)                      */
-    uint32_t* bin_cnt;      /* [2][n_groups][CC_SUBLISTS][stride] sub-list fill (word 0) */
-    uint64_t* bin_rec;      /* [2][n_groups][CC_SUBLISTS][bin_cap + bin_pad]   */
+    uint32_t* bin_cnt;      /* [2][n_groups][n_sub][stride] sub-list fill (word 0) */
+    uint64_t* bin_rec;      /* [2][n_groups][n_sub][bin_cap + bin_pad]   */
     uint32_t* grp_n;        /* [n_groups] inputs of the current step per group  */
-    uint32_t* grp_sub;      /* [n_groups][CC_SUBLISTS] records kept per sub-list */
+    uint32_t* grp_sub;      /* [n_groups][n_sub] records kept per sub-list */
     uint32_t* ovf_rec;      /* [2][ovf_cap][4] {group, lane, spike_ref, w_bits} */
     uint32_t* ovf_cnt;      /* [2]                                             */
     uint32_t* ovf_sorted;   /* [ovf_cap][4] overflow of the current step, grouped by group */
@@ -323,16 +331,17 @@ int cc_xwin_open(const uint8_t* handle64, void** ptr);
 int cc_xwin_close(void* ptr);
 int cc_xwin_free(void* ptr);
 
-/* CC_SUBLISTS as compiled (hosts size bin_cnt / bin_rec / grp_sub with it). */
-int32_t cc_sublists(void);
+/* CC_CNT_STRIDE_FOR(n_sub) if the library carries the step kernels for n_sub
+ * sub-lists per group (CC_NSUB_A, CC_NSUB_B), else 0. */
+int32_t cc_cnt_stride(int32_t n_sub);
 
 /* Kernels cc_deliver + cc_neuron_step launch per step for this shard: 3
  * (k_deliver, k_plan, k_stage), 2 when the planning runs inside k_stage. */
 int32_t cc_kernels_per_step(const cc_shard* sh);
 
-/* Warps of k_stage's persistent grid for a shard with this d_max (SM count x
- * resident blocks per SM x warps per block). */
-int32_t cc_stage_warps(int32_t d_max);
+/* Warps of k_stage's persistent grid for this shard (SM count x resident blocks
+ * per SM x warps per block; depends on d_max and n_sub). */
+int32_t cc_stage_warps(const cc_shard* sh);
 
 /* Delay-segment table of a CSR whose rows are sorted by delay: out[r][d] =
  * synapses of row r with delay <= d, d = 0..d_max (u16, row stride `stride`).

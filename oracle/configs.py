@@ -29,7 +29,7 @@ KERNELS = {
 REGIMES = {
     "literal": {"gaussian": (3.0, -1.2, -1.2), "exponential": (3.0, -1.2, -1.2)},
     "calibrated": {"gaussian": (40.0, -2.0, -2.0), "exponential": (55.0, -8.0, -1.0)},
-    "stress": {"gaussian": (40.0, -2.0, -2.0), "exponential": (400.0, -12.0, -0.5)},
+    "stress": {"gaussian": (40.0, -2.0, -2.0), "exponential": (200.0, -8.0, -8.0)},
 }
 NEURON = dict(tau_m=20.0, C_m=1.0, E=0.0, tau_c=300.0, g_c=0.5, V_theta=20.0, V_r=15.0,
               tau_arp=2.0, alpha_c=0.01)

@@ -15,10 +15,9 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "XPeer", "check", "EngineError",
 
 LIB_PATH = os.environ.get("CC_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 26
+ABI_VERSION = 27
 ITEM_CLASSES = 8
 FLAG_NO_TAIL_DELIVERY = 0x1000   # CC_FLAG_NO_TAIL_DELIVERY (include/corticarc_b200.h)
-CNT_STRIDE_MAX = 64          # bin_cnt words per group allocated (CC_CNT_STRIDE <= this)
 
 ERR_BITS = {
     0x01: "spike log full (more spikes in one step than planned)",
@@ -88,7 +87,7 @@ class Shard(C.Structure):
         ("scratch_cap", C.c_int64), ("n_rows", C.c_int64),
         ("out_cap", C.c_int32), ("ext_budget", C.c_int32), ("n_probe", C.c_int32),
         ("direct_log", C.c_int32), ("flags", C.c_int32), ("plan_in_stage", C.c_int32),
-        ("del_lps_log2", C.c_int32), ("pad32_", C.c_int32),
+        ("del_lps_log2", C.c_int32), ("n_sub", C.c_int32),
         ("h2_ext", C.c_uint64), ("h2_time", C.c_uint64), ("h2_init", C.c_uint64),
         ("dt", C.c_double), ("ext_weight", C.c_double), ("ext_thresh", C.c_double),
         ("pop", Pop * 2),
@@ -152,9 +151,9 @@ _SIGS = {
     "cc_xwin_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
     "cc_xwin_close": (C.c_int, [_P]),
     "cc_xwin_free": (C.c_int, [_P]),
-    "cc_sublists": (C.c_int32, []),
+    "cc_cnt_stride": (C.c_int32, [C.c_int32]),
     "cc_kernels_per_step": (C.c_int32, [_P]),
-    "cc_stage_warps": (C.c_int32, [C.c_int32]),
+    "cc_stage_warps": (C.c_int32, [_P]),
     "cc_csr_checksum": (C.c_int, [_P, _P, C.c_int64, _P, _P, _P, C.c_int32, C.c_int32, _P, _P]),
     "cc_test_philox": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_int32,
                                  _P, _P]),
@@ -187,9 +186,15 @@ def load_library(path: str = LIB_PATH):
     return L
 
 
-def sublists() -> int:
-    """Input sub-lists per neuron group, as compiled into the library."""
-    return int(load_library().cc_sublists())
+def cnt_stride(n_sub: int) -> int:
+    """u32 words between the fill counters of consecutive input lists for a
+    shard with n_sub sub-lists per group; raises if the library does not carry
+    that variant (include/corticarc_b200.h: CC_NSUB_A, CC_NSUB_B)."""
+    st = int(load_library().cc_cnt_stride(int(n_sub)))
+    if st <= 0:
+        raise ValueError(f"the library has no step kernels for {n_sub} sub-lists per group")
+    return st
+
 
 
 def lib():

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 GEN = os.path.join(CSRC, "_gen")
 LIB = os.path.join(PKG, "libcorticarc_b200.so")
-SOURCES = ["capi.cu", "sim_kernels.cu", "gen_kernels.cu"]
+SOURCES = ["capi.cu", "dispatch.cu", "sim_kernels.cu", "gen_kernels.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false",
          "-gencode", "arch=compute_100a,code=sm_100a",
@@ -36,9 +36,20 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _defined(defines, key, default):
+    for d in defines:
+        if d.split("=")[0] == key:
+            return d.split("=", 1)[1]
+    return default
+
+
 def build(force: bool = False, verbose: bool = False, out: str | None = None,
           defines: tuple = ()) -> str:
-    """Compile the library; `out`/`defines` build tuning variants (tools/)."""
+    """Compile the library; `out`/`defines` build tuning variants (tools/).
+
+    sim_kernels.cu is compiled once per sub-list variant (CC_NSUB_A and
+    CC_NSUB_B sub-lists per group, include/corticarc_b200.h; a `CC_SUBLISTS=n`
+    define builds that single variant instead), the objects in parallel."""
     target = out or LIB
     os.makedirs(os.path.dirname(os.path.abspath(target)), exist_ok=True)
     if out is None and not force and not _stale():
@@ -49,17 +60,41 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     finally:
         sys.path.pop(0)
     gen_ziggurat.emit(os.path.join(GEN, "cc_ziggurat_tables.h"))
-    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-shared",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           "-I", GEN, *[os.path.join(CSRC, s) for s in SOURCES], "-o", target + ".tmp"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    defines = tuple(defines)
+    single = _defined(defines, "CC_SUBLISTS", None)
+    if single is not None:          # one variant: both slots name it
+        defines = tuple(d for d in defines if d.split("=")[0] != "CC_SUBLISTS")
+        defines += (f"CC_NSUB_A={single}", f"CC_NSUB_B={single}")
+    nsub = sorted({_defined(defines, "CC_NSUB_A", "1"), _defined(defines, "CC_NSUB_B", "8")})
+    objdir = os.path.join(GEN, "obj_" + os.path.basename(target).replace(".", "_"))
+    os.makedirs(objdir, exist_ok=True)
+    common = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+              "-I", CSRC, "-I", GEN]
+    jobs = [(os.path.join(objdir, name.replace(".cu", ".o")), [os.path.join(CSRC, name)], [])
+            for name in SOURCES if name != "sim_kernels.cu"]
+    jobs += [(os.path.join(objdir, f"sim_kernels_s{n}.o"), [os.path.join(CSRC, "sim_kernels.cu")],
+              [f"-DCC_SUBLISTS={n}"]) for n in nsub]
+    procs = [(obj, subprocess.Popen([*common, *extra, "-c", *src, "-o", obj],
+                                    stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+             for obj, src, extra in jobs]
+    log, failed = [], None
+    for obj, pr in procs:
+        so, se = pr.communicate()
+        log.append(f"==== {os.path.basename(obj)}\n{so}{se}")
+        if pr.returncode != 0 and failed is None:
+            failed = se
     with open(os.path.join(GEN, "ptxas.log"), "w") as fh:
-        fh.write(res.stdout + res.stderr)
+        fh.write("\n".join(log))
+    if failed is not None:
+        raise RuntimeError("nvcc failed:\n" + failed[-6000:])
+    res = subprocess.run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
+                          *[obj for obj, _, _ in jobs], "-o", target + ".tmp"],
+                         capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stderr[-6000:])
+        raise RuntimeError("link failed:\n" + res.stderr[-6000:])
     os.replace(target + ".tmp", target)
     if verbose:
-        print(res.stderr)
+        print("\n".join(log))
     return target
 
 

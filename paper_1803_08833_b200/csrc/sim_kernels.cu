@@ -20,13 +20,25 @@
 #include <type_traits>
 #include "cc_common.cuh"
 
+// This translation unit is compiled once per sub-list variant (build.py):
+// CC_SUBLISTS sub-lists per group, entry points suffixed _s<CC_SUBLISTS>
+// (dispatch.cu selects by cc_shard.n_sub).  The primary variant (CC_NSUB_A)
+// also carries the entry points that do not depend on the lists.
+#ifndef CC_SUBLISTS
+#define CC_SUBLISTS CC_NSUB_A
+#endif
+#define CC_PRIMARY (CC_SUBLISTS == CC_NSUB_A)
+#define CC_CAT2_(a, b) a##_s##b
+#define CC_CAT2(a, b) CC_CAT2_(a, b)
+#define CC_V(name) CC_CAT2(name, CC_SUBLISTS)
+
 // cache-policy experiments (tools/sweep_variants.py): evict-first CSR loads in
 // k_deliver, evict-first ordered-input records in k_stage
 // list fill counters CC_CNT_STRIDE words apart: a step's reservations (one
 // atomic per run) hit n_groups counters, which a dense array would put in a
 // handful of L2 slices
 #ifndef CC_CNT_STRIDE
-#define CC_CNT_STRIDE 64
+#define CC_CNT_STRIDE CC_CNT_STRIDE_FOR(CC_SUBLISTS)
 #endif
 #ifndef CC_STATIC_FIRST
 #define CC_STATIC_FIRST 1     // k_stage: each warp's first item by its index
@@ -1941,13 +1953,13 @@ static int sm_count() {
     return n;
 }
 
-extern "C" int32_t cc_sublists(void) { return CC_SUBLISTS; }
+extern "C" int32_t CC_V(cc_sublists)(void) { return CC_SUBLISTS; }
 
 static int stage_blocks_(int d_max, bool fused = false);
 
 // Kernels cc_deliver + cc_neuron_step launch per step for a shard of n_groups
 // neuron groups (k_plan runs inside k_stage when groups outnumber its warps).
-extern "C" int32_t cc_kernels_per_step(const cc_shard* sh) {
+extern "C" int32_t CC_V(cc_kernels_per_step)(const cc_shard* sh) {
     if (!sh) return 0;
     const bool fused = (sh->flags & CC_FLAG_PLAN_FUSED) ||
                        (!(sh->flags & CC_FLAG_PLAN_SEPARATE) &&
@@ -1955,7 +1967,7 @@ extern "C" int32_t cc_kernels_per_step(const cc_shard* sh) {
     return fused ? 2 : 3;
 }
 
-extern "C" int cc_build_dseg(const int64_t* row_off, const uint8_t* syn_d, int64_t n_rows,
+extern "C" int CC_V(cc_build_dseg)(const int64_t* row_off, const uint8_t* syn_d, int64_t n_rows,
                              int32_t d_max, int32_t stride, uint16_t* out, unsigned* err,
                              void* stream) {
     if (d_max < 1 || d_max >= DEL_DMAX || stride < d_max + 1 || stride % 8)
@@ -1967,14 +1979,14 @@ extern "C" int cc_build_dseg(const int64_t* row_off, const uint8_t* syn_d, int64
     return cc_check_launch("k_build_dseg");
 }
 
-extern "C" int cc_init_state(const cc_shard* sh, void* stream) {
+extern "C" int CC_V(cc_init_state)(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_init_state: null shard");
     if (sh->n_local == 0) return 0;
     k_init_state<<<(sh->n_local + 255) / 256, 256, 0, (cudaStream_t)stream>>>(*sh);
     return cc_check_launch("k_init_state");
 }
 
-extern "C" int cc_deliver(const cc_shard* sh, void* stream) {
+extern "C" int CC_V(cc_deliver)(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_deliver: null shard");
     k_deliver<<<sm_count() * CC_DEL_MINB, CC_DEL_THREADS, 0, (cudaStream_t)stream>>>(*sh);
     return cc_check_launch("k_deliver");
@@ -1990,7 +2002,7 @@ static size_t stage_smem(int d_max) {
     return stage_warp_bytes() * STAGE_WARPS + stage_tail_bytes(d_max);
 }
 
-extern "C" int cc_prepare(void) {
+extern "C" int CC_V(cc_prepare)(void) {
     if (stage_prepared) return 0;
     if (cudaFuncSetAttribute(k_stage<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)stage_smem(DEL_DMAX - 1)) != cudaSuccess ||
@@ -2017,20 +2029,20 @@ extern "C" int cc_prepare(void) {
 }
 
 static int stage_blocks_(int d_max, bool fused) {
-    cc_prepare();
+    CC_V(cc_prepare)();
     return stage_blocks_by_d[fused][d_max < 1 ? 1 : (d_max >= DEL_DMAX ? DEL_DMAX - 1 : d_max)];
 }
 
-extern "C" int32_t cc_stage_warps(int32_t d_max) { return stage_blocks_(d_max) * STAGE_WARPS; }
+extern "C" int32_t CC_V(cc_stage_warps)(int32_t d_max) { return stage_blocks_(d_max) * STAGE_WARPS; }
 
-extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
+extern "C" int CC_V(cc_neuron_step)(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_neuron_step: null shard");
     if (sh->n_local <= 0) return cc_set_error("cc_neuron_step: empty shard");
     const int groups = (sh->n_local + 31) / 32;
     if (sh->d_max < 1 || sh->d_max >= DEL_DMAX)
         return cc_set_error("cc_neuron_step: d_max must be in [1, %d)", DEL_DMAX);
     const size_t smem = stage_smem(sh->d_max);
-    if (const int rc = cc_prepare()) return rc;
+    if (const int rc = CC_V(cc_prepare)()) return rc;
     const bool fused = (sh->flags & CC_FLAG_PLAN_FUSED) ||
                        (!(sh->flags & CC_FLAG_PLAN_SEPARATE) &&
                         groups > stage_blocks_(sh->d_max, false) * STAGE_WARPS);
@@ -2065,14 +2077,14 @@ extern "C" int cc_neuron_step(const cc_shard* sh, void* stream) {
 
 }
 
-extern "C" int cc_ingest(const cc_shard* sh, const uint32_t* in_gid, const double* in_t,
+extern "C" int CC_V(cc_ingest)(const cc_shard* sh, const uint32_t* in_gid, const double* in_t,
                          const int32_t* in_n, void* stream) {
     if (!sh) return cc_set_error("cc_ingest: null shard");
     k_ingest<<<sm_count() * 2, 256, 0, (cudaStream_t)stream>>>(*sh, in_gid, in_t, in_n);
     return cc_check_launch("k_ingest");
 }
 
-extern "C" int cc_pack_aer(const cc_shard* sh, const uint32_t* dest_mask_by_local,
+extern "C" int CC_V(cc_pack_aer)(const cc_shard* sh, const uint32_t* dest_mask_by_local,
                            int32_t n_dest, int32_t cap, int64_t* send,
                            const int32_t* local_of_col, void* stream) {
     if (!sh) return cc_set_error("cc_pack_aer: null shard");
@@ -2084,7 +2096,7 @@ extern "C" int cc_pack_aer(const cc_shard* sh, const uint32_t* dest_mask_by_loca
     return cc_check_launch("k_pack_aer");
 }
 
-extern "C" int cc_ingest_aer(const cc_shard* sh, const int64_t* recv, int32_t n_src, int32_t cap,
+extern "C" int CC_V(cc_ingest_aer)(const cc_shard* sh, const int64_t* recv, int32_t n_src, int32_t cap,
                              void* stream) {
     if (!sh) return cc_set_error("cc_ingest_aer: null shard");
     k_ingest_aer<<<sm_count(), 256, 0, (cudaStream_t)stream>>>(
@@ -2092,7 +2104,7 @@ extern "C" int cc_ingest_aer(const cc_shard* sh, const int64_t* recv, int32_t n_
     return cc_check_launch("k_ingest_aer");
 }
 
-extern "C" int cc_exchange_ingest(const cc_shard* sh, void* stream) {
+extern "C" int CC_V(cc_exchange_ingest)(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_exchange_ingest: null shard");
     if (!sh->xsrc || !sh->xdst) return cc_set_error("cc_exchange_ingest: no peer exchange set up");
     if (sh->n_ranks < 1 || sh->n_ranks > 32) return cc_set_error("cc_exchange_ingest: 1..32 ranks");
@@ -2102,7 +2114,7 @@ extern "C" int cc_exchange_ingest(const cc_shard* sh, void* stream) {
     return cc_check_launch("k_xingest");
 }
 
-extern "C" int cc_test_math(int32_t kind, const double* x, double* out, int64_t n, void* stream) {
+extern "C" int CC_V(cc_test_math)(int32_t kind, const double* x, double* out, int64_t n, void* stream) {
     if (kind < 0 || kind > 3) return cc_set_error("cc_test_math: kind 0..3");
     if (n <= 0) return 0;
     k_test_math<<<sm_count() * 4, 256, 0, (cudaStream_t)stream>>>(kind, x, out, n);

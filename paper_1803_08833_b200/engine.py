@@ -149,7 +149,7 @@ class Simulator:
                  use_graphs: bool = True, direct_log: Optional[bool] = None,
                  remote=None,
                  raster_steps: Optional[int] = None, substeps: bool = False, device=None,
-                 capacity=None):
+                 capacity=None, sublists: Optional[int] = None):
         import torch
         self.L = _lib.lib()
         self.torch = torch
@@ -165,8 +165,22 @@ class Simulator:
         D = cfg.d_max
         bound = _spikes_per_step_bound(cfg)
         step_cap = default_bin_cap(cfg)        # records per group and step
+        # Input sub-lists per group (by target lane range).  One list per group
+        # has the fewest reservation atomics and is best while a group's inputs
+        # fit two or three work items; at high rates (a group takes ten and
+        # more items, each of which would read the whole list) 8 sub-lists let
+        # an item read only its own lanes' records: -19 % per step at the 37 Hz
+        # stress point, +7 % / +18 % at configs 1 / 3.  The rate is not known
+        # before the run: a drive of >= 10 external events per neuron and step
+        # is taken as the mark of the high-rate regime (CC_SUBLISTS overrides).
+        if sublists is None:
+            sublists = int(os.environ.get("CC_SUBLISTS", "0")) or \
+                (8 if cfg.external.mean_per_step(cfg.timestep_ms) >= 10.0 else 1)
+        n_sub = int(sublists)
+        cnt_stride = _lib.cnt_stride(n_sub)
+        self.n_sub = n_sub
         if bin_cap is None:                    # per sub-list: 2x an even share
-            bin_cap = max(256, 2 * step_cap // _lib.sublists())
+            bin_cap = max(256, 2 * step_cap // n_sub)
         n_groups = (n_local + 31) // 32
         # list stride bin_cap + bin_pad records: with a power-of-two stride the
         # appends of one step (same small offsets in thousands of lists) land in
@@ -204,12 +218,12 @@ class Simulator:
         self.buf = dict(
             gid=T.from_numpy(gids.astype(np.uint32).view(np.int32)).to(dev),
             state=T.zeros((n_local, 4), dtype=f64, device=dev),
-            bin_cnt=T.zeros(2 * n_groups * _lib.sublists() * _lib.CNT_STRIDE_MAX, dtype=i32,
+            bin_cnt=T.zeros(2 * n_groups * n_sub * cnt_stride, dtype=i32,
                             device=dev),
-            bin_rec=T.empty((2, n_groups, _lib.sublists(), bin_cap + bin_pad), dtype=i64,
+            bin_rec=T.empty((2, n_groups, n_sub, bin_cap + bin_pad), dtype=i64,
                             device=dev),
             grp_n=T.zeros(n_groups, dtype=i32, device=dev),
-            grp_sub=T.zeros((n_groups, _lib.sublists()), dtype=i32, device=dev),
+            grp_sub=T.zeros((n_groups, n_sub), dtype=i32, device=dev),
             ovf_rec=T.empty((2, ovf_cap, 4), dtype=i32, device=dev),
             ovf_cnt=T.zeros(2, dtype=i32, device=dev),
             ovf_sorted=T.empty((ovf_cap, 4), dtype=i32, device=dev),
@@ -252,6 +266,7 @@ class Simulator:
         sh.n_local, sh.n_col, sh.n_exc_col = n_local, n, grid.n_excitatory_per_column
         sh.d_max, sh.bin_cap, sh.log_slots = D, bin_cap, D + 1
         sh.n_groups, sh.bin_pad = n_groups, bin_pad
+        sh.n_sub = n_sub
         sh.flags = int(os.environ.get("CC_FLAGS", "0"))    # CC_FLAG_* (measurement / tests)
         sh.spk_cap, sh.seg_stride = spk_cap, seg_stride
         # delivery lanes per spike: 16 on shards of >= 2 M neurons (config 3 gaussian: k_deliver

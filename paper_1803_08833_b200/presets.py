@@ -9,7 +9,7 @@ Three regimes per config:
 * ``calibrated`` - the operating point used for performance: J_inh = -2.0 mV
                    and an external drive pinned with the calibration sweep so
                    the Gaussian grids fire at ~7.5 Hz.
-* ``stress``     - the exponential grids at ~33 Hz mean rate (see STRESS below):
+* ``stress``     - the exponential grids at ~37 Hz mean rate (see STRESS below):
                    the paper's event volume, for the delivery path.
 
 Not expressible in the reference and therefore not used: periodic borders
@@ -57,15 +57,16 @@ CALIBRATED_DRIVE_HZ = {"gaussian": 40.0, "exponential": 55.0}
 CALIBRATED_J_INH = {"gaussian": (-2.0, -2.0), "exponential": (-8.0, -1.0)}   # (->exc, ->inh)
 
 # ``stress``: the exponential grids at the paper's event volume (PAPER.md:530-532
-# quotes 32-38 Hz).  The BASELINE neuron/weight model has no asynchronous state
-# there with equal inhibitory weights (every J_inh->exc = J_inh->inh in -2..-8
-# runs away at drive >= 50 Hz: tools/sweep_rates.py, profiles/operating_points_r02.md);
-# with strong inhibition onto excitatory cells and weak inhibition between
-# inhibitory cells it settles at ~33 Hz mean (excitatory ~7 Hz, inhibitory
-# ~185 Hz) with a flat population rate (CV of the per-step spike count 0.16):
-# 400 Hz drive per external synapse, J_inh->exc = -12 mV, J_inh->inh = -0.5 mV.
-# A labelled stress point for the delivery path, not a biological calibration.
-STRESS = {"gaussian": (40.0, -2.0, -2.0), "exponential": (400.0, -12.0, -0.5)}
+# quotes 32-38 Hz).  With the inhibitory weights raised to -8 mV onto both
+# populations the BASELINE model has a stable asynchronous state whose rate
+# follows the drive (tools/sweep_rates.py on config 2, 0.3 s runs,
+# profiles/operating_points_r02.md): 55 Hz drive -> 18 Hz, 100 -> 25, 200 -> 37,
+# 400 -> 58 Hz, excitatory and inhibitory rates within 10 % of each other and a
+# flat population rate (CV of the per-step spike count 0.02-0.07).  The stress
+# point is 200 Hz drive: 37 Hz, ~52 M recurrent + 14 M external events per step
+# at config 2 (SURVEY.md 8(a) sizes config 2 at 50 M recurrent events per step).
+# A labelled operating point for the event volume, not a biological calibration.
+STRESS = {"gaussian": (40.0, -2.0, -2.0), "exponential": (200.0, -8.0, -8.0)}
 
 
 def baseline_config(index: int, regime: str = "calibrated", kernel: str | None = None,

@@ -52,7 +52,7 @@ def test_workload_defaults_and_scaling(monkeypatch):
     grid = bench.workload(_args(config=4, grid="48x24"))
     assert (grid.grid.nx, grid.grid.ny) == (48, 24)
     stress = bench.workload(_args(config=2, regime="stress"))
-    assert stress.external.rate_per_synapse_hz == 400.0 and stress.genspec.j_inh_inh == -0.5
+    assert stress.external.rate_per_synapse_hz == 200.0 and stress.genspec.j_inh_inh == -8.0
 
 
 def test_reference_arm_config_is_the_gpu_arm_config(monkeypatch):

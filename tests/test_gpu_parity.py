@@ -262,6 +262,20 @@ def test_planning_inside_k_stage_same_run(cuda, name, monkeypatch):
     _assert_same_run(run_b200(cfg, 1), meta, arr)
 
 
+@pytest.mark.parametrize("name", ["config0_cal", "tiny_exp", "tiny_gauss_long"])
+@pytest.mark.parametrize("flags", ["0", "4096", "32768"])
+def test_sublists_by_lane_range_same_run(cuda, name, flags, monkeypatch):
+    """The high-rate variant of the step kernels (8 input sub-lists per group, by
+    target lane range; chosen by the drive rate, forced here) reproduces the
+    reference run in every delivery / planning mode."""
+    from paper_1803_08833_b200.engine import run_b200
+    cfg, meta, arr = golden_run(name)
+    monkeypatch.setenv("CC_SUBLISTS", "8")
+    monkeypatch.setenv("CC_FLAGS", flags)
+    res = run_b200(cfg, 1)
+    _assert_same_run(res, meta, arr)
+
+
 def test_planning_modes_agree_at_scale(cuda, monkeypatch):
     """10x10 columns (3,875 groups > k_stage's warps: planning inside k_stage by
     default) - the same raster as with the separate k_plan kernel."""
@@ -697,6 +711,10 @@ for flags in ("4096", "32768"):
     out["tiny_gauss_long/" + flags] = same(run_b200(cfg, 1), meta, arr)
 os.environ["CC_FLAGS"] = "0"
 out["overflow"] = same(run_b200(cfg, 1, bin_cap=2), meta, arr)
+os.environ["CC_SUBLISTS"] = "8"
+out["sublists8"] = same(run_b200(cfg, 1), meta, arr)
+out["sublists8/overflow"] = same(run_b200(cfg, 1, bin_cap=2), meta, arr)
+del os.environ["CC_SUBLISTS"]
 cfg, meta, arr = golden_run("tiny_gauss")
 out["p2p_local_3"] = same(run_local_shards(cfg, 3, transport="p2p"), meta, arr)
 out["slots_local_4"] = same(run_local_shards(cfg, 4), meta, arr)
