@@ -36,7 +36,7 @@ def raw(rep):
                 if x is not None and un in SCALE:
                     x *= SCALE[un]
                 d[k] = x
-        d["kernel"] = r[h.index("Kernel Name")].split("(")[0].replace("<unnamed>::", "")
+        d["kernel"] = r[h.index("Kernel Name")].replace("<unnamed>::", "").replace("void ", "").split("(")[0].split("<")[0]
         res.append(d)
     return res
 
@@ -73,7 +73,9 @@ if os.path.exists(lc):
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
     agg = defaultdict(lambda: [0, 0.0])
     for r in rows[1:]:
-        k = r[ki].split("(")[0].replace("<unnamed>::", "").replace("void ", "")
+        k = r[ki].replace("<unnamed>::", "").replace("void ", "").split("(")[0]
+        if k.startswith("k_"):
+            k = k.split("<")[0]
         agg[k][0] += 1
         agg[k][1] += float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1)
     step = {k: v for k, v in agg.items() if k in ("k_deliver", "k_plan", "k_stage", "k_xingest")}
