@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 27
+#define CC_ABI_VERSION 28
 
 /* Input sub-lists per 32-neuron group, by target lane range: sub-list j of a
  * group holds the events of its lanes [32 j / n, 32 (j + 1) / n).  The library
@@ -41,6 +41,13 @@ extern "C" {
 #define CC_CNT_STRIDE_FOR(n) ((n) >= 8 ? 8 : (n) >= 4 ? 16 : (n) >= 2 ? 32 : 64)
 /* Work items are queued in this many size classes, largest first. */
 #define CC_ITEM_CLASSES 8
+/* Routed (two-pass) delivery, cc_shard.l1_cnt != NULL: regions of 2^l1_rb
+ * consecutive neurons; at most CC_L1_MAX_REGIONS regions per shard and
+ * CC_L1_MAX_LISTS input lists per region; region fill counters CC_L1_STRIDE
+ * u32 words apart. */
+#define CC_L1_MAX_REGIONS 2048
+#define CC_L1_MAX_LISTS 1024
+#define CC_L1_STRIDE 32
 
 /* cc_shard.flags: measurement / test modes.  NO_TAIL_DELIVERY: k_stage's idle
  * warps do not deliver the next step's delay >= 2 events, so cc_deliver
@@ -245,6 +252,22 @@ typedef struct cc_shard {
     const cc_xpeer* xsrc;   /* [n_ranks] receive side (device memory)           */
     uint32_t* xcnt;         /* [32] records pushed per destination this step (zero between steps) */
     int64_t xwait_ns;       /* give up waiting for a source's flag after this long (CC_ERR_XWAIT) */
+
+    /* routed delivery (l1_cnt == NULL: cc_deliver deposits straight into the
+     * input lists, one scattered 8 B store per event).  With it, cc_deliver
+     * runs two passes, each a counting sort of a tile of events in shared
+     * memory followed by coalesced run copies: pass 1 (k_route) routes the
+     * step's arrivals to one record array per region of 2^l1_rb consecutive
+     * target neurons, pass 2 (k_bin) distributes every region's records to its
+     * input lists.  A pass-1 record is 10 B: spike_ref, weight bits, target
+     * within the region. */
+    int32_t l1_rb;          /* log2 neurons per region (5 .. 16)                 */
+    int32_t n_regions;      /* ceil(n_local / 2^l1_rb) <= CC_L1_MAX_REGIONS     */
+    int64_t l1_cap;         /* records per region and step                      */
+    uint32_t* l1_cnt;       /* [2][n_regions][CC_L1_STRIDE] region fill (word 0), by step parity */
+    uint32_t* l1_ref;       /* [n_regions][l1_cap]                              */
+    uint32_t* l1_w;         /* [n_regions][l1_cap]                              */
+    uint16_t* l1_tgt;       /* [n_regions][l1_cap]                              */
 } cc_shard;
 
 /* ---------------------------------------------------------------- misc */

@@ -110,7 +110,8 @@ CHECKED_VARIANT = os.path.join(PKG, "libcorticarc_b200_chk.so")
 
 def build_test_variants(force: bool = False) -> None:
     for path, defines in ((SPILL_VARIANT, ("CC_NEURON_WCAP=4", "CC_UPD_PIPE=0")),
-                          (CHECKED_VARIANT, ("CC_CHECKS=1",))):
+                          (CHECKED_VARIANT, ("CC_CHECKS=1", "CC_RT_PER_THREAD=1", "CC_BN_PER_THREAD=1",
+                                             "CC_RT_BLOCKS=3"))):
         if force or not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(LIB):
             build(force=True, out=path, defines=defines)
 

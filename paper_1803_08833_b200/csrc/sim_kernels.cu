@@ -1223,48 +1223,54 @@ k_stage(const cc_shard sh) {
         //      the group's run of the grouped overflow), keep the item's lanes
         {
             const uint32_t c_all = sh.grp_n[group];
-            SubMap M;
-            M.init(lane < NSUB ? sh.grp_sub[(size_t)group * NSUB + lane] : 0u);
-            const uint32_t c_list = M.pre[NSUB];
+            // lane j < NSUB: records kept in sub-list j
+            const uint32_t cj = lane < NSUB ? sh.grp_sub[(size_t)group * NSUB + lane] : 0u;
+            uint32_t c_list = cj;
+#pragma unroll
+            for (int o = NSUB >> 1; o > 0; o >>= 1) c_list += __shfl_xor_sync(0xffffffffu, c_list, o);
+            c_list = __shfl_sync(0xffffffffu, c_list, 0);
             const size_t KS = (size_t)K + sh.bin_pad;
             const uint64_t* lst = list_set(sh, t).rec + (size_t)group * NSUB * KS;
             const uint4* ov = reinterpret_cast<const uint4*>(sh.ovf_sorted) + sh.ovf_off[group];
             B.hist[lane] = 0u;                          // per-lane fill cursors
             __syncwarp();
-            // concatenated positions [rs, re) of the list part: with sub-lists
-            // by lane range only the ones the item's lanes [l0, l1) fall into
-            uint32_t rs = 0u, re = c_list;
+            auto keep = [&](uint64_t rec) {             // stage a record of the item's lanes
+                const int L = (int)((uint32_t)rec & 31u);
+                if (L < l0 || L >= l1) return;
+                const int dst = B.seg[L] + (int)atomicAdd(&B.hist[L], 1u);
+                CC_CHK(ctl, dst >= B.seg[L] && dst < B.seg[L + 1] && dst < (int)rtot);
+                const Ev ev = make_rec_event(sh, rec, t_mod_l);
+                Et[dst] = ev.t; Es[dst] = ev.src; Ew[dst] = ev.w;
+                Eo[dst] = (uint8_t)L;
+            };
+            // the sub-lists the item's lanes [l0, l1) fall into (sub-lists by
+            // lane range), one after the other, four records per lane in flight
+            int j0 = 0, j1 = NSUB;
 #if CC_SUB_BY_LANE
             if (NSUB > 1) {
-                rs = M.pre_at((l0 * NSUB) >> 5);
-                re = M.pre_at((((l1 - 1) * NSUB) >> 5) + 1);
+                j0 = (l0 * NSUB) >> 5;
+                j1 = (((l1 - 1) * NSUB) >> 5) + 1;
             }
 #endif
-            const uint32_t n_rd = (re - rs) + (c_all - c_list);
-            for (uint32_t r0 = 0; r0 < n_rd; r0 += 128) {
-                uint64_t rec[4];
+            for (int j = j0; j < j1; ++j) {
+                const uint32_t cnt = __shfl_sync(0xffffffffu, cj, j);
+                const uint64_t* lj = lst + (size_t)j * KS;
+                for (uint32_t r0 = 0; r0 < cnt; r0 += 128) {
+                    uint64_t rec[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t q0 = r0 + u * 32 + lane;
-                    rec[u] = ~0ull;
-                    if (q0 < re - rs) {
-                        rec[u] = lst[M.at(rs + q0, KS)];
-                    } else if (q0 < n_rd) {
-                        const uint4 q = ov[q0 - (re - rs)];
-                        rec[u] = (uint64_t)((q.z << 5) | q.y) | ((uint64_t)q.w << 32);
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t q0 = r0 + u * 32 + lane;
+                        rec[u] = q0 < cnt ? lj[q0] : ~0ull;
                     }
-                }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (rec[u] == ~0ull) continue;
-                    const int L = (int)((uint32_t)rec[u] & 31u);
-                    if (L < l0 || L >= l1) continue;
-                    const int dst = B.seg[L] + (int)atomicAdd(&B.hist[L], 1u);
-                    CC_CHK(ctl, dst >= B.seg[L] && dst < B.seg[L + 1] && dst < (int)rtot);
-                    const Ev ev = make_rec_event(sh, rec[u], t_mod_l);
-                    Et[dst] = ev.t; Es[dst] = ev.src; Ew[dst] = ev.w;
-                    Eo[dst] = (uint8_t)L;
+                    for (int u = 0; u < 4; ++u)
+                        if (rec[u] != ~0ull) keep(rec[u]);
                 }
+            }
+            // then the group's run of the grouped overflow list
+            for (uint32_t q0 = lane; q0 < c_all - c_list; q0 += 32) {
+                const uint4 q = ov[q0];
+                keep((uint64_t)((q.z << 5) | q.y) | ((uint64_t)q.w << 32));
             }
             __syncwarp();
         }
@@ -1600,6 +1606,65 @@ __device__ void group_overflow(const cc_shard& sh, const ListSet& S, unsigned m)
     for (unsigned j = threadIdx.x; j < m; j += blockDim.x) sh.ovf_fill[rec[j].x] = 0;
 }
 
+// Per-step bookkeeping of the first delivery kernel's first thread.
+__device__ __forceinline__ void deliver_prologue(const cc_shard& sh, long long t) {
+    cc_ctl* ctl = sh.ctl;
+    const int L = sh.log_slots;
+    // recurrent_events: row lengths of the spikes of step t - 1, counted at
+    // their expansion step like engine.py:366
+    const unsigned long long ev = sh.log_len[pos_mod(t - 1, L)];
+    if (ev) atomicAdd(&ctl->rec_events, ev);
+    sh.log_ctr[pos_mod(t, L)] = 0ull;      // the slot k_stage(t) fills (step t - d_max - 1)
+    sh.tailc[64] = 0u;                     // k_stage(t)'s grid barrier
+    sh.log_len[pos_mod(t, L)] = 0ull;
+    ctl->scratch_used = 0ull;
+    ctl->stream_used = 0ull;
+    sh.tailc[128] = 0u;                    // k_stage's ordered-input record cursor
+    ctl->n_rounds = 0u;
+    ctl->round_next = 0u;
+    sh.tailc[96] = 0u;                     // k_stage's item claims (own L2 line)
+#pragma unroll
+    for (int c = 0; c < CC_ITEM_CLASSES; ++c) ctl->cls_n[c] = 0u;
+}
+
+// Block-wide end of the step's last delivery kernel: the deposited-event count
+// and, in the last block out (step t's inputs are complete then), the overflow
+// records grouped by group for k_plan(t).
+__device__ __forceinline__ void deliver_epilogue(const cc_shard& sh, const ListSet& S,
+                                                 unsigned long long my_ev) {
+    cc_ctl* ctl = sh.ctl;
+    const int lane = threadIdx.x & 31;
+    __shared__ bool am_last;
+    __shared__ unsigned long long blk_ev;
+    if (threadIdx.x == 0) blk_ev = 0ull;
+    __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_ev += __shfl_xor_sync(0xffffffffu, my_ev, o);
+    if (lane == 0 && my_ev) atomicAdd(&blk_ev, my_ev);
+    __syncthreads();
+    if (threadIdx.x == 0 && blk_ev) atomicAdd(&ctl->del_events, blk_ev);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        am_last = atomicAdd(&ctl->done_deliver, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (CC_TIMING_PROBES && (sh.flags & 256) && threadIdx.x == 0) {
+        unsigned long long* d_ = reinterpret_cast<unsigned long long*>(sh.scratch)
+                                 + (size_t)sh.scratch_cap * 7 - 65536ull * 8 - 65536ull * 4 - (size_t)(blockIdx.x + 1);
+        d_[0] = gtimer();
+    }
+    if (!am_last) return;
+    __threadfence();
+    const unsigned m = min(*(volatile unsigned*)S.ovf_cnt, (unsigned)sh.ovf_cap);
+    if (threadIdx.x == 0) {
+        ctl->done_deliver = 0;
+        ctl->ovf_grouped = m;
+        sh.tailc[0] = 0u;                      // k_stage(t) offers step t+1's units
+    }
+    if (m == 0) return;
+    group_overflow(sh, S, m);
+}
+
 // Delivery of arrival step t (pull): the events arriving at t are the delay-d
 // segments of the rows of the spikes of step t - d, d = 1..d_max.  The units
 // of delay >= 2 were already offered to the idle warps of k_stage(t - 1)
@@ -1614,23 +1679,7 @@ k_deliver(const cc_shard sh) {
     if (*(volatile unsigned*)&ctl->error_bits) return;      // failed run: stop working
     const int L = sh.log_slots, D = sh.d_max;
     __shared__ unsigned s_n[DEL_DMAX], s_pre[DEL_DMAX + 1];
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        // recurrent_events: row lengths of the spikes of step t - 1, counted at
-        // their expansion step like engine.py:366
-        const unsigned long long ev = sh.log_len[pos_mod(t - 1, L)];
-        if (ev) atomicAdd(&ctl->rec_events, ev);
-        sh.log_ctr[pos_mod(t, L)] = 0ull;      // the slot k_stage(t) fills (step t - d_max - 1)
-        sh.tailc[64] = 0u;                     // k_stage(t)'s grid barrier
-        sh.log_len[pos_mod(t, L)] = 0ull;
-        ctl->scratch_used = 0ull;
-        ctl->stream_used = 0ull;
-        sh.tailc[128] = 0u;                    // k_stage's ordered-input record cursor
-        ctl->n_rounds = 0u;
-        ctl->round_next = 0u;
-        sh.tailc[96] = 0u;                     // k_stage's item claims (own L2 line)
-#pragma unroll
-        for (int c = 0; c < CC_ITEM_CLASSES; ++c) ctl->cls_n[c] = 0u;
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) deliver_prologue(sh, t);
     // units [0, c) were delivered by k_stage(t - 1)'s idle warps (claimed in
     // order); read by warp 1 while warp 0 builds the unit prefix
     __shared__ unsigned s_c0;
@@ -1695,38 +1744,11 @@ k_deliver(const cc_shard sh) {
         d_[3] = (unsigned long long)smid_ | ((unsigned long long)(n_units - c0) << 32);
     }
 
-    // Step t's inputs are complete now (this kernel is their last depositor):
-    // the last block out groups the overflow records by group for k_plan(t).
-    __shared__ bool am_last;
-    __shared__ unsigned long long blk_ev;
-    if (threadIdx.x == 0) blk_ev = 0ull;
-    __syncthreads();
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) my_ev += __shfl_xor_sync(0xffffffffu, my_ev, o);
-    if (lane == 0 && my_ev) atomicAdd(&blk_ev, my_ev);
-    __syncthreads();
-    if (threadIdx.x == 0 && blk_ev) atomicAdd(&ctl->del_events, blk_ev);
-    if (threadIdx.x == 0) {
-        __threadfence();
-        am_last = atomicAdd(&ctl->done_deliver, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (CC_TIMING_PROBES && (sh.flags & 256) && threadIdx.x == 0) {
-        unsigned long long* d_ = reinterpret_cast<unsigned long long*>(sh.scratch)
-                                 + (size_t)sh.scratch_cap * 7 - 65536ull * 8 - 65536ull * 4 - (size_t)(blockIdx.x + 1);
-        d_[0] = gtimer();
-    }
-    if (!am_last) return;
-    __threadfence();
-    const unsigned m = min(*(volatile unsigned*)S.ovf_cnt, (unsigned)sh.ovf_cap);
-    if (threadIdx.x == 0) {
-        ctl->done_deliver = 0;
-        ctl->ovf_grouped = m;
-        sh.tailc[0] = 0u;                      // k_stage(t) offers step t+1's units
-    }
-    if (m == 0) return;
-    group_overflow(sh, S, m);
+    // Step t's inputs are complete now (this kernel is their last depositor)
+    deliver_epilogue(sh, S, my_ev);
 }
+
+#include "route_kernels.cuh"
 
 // Delay-segment table: dseg[r][d] = synapses of row r with delay <= d,
 // d = 0..d_max (rows sorted by delay).  One warp per row.
@@ -1964,7 +1986,7 @@ extern "C" int32_t CC_V(cc_kernels_per_step)(const cc_shard* sh) {
     const bool fused = (sh->flags & CC_FLAG_PLAN_FUSED) ||
                        (!(sh->flags & CC_FLAG_PLAN_SEPARATE) &&
                         sh->n_groups > stage_blocks_(sh->d_max) * STAGE_WARPS);
-    return fused ? 2 : 3;
+    return (fused ? 2 : 3) + (sh->l1_cnt ? 1 : 0);
 }
 
 extern "C" int CC_V(cc_build_dseg)(const int64_t* row_off, const uint8_t* syn_d, int64_t n_rows,
@@ -1986,10 +2008,32 @@ extern "C" int CC_V(cc_init_state)(const cc_shard* sh, void* stream) {
     return cc_check_launch("k_init_state");
 }
 
+static int bin_blocks_per_sm = 0;
+extern "C" int CC_V(cc_prepare)(void);
+
 extern "C" int CC_V(cc_deliver)(const cc_shard* sh, void* stream) {
     if (!sh) return cc_set_error("cc_deliver: null shard");
-    k_deliver<<<sm_count() * CC_DEL_MINB, CC_DEL_THREADS, 0, (cudaStream_t)stream>>>(*sh);
-    return cc_check_launch("k_deliver");
+    if (!sh->l1_cnt) {
+        k_deliver<<<sm_count() * CC_DEL_MINB, CC_DEL_THREADS, 0, (cudaStream_t)stream>>>(*sh);
+        return cc_check_launch("k_deliver");
+    }
+    // routed delivery: regions of 2^l1_rb neurons
+    if (sh->l1_rb < 5 || sh->l1_rb > 16 || sh->n_regions < 1 ||
+        sh->n_regions > CC_L1_MAX_REGIONS ||
+        (long long)sh->n_regions << sh->l1_rb < (long long)sh->n_local ||
+        (NSUB << (sh->l1_rb - 5)) > CC_L1_MAX_LISTS || sh->l1_cap < 1 ||
+        sh->l1_cap >= (1ll << 32) || !sh->l1_ref || !sh->l1_w || !sh->l1_tgt)
+        return cc_set_error("cc_deliver: routed delivery needs 5 <= l1_rb <= 16, n_regions = "
+                            "ceil(n_local / 2^l1_rb) <= %d, at most %d lists per region, "
+                            "l1_cap < 2^32 and the region arrays",
+                            CC_L1_MAX_REGIONS, CC_L1_MAX_LISTS);
+    if (const int rc = CC_V(cc_prepare)()) return rc;
+    k_route<<<CC_RT_BLOCKS ? CC_RT_BLOCKS : sm_count() * CC_RT_MINB, RT_THREADS, route_smem_bytes(),
+              (cudaStream_t)stream>>>(*sh);
+    if (const int rc = cc_check_launch("k_route")) return rc;
+    k_bin<<<sm_count() * bin_blocks_per_sm, BN_THREADS, bin_smem_bytes(),
+            (cudaStream_t)stream>>>(*sh);
+    return cc_check_launch("k_bin");
 }
 
 // One-time kernel attributes (not settable inside a CUDA graph capture, so done
@@ -2009,6 +2053,15 @@ extern "C" int CC_V(cc_prepare)(void) {
         cudaFuncSetAttribute(k_stage<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)stage_smem(DEL_DMAX - 1)) != cudaSuccess)
         return cc_set_error("cc_prepare: %s", cudaGetErrorString(cudaGetLastError()));
+    if (cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)route_smem_bytes()) != cudaSuccess ||
+        cudaFuncSetAttribute(k_bin, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)bin_smem_bytes()) != cudaSuccess)
+        return cc_set_error("cc_prepare (routed delivery): %s",
+                            cudaGetErrorString(cudaGetLastError()));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bin_blocks_per_sm, k_bin, BN_THREADS,
+                                                  bin_smem_bytes());
+    if (bin_blocks_per_sm < 1) bin_blocks_per_sm = 1;
     // (filled here, outside any stream capture; the tail tables grow by 16 B
     // per two delay steps, so the occupancy changes at a few d_max values only)
     int per_sm[2] = {0, 0};

@@ -34,6 +34,8 @@ MASK64 = (1 << 64) - 1
 DOMAIN = 0x636F727469636172
 # shards of at least this many neurons deliver with 16 lanes per spike (see Shard setup)
 DEL_WIDE_NEURONS = 2_000_000
+ROUTED_DEFAULT = True          # routed delivery in the high-rate regime (Simulator)
+L1_TARGET_REGIONS = 1024       # routed delivery: regions grow from 1024 neurons to stay below this
 P_INIT_STATE, P_EXTERNAL, P_EXTERNAL_TIME = 4, 5, 7
 
 
@@ -149,7 +151,8 @@ class Simulator:
                  use_graphs: bool = True, direct_log: Optional[bool] = None,
                  remote=None,
                  raster_steps: Optional[int] = None, substeps: bool = False, device=None,
-                 capacity=None, sublists: Optional[int] = None):
+                 capacity=None, sublists: Optional[int] = None,
+                 routed: Optional[bool] = None):
         import torch
         self.L = _lib.lib()
         self.torch = torch
@@ -253,6 +256,34 @@ class Simulator:
             ctl=T.zeros(C.sizeof(_lib.Ctl) // 8, dtype=i64, device=dev),
             tailc=T.zeros(256, dtype=i32, device=dev),
         )
+        # Routed (two-pass) delivery (csrc/route_kernels.cuh): the step's arrivals
+        # go first to one record array per region of 2^rb consecutive neurons,
+        # then from there to the input lists, both passes sorting tiles in shared
+        # memory and copying whole runs instead of one scattered store per event.
+        # It pays at the paper's event volumes (the high-rate regime, where the
+        # sub-lists are on as well); below, k_deliver's single pass is faster.
+        # CC_ROUTED=0/1 overrides.
+        if routed is None:
+            env = os.environ.get("CC_ROUTED", "")
+            routed = bool(int(env)) if env else ROUTED_DEFAULT and n_sub > 1
+        self.routed = bool(routed)
+        if self.routed:
+            rb_max = 15 - (n_sub.bit_length() - 1)       # lists per region <= CC_L1_MAX_LISTS
+            rb = int(os.environ.get("CC_L1_RB", "0")) or 11
+            while rb < rb_max and -(-n_local // (1 << rb)) > L1_TARGET_REGIONS:
+                rb += 1
+            n_regions = -(-n_local // (1 << rb))
+            if rb > rb_max or n_regions > _lib.L1_MAX_REGIONS:
+                raise MemoryBudgetError(f"routed delivery: {n_local} neurons need more than "
+                                        f"{_lib.L1_MAX_REGIONS} regions")
+            # records per region and step: half the list capacity of its groups
+            l1_cap = (int(os.environ.get("CC_L1_CAP", "0")) or
+                      max(4096, (1 << (rb - 5)) * step_cap // 2)) * cap["ovf"]
+            self.buf.update(
+                l1_cnt=T.zeros(2 * n_regions * _lib.L1_STRIDE, dtype=i32, device=dev),
+                l1_ref=T.empty((n_regions, l1_cap), dtype=i32, device=dev),
+                l1_w=T.empty((n_regions, l1_cap), dtype=i32, device=dev),
+                l1_tgt=T.empty((n_regions, l1_cap), dtype=T.int16, device=dev))
         self.probes = None if probes is None else np.asarray(probes, np.int64)
         n_probe = 0 if self.probes is None else len(self.probes)
         if n_probe:
@@ -268,6 +299,12 @@ class Simulator:
         sh.n_groups, sh.bin_pad = n_groups, bin_pad
         sh.n_sub = n_sub
         sh.flags = int(os.environ.get("CC_FLAGS", "0"))    # CC_FLAG_* (measurement / tests)
+        if self.routed:
+            sh.l1_rb, sh.n_regions, sh.l1_cap = rb, n_regions, l1_cap
+            for k in ("l1_cnt", "l1_ref", "l1_w", "l1_tgt"):
+                setattr(sh, k, b[k].data_ptr())
+            # the tail delivery's scattered deposits are what this mode avoids
+            sh.flags |= _lib.FLAG_NO_TAIL_DELIVERY
         sh.spk_cap, sh.seg_stride = spk_cap, seg_stride
         # delivery lanes per spike: 16 on shards of >= 2 M neurons (config 3 gaussian: k_deliver
         # 448 -> 367 us, step -3.3 %), 8 below (configs 1, 2 and the config-4 GPU block: 16 lanes are ~1 % slower);
@@ -354,6 +391,10 @@ class Simulator:
     def _launch_step(self, stream) -> None:
         _lib.check(self.L.cc_deliver(C.byref(self.shard), stream), "cc_deliver")
         _lib.check(self.L.cc_neuron_step(C.byref(self.shard), stream), "cc_neuron_step")
+
+    def kernels_per_step(self) -> int:
+        """Kernels cc_deliver + cc_neuron_step launch per step for this shard."""
+        return int(self.L.cc_kernels_per_step(C.byref(self.shard)))
 
     def ctl(self) -> _lib.Ctl:
         raw = self.buf["ctl"].cpu().numpy().tobytes()

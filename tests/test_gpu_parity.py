@@ -276,6 +276,79 @@ def test_sublists_by_lane_range_same_run(cuda, name, flags, monkeypatch):
     _assert_same_run(res, meta, arr)
 
 
+@pytest.mark.parametrize("name", ["config0_cal", "tiny_exp", "tiny_gauss_long"])
+@pytest.mark.parametrize("sublists", ["1", "8"])
+@pytest.mark.parametrize("rb", ["5", "10"])
+def test_routed_delivery_same_run(cuda, name, sublists, rb, monkeypatch):
+    """Routed delivery (k_route to per-region record arrays, k_bin from there
+    to the input lists; regions of 32 or 1024 neurons) reproduces the
+    reference run with either list variant; every arrival goes through it."""
+    from paper_1803_08833_b200.engine import Simulator, run_b200
+    from paper_1803_08833_b200.network import build_b200
+    cfg, meta, arr = golden_run(name)
+    monkeypatch.setenv("CC_ROUTED", "1")
+    monkeypatch.setenv("CC_L1_RB", rb)
+    monkeypatch.setenv("CC_SUBLISTS", sublists)
+    res = run_b200(cfg, 1)
+    _assert_same_run(res, meta, arr)
+    sim = Simulator(cfg, build_b200(cfg))
+    assert sim.routed and sim.shard.l1_rb == int(rb)
+    assert sim.kernels_per_step() == Simulator(cfg, sim.net, routed=False).kernels_per_step() + 1
+    sim.advance(cfg.n_steps)
+    c = sim.ctl()
+    # (rec_events counts a spike's whole row at its expansion, engine.py:366;
+    # the later delays of the last steps' spikes are never delivered)
+    assert c.tail_events == 0 and c.rec_events == meta["recurrent_events"]
+    assert 0.9 * c.rec_events < c.del_events <= c.rec_events
+
+
+def test_routed_delivery_list_overflow_and_region_capacity(cuda, monkeypatch):
+    """Routed delivery with 2-record input lists (k_bin's overflow path) gives
+    the reference raster; a region array too small for a step's records stops
+    the run with the capacity error of the step instead of dropping records."""
+    from paper_1803_08833_b200 import _lib
+    from paper_1803_08833_b200.engine import Simulator, run_b200
+    from paper_1803_08833_b200.network import build_b200
+    cfg, meta, arr = golden_run("tiny_gauss_long")
+    monkeypatch.setenv("CC_ROUTED", "1")
+    res = run_b200(cfg, 1, bin_cap=2)
+    assert res.device_stats["overflow"] > 0
+    _assert_same_run(res, meta, arr)
+    monkeypatch.setenv("CC_L1_RB", "5")           # 12 regions of 32 neurons
+    monkeypatch.setenv("CC_L1_CAP", "16")
+    sim = Simulator(cfg, build_b200(cfg), use_graphs=False)
+    with pytest.raises(_lib.EngineError, match="step") as ei:
+        sim.advance(cfg.n_steps)
+    assert ei.value.bits & 0x04 and _lib.capacity_error(ei.value)
+    # run_b200 re-runs with the region arrays doubled until they fit
+    _assert_same_run(run_b200(cfg, 1), meta, arr)
+
+
+def test_routed_delivery_agrees_at_the_stress_point(cuda, monkeypatch):
+    """A 12x12 exponential grid at the 200 Hz stress drive (~10 M recurrent
+    events per step: every k_route block stages several full tiles per step,
+    every region many k_bin tiles): routed and direct delivery give the same
+    raster, spike for spike, and the same event counts."""
+    from dataclasses import replace
+    from paper_1803_08833_b200.engine import run_b200
+    from paper_1803_08833_b200.network import build_b200
+    from paper_1803_08833_b200.presets import baseline_config
+    from paper_1803_08833_b200.spec import GridSpec
+    cfg = baseline_config(2, "stress", duration_s=0.05)
+    cfg = replace(cfg, grid=GridSpec(nx=12, ny=12, neurons_per_column=1240,
+                                     excitatory_fraction=0.8, spacing_alpha=100.0))
+    net = build_b200(cfg)
+    monkeypatch.setenv("CC_ROUTED", "0")
+    a = run_b200(cfg, 1, net=net)
+    monkeypatch.setenv("CC_ROUTED", "1")
+    b = run_b200(cfg, 1, net=net)
+    assert a.n_spikes == b.n_spikes > 100_000
+    assert a.recurrent_events == b.recurrent_events > 2e8
+    assert a.raster_checksum == b.raster_checksum
+    assert np.array_equal(a.raster_gids, b.raster_gids)
+    assert np.array_equal(a.raster_times.view(np.uint64), b.raster_times.view(np.uint64))
+
+
 def test_planning_modes_agree_at_scale(cuda, monkeypatch):
     """10x10 columns (3,875 groups > k_stage's warps: planning inside k_stage by
     default) - the same raster as with the separate k_plan kernel."""
@@ -714,7 +787,17 @@ out["overflow"] = same(run_b200(cfg, 1, bin_cap=2), meta, arr)
 os.environ["CC_SUBLISTS"] = "8"
 out["sublists8"] = same(run_b200(cfg, 1), meta, arr)
 out["sublists8/overflow"] = same(run_b200(cfg, 1, bin_cap=2), meta, arr)
+os.environ["CC_ROUTED"] = "1"          # (this variant: 1024-event k_route tiles on 3 blocks)
+out["sublists8/routed"] = same(run_b200(cfg, 1), meta, arr)
+out["sublists8/routed/overflow"] = same(run_b200(cfg, 1, bin_cap=2), meta, arr)
 del os.environ["CC_SUBLISTS"]
+os.environ["CC_L1_RB"] = "5"
+out["routed/rb5"] = same(run_b200(cfg, 1), meta, arr)
+del os.environ["CC_L1_RB"]
+for name in ("tiny_exp", "config0_cal_0p1"):
+    c2, m2, a2 = golden_run(name)
+    out["routed/" + name] = same(run_b200(c2, 1), m2, a2)
+del os.environ["CC_ROUTED"]
 cfg, meta, arr = golden_run("tiny_gauss")
 out["p2p_local_3"] = same(run_local_shards(cfg, 3, transport="p2p"), meta, arr)
 out["slots_local_4"] = same(run_local_shards(cfg, 4), meta, arr)
