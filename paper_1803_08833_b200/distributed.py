@@ -769,10 +769,14 @@ def _rank_run(config, rank: int, size: int, transport: str, group, nccl_group=No
 
 
 def _spawn_worker(rank: int, size: int, port: int, config, transport: str, chunk: int, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
-    dist.init_process_group("gloo", rank=rank, world_size=size)
+    # own rendezvous: a parent started by torchrun hands down
+    # TORCHELASTIC_USE_AGENT_STORE, with which rank 0 would connect to the
+    # agent's store instead of starting this one
+    os.environ.pop("TORCHELASTIC_USE_AGENT_STORE", None)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=size)
     try:
         nccl_group = None
         if transport == "nccl":

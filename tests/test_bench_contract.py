@@ -146,3 +146,49 @@ def test_bench_line_contract():
     assert line["clocks"]["sm_mhz"] > 0
     # the device-timed value replays warm graphs: not below the end-to-end rate
     assert line["value"] >= 0.9 * e["value"]
+
+
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _torchrun_bench(n, *argv, timeout=900, env=None):
+    """bench.py under the driver's launch command for N > 1."""
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", str(n), "--master-addr", "127.0.0.1",
+                        "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+                        "--gpus", str(n), *argv],
+                       capture_output=True, text=True, timeout=timeout, cwd=ROOT,
+                       env=dict(os.environ, **(env or {})))
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, p.stdout                   # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+@pytest.mark.gpu
+def test_bench_under_torchrun_two_ranks():
+    """The driver's N = 2 launch on a one-GPU box: the two ranks share cuda:0
+    (host-synchronised peer exchange), rank 0 prints the line with the
+    exchange figures; config 1 split into two 4x8 column blocks."""
+    line = _torchrun_bench(2, "--config", "1", "--steps", "100", "--warmup", "10")
+    assert line["n_gpus"] == 2 and line["steps"] == 100 and line["scaling"] == "strong"
+    assert line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["config"]["neurons"] == 79360
+    assert 0 <= line["exchange_fraction"] < 1
+    assert line["exchange"]["per_rank_bytes_per_step_max"] > 0
+    assert line["gpu_launches"] >= 3 * 100
+    assert 0 < line["roofline"]["frac"] <= 1
+
+
+def test_reference_arm_under_torchrun_two_ranks():
+    """--impl reference under torchrun: rank 0 alone runs the CPU oracle and
+    prints; the other rank exits 0 without work."""
+    line = _torchrun_bench(2, "--impl", "reference", "--config", "0", "--grid", "2x1",
+                           "--steps", "4", "--warmup", "3", env={"CC_REF_BUDGET_S": "120"})
+    assert line["impl"] == "reference" and line["n_gpus"] == 2
+    assert line["cpu_baseline"]["value"] == line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
