@@ -885,19 +885,51 @@ def bench_distributed(args, cfg) -> Optional[dict]:
     """bench.py under torchrun (N > 1) or with --exchange on one GPU (loopback):
     K steps timed with CUDA events on every rank (max over ranks); rank 0
     returns the JSON line."""
+    import sys
     import torch
     import torch.distributed as dist
+    from . import _lib
     rank, size = _init_dist()
     group = dist.new_group(backend="gloo")
     transport = getattr(args, "transport", "p2p")
-    nccl_group = dist.new_group(backend="nccl") if transport == "nccl" else None
     dev_idx, sync = _pick_device(rank, size)
     torch.cuda.set_device(dev_idx)
     loop = size == 1
-    ds = DistributedSimulator(cfg, rank, size, device=f"cuda:{dev_idx}", group=group,
-                              nccl_group=nccl_group, transport=transport, sync=sync,
-                              loopback=loop, raster_steps=args.steps + 100)
-    ds.advance(args.warmup)
+
+    def start(tr):
+        """Shard + exchange over transport `tr`, warmed up; None (on every
+        rank) if any rank's exchange failed during the warm-up."""
+        nccl_group = dist.new_group(backend="nccl") if tr == "nccl" else None
+        d, ok = None, 1
+        try:
+            d = DistributedSimulator(cfg, rank, size, device=f"cuda:{dev_idx}", group=group,
+                                     nccl_group=nccl_group, transport=tr, sync=sync,
+                                     loopback=loop, raster_steps=args.steps + 100)
+            d.advance(args.warmup)
+            if tr == "p2p" and os.environ.get("CC_TEST_P2P_FAIL"):      # tests
+                raise _lib.EngineError("step 0: injected peer-exchange failure", 0x400)
+        except _lib.EngineError as err:
+            if not (err.bits & (0x400 | 0x800)):                         # not the exchange
+                raise
+            print(f"[bench] rank {rank}: {tr} exchange failed ({err})", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int64)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if int(flag.item()):
+            return d
+        if d is not None:
+            d.close()
+        return None
+
+    # the peer-store exchange is the product path; if its flags do not cross
+    # between the GPUs of this box (CC_ERR_XWAIT on some rank during the
+    # warm-up) the run falls back to the NCCL slots transport and says so
+    ds = start(transport)
+    if ds is None and transport == "p2p" and sync == "device":
+        transport = "nccl"
+        ds = start(transport)
+    if ds is None:
+        raise RuntimeError("bench: the spike exchange failed on every transport")
     # one warm replay of the chunk graph outside the timed region
     if sync == "device" and args.steps >= ds.chunk:
         ds.advance(ds.chunk)

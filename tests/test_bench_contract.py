@@ -192,3 +192,17 @@ def test_reference_arm_under_torchrun_two_ranks():
     assert line["impl"] == "reference" and line["n_gpus"] == 2
     assert line["cpu_baseline"]["value"] == line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+def test_bench_exchange_falls_back_to_nccl(monkeypatch):
+    """A peer-store exchange that fails during the warm-up (injected on every
+    rank here; CC_ERR_XWAIT on a box whose GPUs cannot reach each other's
+    windows) makes the multi-GPU bench fall back to the NCCL slots transport,
+    and the line says which transport ran."""
+    line = _run_bench("--exchange", "--steps", "100", "--warmup", "10",
+                      env={"CC_TEST_P2P_FAIL": "1"})
+    assert "nccl exchange" in line["config"]["parallelism"]
+    assert line["value"] > 0 and 0 <= line["exchange_fraction"] < 1
+    line = _run_bench("--exchange", "--steps", "100", "--warmup", "10")
+    assert "p2p exchange" in line["config"]["parallelism"]
