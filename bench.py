@@ -381,9 +381,10 @@ def _bench_single(args, cfg, net, capacity):
     def instrumented(debug: int):
         timer = C.c_void_p()
         _lib.check(L.cc_timer_create(3 * NI, C.byref(timer)))
-        sim.shard.flags = debug
+        base_flags = sim.shard.flags                   # (routed delivery: no tail delivery)
+        sim.shard.flags = base_flags | debug
         g_t = sim.capture(NI, timer=timer)
-        sim.shard.flags = 0
+        sim.shard.flags = base_flags
         ca = sim.check(collect_raster=False)
         g_t.replay()
         torch.cuda.synchronize(dev)
@@ -413,6 +414,9 @@ def _bench_single(args, cfg, net, capacity):
             prof_d = json.load(open(prof)).get(key, {})
             # the roofline kernel is replay (b)'s k_deliver: its ncu DRAM bytes
             traffic = prof_d.get("k_deliver_b", {}).get("dram_bytes_per_launch")
+            if traffic is None and "k_route_b" in prof_d:         # routed delivery: both passes
+                traffic = (prof_d["k_route_b"]["dram_bytes_per_launch"]
+                           + prof_d.get("k_bin_b", {}).get("dram_bytes_per_launch", 0.0))
             stage_ncu = prof_d.get("k_stage", {})
         except Exception:
             traffic = None
@@ -459,7 +463,7 @@ def _bench_single(args, cfg, net, capacity):
             "kernel": "k_plan + k_stage (k_neuron)", "share": neu_ms / (del_ms + neu_ms),
             "inputs_per_s": run_a["ev"] / NI / (neu_ms / NI / 1e3),
             "bound": "fp64 latency / issue: per input 2 exp, 1 expm1, 4 divides, the "
-                     "exact ordering and a serial in-order update; 20 resident warps/SM",
+                     "exact ordering and a serial in-order update; 24 resident warps/SM",
             "k_stage_ncu": {k: stage_ncu[k] for k in ("warp_instructions", "ipc_per_sm",
                                                         "warps_active_per_sm",
                                                         "dram_bytes_per_launch", "source")

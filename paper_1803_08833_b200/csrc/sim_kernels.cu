@@ -52,6 +52,12 @@
 #ifndef CC_TAIL_STOP
 #define CC_TAIL_STOP 10
 #endif
+#ifndef CC_BALANCED_ITEMS
+#define CC_BALANCED_ITEMS 0  // k_plan: a group's work items of about equal size (measured: no gain)
+#endif
+#ifndef CC_REFR_BOOST
+#define CC_REFR_BOOST 2      // queue classes a group with a refractory neuron moves up
+#endif
 #ifndef CC_CSR_STREAM
 #define CC_CSR_STREAM 0
 #endif
@@ -803,7 +809,17 @@ __device__ __forceinline__ void plan_group(const cc_shard& sh, long long t, int 
     uint32_t gtot;
     const uint32_t excl = warp_excl_scan(nn, gtot);
     const uint32_t incl = excl + nn;
-    const uint32_t thr = excl + (uint32_t)NEURON_WCAP;
+    // item size limit: NEURON_WCAP, or (CC_BALANCED_ITEMS) the group's total
+    // split evenly over the fewest items that hold it, plus one neuron's worth
+    // of slack so that whole lanes still pack into that many items - a 415-input
+    // group becomes ~230 + ~185 instead of ~250 + ~165, and the longest item of
+    // a round of items (which every warp of the round waits behind) is shorter
+    uint32_t icap = (uint32_t)NEURON_WCAP;
+    if (CC_BALANCED_ITEMS && gtot > (uint32_t)NEURON_WCAP) {
+        const uint32_t k = (gtot + NEURON_WCAP - 1) / NEURON_WCAP;
+        icap = min(icap, (gtot + k - 1) / k + nmax);
+    }
+    const uint32_t thr = excl + icap;
     int lo = lane + 1, hi = 32;
 #pragma unroll
     for (int it = 0; it < 6; ++it) {
@@ -832,11 +848,23 @@ __device__ __forceinline__ void plan_group(const cc_shard& sh, long long t, int 
     __syncthreads();
     int cls = 0;
     unsigned local = 0;
+    // a neuron inside its refractory window at the step start takes the slow
+    // step of the update for every input before the window ends (measured at
+    // config 1: +0.38 us per slow step on a 9 us group update; the last groups
+    // to finish were those of second-round items with 15-25 slow steps):
+    // such groups move CC_REFR_BOOST classes up, so their updates start early
+    bool boost = false;
+    if (CC_REFR_BOOST > 0) {
+        const bool refr = active && nn > 0 &&
+                          sh.state[(size_t)li * 4 + 3] > (double)t * sh.dt;
+        boost = __any_sync(0xffffffffu, refr);
+    }
     if (lane < ni) {
         // class by the GROUP's input total: all items of a heavy group are
         // claimed early, so its (long) in-order update does not start last
         cls = CC_ITEM_CLASSES - 1 - (int)min(gtot / (uint32_t)NEURON_WCAP,
                                              (uint32_t)(CC_ITEM_CLASSES - 1));
+        if (boost) cls = max(cls - CC_REFR_BOOST, 0);
         local = atomicAdd(&blk_cls[cls], 1u);
     }
     if (lane == 0) {
@@ -935,7 +963,9 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 
 __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long long t, int e_t,
                                              double2* S, uint32_t& my_spikes,
-                                             const double2* xt) {
+                                             const double2* xt,
+                                             [[maybe_unused]] unsigned long long* dbg_info = nullptr) {
+    [[maybe_unused]] unsigned dbg_slow = 0, dbg_spk = 0;
     cc_ctl* ctl = sh.ctl;
     const int lane = threadIdx.x & 31;
     const int li = li0 + lane;
@@ -1028,8 +1058,10 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
                 const double V = Vt + wv;
                 if (V > P->V_theta) spike = true; else s.V = V;
             } else {
+                if (CC_TIMING_PROBES) ++dbg_slow;
                 spike = slow_step(s, *P, tj, stale, cflag, em, ec, f, ecr, wv, xt);
             }
+            if (CC_TIMING_PROBES && spike) ++dbg_spk;
             if (spike) {                             // strict threshold crossed
                 s.V = P->V_r;
                 s.c = s.c + P->alpha_c;
@@ -1062,6 +1094,13 @@ __device__ __forceinline__ void update_group(const cc_shard& sh, int li0, long l
     if (n) {
         reinterpret_cast<double2*>(st)[0] = make_double2(s.V, s.c);
         reinterpret_cast<double2*>(st)[1] = make_double2(s.last, s.ru);
+    }
+    if (CC_TIMING_PROBES && dbg_info) {
+        // nmax | max slow steps of a lane << 16 | lanes with slow steps << 32 | spikes << 48
+        const unsigned lanes_slow = __popc(__ballot_sync(0xffffffffu, dbg_slow > 0));
+        const unsigned nspk = __popc(__ballot_sync(0xffffffffu, dbg_spk > 0));
+        *dbg_info = (unsigned long long)nmax | ((unsigned long long)warp_max_u32(dbg_slow) << 16) |
+                    ((unsigned long long)lanes_slow << 32) | ((unsigned long long)nspk << 48);
     }
 }
 
@@ -1458,8 +1497,10 @@ k_stage(const cc_shard sh) {
             __threadfence();
             if (lane == 0) sh.grp_done[group] = 0u;
             CC_DBG(5, gtimer());                       // update start (0: no update)
+            unsigned long long dbg_info = 0ull;
             update_group(sh, li0, t, t_mod_l, reinterpret_cast<double2*>(nsm + wib * stage_warp_bytes()),
-                         my_spikes, s_xt);
+                         my_spikes, s_xt, &dbg_info);
+            CC_DBG(1, dbg_info | (1ull << 63));        // (probe runs: overwrites "gathered")
         }
         {
             CC_DBG(4, gtimer());

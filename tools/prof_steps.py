@@ -42,7 +42,7 @@ while True:                      # onset bursts: grow the overflowed buffer (run
             raise
         del sim
         torch.cuda.empty_cache()
-sim.shard.flags = a.flags
+sim.shard.flags |= a.flags          # (keeps the routed mode's no-tail-delivery flag)
 s = torch.cuda.current_stream().cuda_stream
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
