@@ -2,7 +2,7 @@
 oracle (numpy port of the reference loop, pinned to the reference's own
 fixtures) on the same connectivity, over the config's whole duration.
 
-    python tools/long_parity.py [CONFIG] [DURATION_S] [SHARDS]
+    python tools/long_parity.py [CONFIG] [DURATION_S] [SHARDS] [REGIME]
 
 SHARDS > 1 runs the multi-shard path (distributed.run_local_shards: W column
 blocks with their own generator, spike exchange by device copies) on one GPU.
@@ -28,7 +28,8 @@ def main():
     idx = int(sys.argv[1]) if len(sys.argv) > 1 else 1
     dur = float(sys.argv[2]) if len(sys.argv) > 2 and float(sys.argv[2]) > 0 else None
     shards = int(sys.argv[3]) if len(sys.argv) > 3 else 1
-    cfg = baseline_config(idx, "calibrated", duration_s=dur)
+    regime = sys.argv[4] if len(sys.argv) > 4 else "calibrated"
+    cfg = baseline_config(idx, regime, duration_s=dur)
     net = build_b200(cfg)
     t0 = time.perf_counter()
     if shards > 1:
@@ -64,10 +65,16 @@ def main():
                external_events=[int(res.external_events), ref["external_events"]],
                raster_checksum=f"0x{res.raster_checksum:016x}", gpu_wall_s=gpu_s,
                oracle_wall_s=cpu_s, oracle_processes=k,
-               mean_rate_hz=res.mean_rate_hz)
+               mean_rate_hz=res.mean_rate_hz, regime=regime,
+               device_stats={k_: v for k_, v in (res.device_stats or {}).items()
+                             if not isinstance(v, dict)},
+               delivery=("routed (k_route + k_bin), 8 sub-lists"
+                         if os.environ.get("CC_ROUTED", "") != "0" and regime == "stress"
+                         else "k_deliver"))
     print(json.dumps(out))
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    name = f"long_parity_config{idx}" + (f"_{shards}shards" if shards > 1 else "")
+    name = (f"long_parity_config{idx}" + (f"_{shards}shards" if shards > 1 else "")
+            + ("" if regime == "calibrated" else f"_{regime}"))
     with open(os.path.join(ROOT, "gpurun_out", name + ".json"), "w") as fh:
         json.dump(out, fh, indent=1)
     ok = same_g and same_t and out["recurrent_events"][0] == out["recurrent_events"][1] \

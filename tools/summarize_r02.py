@@ -78,7 +78,7 @@ if os.path.exists(lc):
             k = k.split("<")[0]
         agg[k][0] += 1
         agg[k][1] += float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1)
-    step = {k: v for k, v in agg.items() if k in ("k_deliver", "k_plan", "k_stage", "k_xingest")}
+    step = {k: v for k, v in agg.items() if k in ("k_deliver", "k_route", "k_bin", "k_plan", "k_stage", "k_xingest")}
     tot = sum(v[1] for v in step.values()) or 1
     lines.append("\n## launch list (bench command `--steps 20 --warmup 30`, from t = 0: onset "
                  "steps included; serialised, cold cache: compare shares)\n\n"
