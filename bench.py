@@ -509,7 +509,30 @@ def _bench_single(args, cfg, net, capacity):
         # advance(K) - pipelined chunk graphs, per-chunk counter checks, error
         # checks and the raster's device->host copies (the expansion-time event
         # count of the onset's first steps stays out of both numbers)
-        sim2 = Simulator(cfg, net, chunk=min(args.chunk, K), raster_steps=K, capacity=capacity)
+        # ... on connectivity uploaded from the host in the reference's own store
+        # layout (import_csr: the "given the reference-generated connectivity"
+        # entry), when the host copy is small enough to make here: a one-time
+        # host->device copy, reported beside the per-step figures
+        net2, conn = net, {"source": "generated on the device from the seed (build_b200)",
+                           "h2d_bytes_once": 0}
+        if net.n_synapses <= int(os.environ.get("CC_E2E_IMPORT_MAX", "300000000")):
+            from paper_1803_08833_b200.network import export_csr, import_csr
+            store = export_csr(net)
+            torch.cuda.synchronize(dev)
+            i0 = time.perf_counter()
+            net2 = import_csr(cfg, store["sources"], store["offsets"], store["target_local"],
+                              store["delay"], store["weight"])
+            torch.cuda.synchronize(dev)
+            imp_s = time.perf_counter() - i0
+            if net2.checksum != net.checksum:
+                raise RuntimeError("import_csr: construction checksum differs from the generator's")
+            conn = {"source": "import_csr(host store in the reference's IncomingSynapses layout, "
+                              "network.py:114-152); checksum equal to the device generator's",
+                    "h2d_bytes_once": int(8 * (cfg.grid.n_neurons + 1) + 13 * net.n_synapses
+                                          + 4 * len(store["sources"])),
+                    "import_seconds": imp_s}
+            del store
+        sim2 = Simulator(cfg, net2, chunk=min(args.chunk, K), raster_steps=K, capacity=capacity)
         sim2.advance(W)
         ca = sim2.check()
         torch.cuda.synchronize(dev)
@@ -525,8 +548,10 @@ def _bench_single(args, cfg, net, capacity):
                        "d2h_bytes_per_step": (12 * n_sp + C.sizeof(_lib.Ctl) * n_chunks) / K,
                        "api": "paper_1803_08833_b200.Simulator.advance(K) wall after advance(W) "
                               "(the step loop of run_b200)",
-                       "steps": K, "warmup": W}
-        del sim2
+                       "steps": K, "warmup": W, "connectivity": conn}
+        if "import_seconds" in conn:
+            line["e2e"]["value_including_import"] = ev / (wall + conn["import_seconds"])
+        del sim2, net2
     if not args.no_cpu:
         cb = cpu_oracle_sample(cfg, net, float(os.environ.get("CC_CPU_BUDGET_S", "20")), 10 ** 9)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}

@@ -208,15 +208,32 @@ def import_csr(cfg, sources, offsets, target_local, delay, weight, rank: int = 0
         raise ValueError("sources must be strictly ascending")
     S = int(offsets[-1]) if len(offsets) else 0
     row_off = torch.from_numpy(row_off_h).to(dev)
-    syn_tgt = torch.from_numpy(np.asarray(target_local, np.int64).astype(np.int32)).to(dev)
-    syn_w = torch.from_numpy(np.asarray(weight, np.float32)).to(dev)
-    syn_d = torch.from_numpy(np.asarray(delay, np.int64).astype(np.uint8)).to(dev)
+
+    def up(a, narrow):
+        """Host array -> device in its own width (no widened host copy); the
+        reference store holds u32 targets, u16 delays, f32 weights."""
+        a = np.ascontiguousarray(a)
+        if a.dtype.kind == "u" and a.dtype.itemsize in (2, 4):     # torch has no u16 / u32
+            a = a.view(np.int16 if a.dtype.itemsize == 2 else np.int32)
+        t = torch.from_numpy(a).to(dev)
+        return t if t.dtype == narrow else t.to(narrow)
+
     if len(delay) and int(np.max(delay)) > cfg.genspec.d_max_steps:
         raise ValueError("imported delay exceeds d_max")
+    if len(target_local) and int(np.max(target_local)) >= len(owned) * grid.neurons_per_column:
+        raise ValueError("imported target index outside the shard")
+    syn_tgt = up(target_local, torch.int32)
+    syn_w = up(weight, torch.float32)
+    syn_d = up(delay, torch.uint8)
     n = grid.neurons_per_column
-    tgt_global = torch.from_numpy(
-        (owned[np.asarray(target_local, np.int64) // n] * n
-         + np.asarray(target_local, np.int64) % n).astype(np.int32)).to(dev)
+    # global target gid of every synapse (construction checksum), on the device
+    # in pieces of 64 M synapses
+    owned_t = torch.from_numpy(np.asarray(owned, np.int64)).to(dev)
+    tgt_global = torch.empty(S, dtype=torch.int32, device=dev)
+    for a0 in range(0, S, 1 << 26):
+        tl = syn_tgt[a0:a0 + (1 << 26)].to(torch.int64)
+        tgt_global[a0:a0 + (1 << 26)] = (owned_t[tl // n] * n + tl % n).to(torch.int32)
+    del owned_t
     src_t = torch.from_numpy(sources.astype(np.uint32).view(np.int32)).to(dev)
     csum = torch.zeros(1, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev).cuda_stream

@@ -140,6 +140,10 @@ def test_bench_line_contract():
     # the inputs are the config and seed (network and drive are generated on the
     # device); the raster and the per-chunk counters come back every step
     assert e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] > 0
+    # the end-to-end run steps on connectivity uploaded from a host store in the
+    # reference's layout (import_csr): a one-time copy, reported as such
+    assert e["connectivity"]["h2d_bytes_once"] > 13 * 94_000_000
+    assert 0 < e["value_including_import"] < e["value"]
     c = line["cpu_baseline"]
     assert c["kind"] == "port" and c["cores"] == 1 and c["value"] > 0
     assert line["gpu_launches"] >= 3 * 20               # k_deliver, k_plan, k_stage per step
