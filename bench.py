@@ -12,7 +12,14 @@ drive are generated on the device from the seed (bit-exact with the
 reference's streams); timing excludes construction like the reference's
 normalized cost (metrics.py:114-123).
 
-value      = (recurrent + external events in steps W .. W+K-1) / device time of
+settle     = the metric is defined at the calibrated steady operating point
+             (~7.5 Hz; its CPU side-by-side times a window after
+             the onset, "e.g. steps 100-149").  A run starts from V0 ~ U[V_r,
+             V_theta) with a synchronous onset burst, so when W < 200 both arms
+             first step the network S = 200 - W untimed steps (`settle_steps` in
+             the line), then do the W warm-up steps and time exactly K steps.
+             With the default W = 200, S = 0.  --settle overrides.
+value      = (recurrent + external events in steps S+W .. S+W+K-1) / device time of
              those K steps (CUDA events around warm CUDA-graph replays, one sync).
 e2e        = same metric, same steps, through the public step API: wall clock of
              Simulator.advance(K) after advance(W) (the loop run_b200 runs:
@@ -50,6 +57,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+SETTLE_MIN = 200              # untimed steps before the timed window (settle + warm-up)
 BYTES_PER_EVENT = 17          # 9 B CSR record + 8 B deposit
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
@@ -116,6 +124,8 @@ def resolve_defaults(args) -> None:
     config 2 split over the GPUs (the config BASELINE states at 1/2/4/8)."""
     if args.config is None:
         args.config = 1 if n_ranks(args) == 1 else 2
+    if getattr(args, "settle", None) is None:
+        args.settle = max(0, SETTLE_MIN - max(args.warmup, 3))
 
 
 def workload_grid(args, nx: int, ny: int):
@@ -134,8 +144,8 @@ def workload(args):
     from dataclasses import replace
     from paper_1803_08833_b200.presets import baseline_config
     cfg = baseline_config(args.config, args.regime, kernel=args.kernel,
-                          duration_s=(args.warmup + args.steps) / 1000.0, seed=args.seed,
-                          drive_hz=args.drive)
+                          duration_s=(args.settle + args.warmup + args.steps) / 1000.0,
+                          seed=args.seed, drive_hz=args.drive)
     nx, ny = workload_grid(args, cfg.grid.nx, cfg.grid.ny)
     return replace(cfg, grid=replace(cfg.grid, nx=nx, ny=ny))
 
@@ -194,17 +204,17 @@ def run_reference_arm(args):
         return
     from oracle.configs import baseline_config as oracle_config
     from oracle.mp_runner import build_global_csr, run_oracle_mp, tiles
-    W, K = args.warmup, args.steps
+    W, K, S = args.warmup, args.steps, args.settle
     probe = oracle_config(args.config, args.regime, kernel=args.kernel)
     nx, ny = workload_grid(args, probe.grid.nx, probe.grid.ny)
     cfg = oracle_config(args.config, args.regime, kernel=args.kernel,
-                        duration_s=(W + K) / 1000.0, seed=args.seed, drive_hz=args.drive,
+                        duration_s=(S + W + K) / 1000.0, seed=args.seed, drive_hz=args.drive,
                         grid=f"{nx}x{ny}")
     k = next(k for k in range(min(host_threads(), cfg.grid.n_columns), 0, -1)
              if tiles(cfg.grid, k))
     budget = float(os.environ.get("CC_REF_BUDGET_S", "150"))
     row_off, tgt, dly, wgt, gen_s = build_global_csr(cfg, k)
-    r = run_oracle_mp(cfg, row_off, tgt, dly, wgt, k, W + K, budget, warmup=W)
+    r = run_oracle_mp(cfg, row_off, tgt, dly, wgt, k, S + W + K, budget, warmup=S + W)
     steps_t = max(1, r["timed_steps"])
     ms = r["timed_wall_s"] * 1000.0 / steps_t
     sample = (f"oracle/mp_runner.py: numpy oracle of the reference loop on {k} processes "
@@ -212,10 +222,11 @@ def run_reference_arm(args):
               f"connectivity generated by the oracle on {k} processes ({len(wgt)} synapses, "
               f"{gen_s:.0f} s); steps 0..{r['steps'] - 1} from t=0 run, the last {steps_t} "
               f"timed ({r['timed_events']} events in {r['timed_wall_s']:.1f} s)"
-              + ("; stopped by the time budget" if r["steps"] < W + K else ""))
+              + ("; stopped by the time budget" if r["steps"] < S + W + K else ""))
     line = {
         "metric": "synaptic events/s (recurrent + external)", "value": r["value"],
         "unit": "events/s", "n_gpus": args.gpus, "steps": steps_t, "warmup": W,
+        "settle_steps": S,
         "ms_per_step": ms, "higher_is_better": True, "scaling": scaling_of(args),
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded counter-based RNG; connectivity and drive bit-exact with "
@@ -273,6 +284,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--settle", type=int, default=None,
+                    help="untimed steps from t = 0 before the warm-up (default: what is "
+                         "missing to 200 untimed steps, so that the timed window is the "
+                         "steady operating point and not the onset burst)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=None,
                     help="BASELINE config (default: 1 on one GPU, 2 on N > 1 GPUs)")
@@ -344,6 +359,8 @@ def _bench_single(args, cfg, net, capacity):
     CH = max(d for d in range(1, min(args.chunk, W, K) + 1) if K % d == 0)
     sim = Simulator(cfg, net, chunk=CH, raster_steps=K + CH, bin_cap=args.bin_cap,
                     capacity=capacity)
+    if args.settle:
+        sim.advance(args.settle, collect_raster=False)     # onset -> steady operating point
     sim.advance(W - CH)                                    # warm-up (eager + graphs)
     sim.check()
     g_main = sim.capture(CH)
@@ -442,6 +459,7 @@ def _bench_single(args, cfg, net, capacity):
     line = {
         "metric": "synaptic events/s (recurrent + external)",
         "value": value, "unit": "events/s", "n_gpus": 1, "steps": K, "warmup": W,
+        "settle_steps": args.settle,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: seeded counter-based RNG (connectivity, Poisson drive), "
@@ -533,6 +551,8 @@ def _bench_single(args, cfg, net, capacity):
                     "import_seconds": imp_s}
             del store
         sim2 = Simulator(cfg, net2, chunk=min(args.chunk, K), raster_steps=K, capacity=capacity)
+        if args.settle:
+            sim2.advance(args.settle, collect_raster=False)
         sim2.advance(W)
         ca = sim2.check()
         torch.cuda.synchronize(dev)

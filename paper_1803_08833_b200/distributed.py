@@ -905,6 +905,9 @@ def bench_distributed(args, cfg) -> Optional[dict]:
             d = DistributedSimulator(cfg, rank, size, device=f"cuda:{dev_idx}", group=group,
                                      nccl_group=nccl_group, transport=tr, sync=sync,
                                      loopback=loop, raster_steps=args.steps + 100)
+            settle = int(getattr(args, "settle", 0) or 0)
+            if settle:
+                d.advance(settle, collect_raster=False)    # onset -> steady operating point
             d.advance(args.warmup)
             if tr == "p2p" and os.environ.get("CC_TEST_P2P_FAIL"):      # tests
                 raise _lib.EngineError("step 0: injected peer-exchange failure", 0x400)
@@ -976,7 +979,9 @@ def bench_distributed(args, cfg) -> Optional[dict]:
         line = {
             "metric": "synaptic events/s (recurrent + external)",
             "value": total / (ms_v / 1e3), "unit": "events/s", "n_gpus": size,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_v / args.steps,
+            "steps": args.steps, "warmup": args.warmup,
+            "settle_steps": int(getattr(args, "settle", 0) or 0),
+            "ms_per_step": ms_v / args.steps,
             "higher_is_better": True,
             "scaling": "weak" if (size > 1 and getattr(args, "scaling", "strong") == "weak")
             else "strong",

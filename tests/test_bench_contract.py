@@ -17,7 +17,7 @@ import bench  # noqa: E402
 
 def _args(**kw):
     a = dict(gpus=1, steps=10, warmup=3, config=None, kernel=None, drive=None, seed=1,
-             grid=None, scaling="strong", regime="calibrated")
+             grid=None, scaling="strong", regime="calibrated", settle=None)
     a.update(kw)
     ns = argparse.Namespace(**a)
     bench.resolve_defaults(ns)
@@ -63,7 +63,8 @@ def test_reference_arm_config_is_the_gpu_arm_config(monkeypatch):
     for idx, regime in ((1, "calibrated"), (2, "calibrated"), (2, "stress"), (0, "literal")):
         a = _args(config=idx, regime=regime)
         g = bench.workload(a)
-        o = oc(idx, regime, duration_s=(a.warmup + a.steps) / 1000.0)
+        assert a.settle == 200 - a.warmup                 # 200 untimed steps before the window
+        o = oc(idx, regime, duration_s=(a.settle + a.warmup + a.steps) / 1000.0)
         assert (o.grid.nx, o.grid.ny, o.grid.n_neurons) == (g.grid.nx, g.grid.ny, g.grid.n_neurons)
         for k in ("kind", "amplitude_A", "scale", "cutoff_p", "local_p"):
             assert getattr(o.kernel, k) == getattr(g.kernel, k), k
@@ -129,6 +130,7 @@ def test_bench_line_contract():
                 "roofline", "clocks", "e2e", "gpu_launches", "cpu_baseline"):
         assert key in line, key
     assert line["n_gpus"] == 1 and line["steps"] == 20 and line["warmup"] == 5
+    assert line["settle_steps"] == 195                    # timed window: steps 200 .. 219
     assert line["value"] > 0 and line["ms_per_step"] > 0 and line["higher_is_better"]
     assert line["config"]["workload"].startswith("BASELINE config 1")
     assert line["config"]["neurons"] == 79360
