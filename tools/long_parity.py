@@ -2,7 +2,9 @@
 oracle (numpy port of the reference loop, pinned to the reference's own
 fixtures) on the same connectivity, over the config's whole duration.
 
-    python tools/long_parity.py [CONFIG] [DURATION_S] [SHARDS] [REGIME]
+    python tools/long_parity.py [CONFIG] [DURATION_S] [SHARDS] [REGIME] [GRID]
+
+GRID (e.g. 48x24: one GPU's block of config 4) replaces the config's grid.
 
 SHARDS > 1 runs the multi-shard path (distributed.run_local_shards: W column
 blocks with their own generator, spike exchange by device copies) on one GPU.
@@ -30,6 +32,11 @@ def main():
     shards = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     regime = sys.argv[4] if len(sys.argv) > 4 else "calibrated"
     cfg = baseline_config(idx, regime, duration_s=dur)
+    grid = sys.argv[5] if len(sys.argv) > 5 else ""
+    if grid:
+        from dataclasses import replace
+        nx, ny = (int(v) for v in grid.lower().split("x"))
+        cfg = replace(cfg, grid=replace(cfg.grid, nx=nx, ny=ny))
     net = build_b200(cfg)
     t0 = time.perf_counter()
     if shards > 1:
@@ -74,7 +81,7 @@ def main():
     print(json.dumps(out))
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     name = (f"long_parity_config{idx}" + (f"_{shards}shards" if shards > 1 else "")
-            + ("" if regime == "calibrated" else f"_{regime}"))
+            + ("" if regime == "calibrated" else f"_{regime}") + (f"_{grid}" if grid else ""))
     with open(os.path.join(ROOT, "gpurun_out", name + ".json"), "w") as fh:
         json.dump(out, fh, indent=1)
     ok = same_g and same_t and out["recurrent_events"][0] == out["recurrent_events"][1] \
