@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CC_ABI_VERSION 28
+#define CC_ABI_VERSION 29
 
 /* Input sub-lists per 32-neuron group, by target lane range: sub-list j of a
  * group holds the events of its lanes [32 j / n, 32 (j + 1) / n).  The library
@@ -48,6 +48,7 @@ extern "C" {
 #define CC_L1_MAX_REGIONS 2048
 #define CC_L1_MAX_LISTS 1024
 #define CC_L1_STRIDE 32
+#define CC_L1_NCNT_MAX_RB 12
 
 /* cc_shard.flags: measurement / test modes.  NO_TAIL_DELIVERY: k_stage's idle
  * warps do not deliver the next step's delay >= 2 events, so cc_deliver
@@ -268,6 +269,12 @@ typedef struct cc_shard {
     uint32_t* l1_ref;       /* [n_regions][l1_cap]                              */
     uint32_t* l1_w;         /* [n_regions][l1_cap]                              */
     uint16_t* l1_tgt;       /* [n_regions][l1_cap]                              */
+    /* optional (l1_rb <= CC_L1_NCNT_MAX_RB): k_bin also counts the records it
+     * stores per target neuron, so that the planning pass takes a neuron's
+     * recurrent input count from here instead of reading the group's records;
+     * every list record of the step must then come through k_bin (no tail
+     * delivery).  The planning pass zeroes what it reads. */
+    uint32_t* l1_ncnt;      /* [2][n_groups * 32] records per neuron, by step parity, or NULL */
 } cc_shard;
 
 /* ---------------------------------------------------------------- misc */

@@ -15,9 +15,9 @@ __all__ = ["lib", "Pop", "Ctl", "Shard", "Gen", "XPeer", "check", "EngineError",
 
 LIB_PATH = os.environ.get("CC_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libcorticarc_b200.so")
-ABI_VERSION = 28
+ABI_VERSION = 29
 ITEM_CLASSES = 8
-L1_MAX_REGIONS, L1_MAX_LISTS, L1_STRIDE = 2048, 1024, 32   # CC_L1_* (include/corticarc_b200.h)
+L1_MAX_REGIONS, L1_MAX_LISTS, L1_STRIDE, L1_NCNT_MAX_RB = 2048, 1024, 32, 12   # CC_L1_* (include/corticarc_b200.h)
 FLAG_NO_TAIL_DELIVERY = 0x1000   # CC_FLAG_NO_TAIL_DELIVERY (include/corticarc_b200.h)
 
 ERR_BITS = {
@@ -108,7 +108,7 @@ class Shard(C.Structure):
         ("n_ranks", C.c_int32), ("rank", C.c_int32), ("xmask", _P), ("xdst", _P), ("xsrc", _P),
         ("xcnt", _P), ("xwait_ns", C.c_int64),
         ("l1_rb", C.c_int32), ("n_regions", C.c_int32), ("l1_cap", C.c_int64),
-        ("l1_cnt", _P), ("l1_ref", _P), ("l1_w", _P), ("l1_tgt", _P),
+        ("l1_cnt", _P), ("l1_ref", _P), ("l1_w", _P), ("l1_tgt", _P), ("l1_ncnt", _P),
     ]
 
 

@@ -263,10 +263,20 @@ constexpr int BN_T = BN_THREADS * BN_PER_THREAD;       // records per tile
 static_assert(CC_L1_MAX_LISTS == BN_LPT * BN_THREADS && CC_L1_MAX_REGIONS == BN_RPT * BN_THREADS,
               "k_bin scans whole lists / regions per thread");
 
-constexpr size_t bin_smem_bytes() {
+// (ncnt_rb: log2 of the per-neuron counters behind the tile arrays, -1: none)
+constexpr size_t bin_smem_bytes(int ncnt_rb = -1) {
     return (size_t)BN_T * (8 + 2) + (size_t)CC_L1_MAX_LISTS * 4 * 3 +
-           (size_t)(CC_L1_MAX_REGIONS + 1) * 4;
+           ((size_t)(CC_L1_MAX_REGIONS + 1) * 4 + 15) / 16 * 16 +
+           (ncnt_rb >= 0 ? ((size_t)4 << ncnt_rb) : 0);
 }
+// Per-neuron counts: CC_BN_TEAM blocks share a contiguous range of tiles (one
+// region after the other), so that a block meets few regions and can keep its
+// counts in shared memory, while the blocks running at a time still touch
+// few regions' lists (fully contiguous ranges - a team of 1 - put 296 regions'
+// lists in flight: k_bin +49 us at the stress point of config 2).
+#ifndef CC_BN_TEAM
+#define CC_BN_TEAM 4
+#endif
 
 __global__ void __launch_bounds__(BN_THREADS, CC_BN_MINB)
 k_bin(const cc_shard sh) {
@@ -279,7 +289,9 @@ k_bin(const cc_shard sh) {
     uint32_t* s_start = s_hist + CC_L1_MAX_LISTS;
     uint32_t* s_base = s_start + CC_L1_MAX_LISTS;
     uint32_t* s_tpre = s_base + CC_L1_MAX_LISTS;             // [n_regions + 1] tile prefix
-    uint16_t* s_list = reinterpret_cast<uint16_t*>(s_tpre + CC_L1_MAX_REGIONS + 1);
+    uint32_t* s_ncnt = s_tpre + (CC_L1_MAX_REGIONS + 1 + 3) / 4 * 4;   // [2^RB] if sh.l1_ncnt
+    const bool count_n = sh.l1_ncnt != nullptr;
+    uint16_t* s_list = reinterpret_cast<uint16_t*>(s_ncnt + (count_n ? (1 << sh.l1_rb) : 0));
     __shared__ uint32_t s_wsum[33];
     const int RB = sh.l1_rb;
     const int n_reg = sh.n_regions;
@@ -315,8 +327,41 @@ k_bin(const cc_shard sh) {
         for (int r = threadIdx.x; r < n_reg; r += BN_THREADS) other[(size_t)r * CC_L1_STRIDE] = 0u;
     }
     for (int l = threadIdx.x; l < CC_L1_MAX_LISTS; l += BN_THREADS) s_hist[l] = 0u;
+    if (count_n)
+        for (int n = threadIdx.x; n < (1 << RB); n += BN_THREADS) s_ncnt[n] = 0u;
     __syncthreads();
-    for (uint32_t it = blockIdx.x; it < total_tiles; it += gridDim.x) {
+    // per-neuron counts (sh.l1_ncnt): the block accumulates the records it
+    // stores per neuron in shared memory and adds them to the global counts
+    // when it leaves a region; its team's tiles are a contiguous range, dealt
+    // round-robin inside the team.  Without the counts the tiles are dealt
+    // round-robin over the whole grid.
+    uint32_t* ncnt = count_n ? sh.l1_ncnt + (size_t)(t & 1) * sh.n_groups * 32 : nullptr;
+    auto flush_counts = [&](int reg) {           // block-wide; barriers by the caller
+        const size_t base = (size_t)reg << RB;
+        for (int n = threadIdx.x; n < (1 << RB); n += BN_THREADS) {
+            const uint32_t c = s_ncnt[n];
+            if (c) {
+                CC_CHK(ctl, base + n < (size_t)sh.n_groups * 32);
+                atomicAdd(&ncnt[base + n], c);
+                s_ncnt[n] = 0u;
+            }
+        }
+    };
+    uint32_t it_first = blockIdx.x, it_end = total_tiles, it_step = gridDim.x;
+    if (count_n) {
+        const unsigned team = min((unsigned)CC_BN_TEAM, gridDim.x);
+        const unsigned n_teams = gridDim.x / team;             // (blocks past the last full team idle)
+        const unsigned g = blockIdx.x / team, m = blockIdx.x % team;
+        if (g < n_teams) {
+            it_first = (uint32_t)((unsigned long long)total_tiles * g / n_teams) + m;
+            it_end = (uint32_t)((unsigned long long)total_tiles * (g + 1) / n_teams);
+        } else {
+            it_first = it_end = 0u;
+        }
+        it_step = team;
+    }
+    int cur_reg = -1;
+    for (uint32_t it = it_first; it < it_end; it += it_step) {
         // region of tile `it`: last r with s_tpre[r] <= it
         int lo = 0, hi = CC_L1_MAX_REGIONS;
         while (hi - lo > 1) {
@@ -325,6 +370,10 @@ k_bin(const cc_shard sh) {
         }
         const int reg = lo;
         CC_CHK(ctl, reg < n_reg && s_tpre[reg] <= it && it < s_tpre[reg + 1]);
+        if (count_n && reg != cur_reg) {
+            if (cur_reg >= 0) { flush_counts(cur_reg); __syncthreads(); }
+            cur_reg = reg;
+        }
         const uint32_t n_r = (uint32_t)min((size_t)gcnt[(size_t)reg * CC_L1_STRIDE], cap);
         const uint32_t j0 = (it - s_tpre[reg]) * BN_T;
         const uint32_t n_t = min((uint32_t)BN_T, n_r - j0);
@@ -347,6 +396,8 @@ k_bin(const cc_shard sh) {
             if (j < n_t) {
                 const unsigned l = list_of((int)tg[k], 0);
                 CC_CHK(ctl, l < (unsigned)nl);
+                // (per-neuron counts: every record here, overflowed ones taken back below)
+                if (count_n) atomicAdd(&s_ncnt[tg[k]], 1u);
                 tg[k] |= atomicAdd(&s_hist[l], 1u) << 16;
             }
         }
@@ -394,6 +445,9 @@ k_bin(const cc_shard sh) {
             if (pos < (uint32_t)K) {
                 S.rec[(size_t)(list0 + l) * KS + pos] = rec;
             } else {                                          // full list: the set's overflow list
+                // (not a list record: taken back from its neuron's count -
+                // the list's group and the record's lane)
+                if (count_n) atomicSub(&s_ncnt[((l / NSUB) << 5) | ((uint32_t)rec & 31u)], 1u);
                 const unsigned o = atomicAdd(S.ovf_cnt, 1u);
                 atomicAdd(&ctl->ovf_total, 1ull);
                 const uint32_t lo32 = (uint32_t)rec;
@@ -406,5 +460,6 @@ k_bin(const cc_shard sh) {
         }
         __syncthreads();
     }
+    if (count_n && cur_reg >= 0) flush_counts(cur_reg);
     deliver_epilogue(sh, S, 0ull);
 }

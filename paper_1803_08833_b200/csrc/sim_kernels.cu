@@ -732,7 +732,18 @@ __device__ __forceinline__ void plan_group(const cc_shard& sh, long long t, int 
     const uint32_t c_ovf = ovf_all ? (uint32_t)max(0ll, min((long long)ovf_all, sh.ovf_cap - o0)) : 0u;
     __syncwarp();
     const uint64_t* lst = S.rec + (size_t)group * NSUB * KS;
-    for (uint32_t r0 = 0; r0 < c_list; r0 += 32 * 8) {
+    // routed delivery with per-neuron counts: k_bin counted the records it
+    // stored per neuron (every list record of the step came through it), so the
+    // records need not be read here; the counts are zeroed for step t + 2
+    if (sh.l1_ncnt) {
+        if (gvalid) {
+            uint32_t* nc = sh.l1_ncnt + (size_t)(t & 1) * sh.n_groups * 32 + (size_t)group * 32 + lane;
+            lane_cnt[wib][lane] = *nc;
+            *nc = 0u;
+        }
+        __syncwarp();
+    }
+    for (uint32_t r0 = 0; r0 < (sh.l1_ncnt ? 0u : c_list); r0 += 32 * 8) {
         uint32_t v[8];                             // 8 loads in flight per lane
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -1157,7 +1168,7 @@ k_stage(const cc_shard sh) {
     const int D = sh.d_max;
     unsigned* const a_n = reinterpret_cast<unsigned*>(nsm + STAGE_WARPS * stage_warp_bytes());
     unsigned* const a_pre = a_n + D;
-    const bool tail_deliver = D > 1 && !(sh.flags & CC_FLAG_NO_TAIL_DELIVERY);
+    const bool tail_deliver = D > 1 && !(sh.flags & CC_FLAG_NO_TAIL_DELIVERY) && !sh.l1_ncnt;
     if (tail_deliver) unit_prefix(sh, slot_add(t_mod_l, 1, sh.log_slots), D - 1, a_n, a_pre);
     // queued items per size class (k_plan is complete); claimed largest first
     __shared__ unsigned cls_n[CC_ITEM_CLASSES];
@@ -2050,6 +2061,7 @@ extern "C" int CC_V(cc_init_state)(const cc_shard* sh, void* stream) {
 }
 
 static int bin_blocks_per_sm = 0;
+static int bin_blocks_per_sm_ncnt[CC_L1_NCNT_MAX_RB + 1] = {0};   // with per-neuron counters, by l1_rb
 extern "C" int CC_V(cc_prepare)(void);
 
 extern "C" int CC_V(cc_deliver)(const cc_shard* sh, void* stream) {
@@ -2072,8 +2084,18 @@ extern "C" int CC_V(cc_deliver)(const cc_shard* sh, void* stream) {
     k_route<<<CC_RT_BLOCKS ? CC_RT_BLOCKS : sm_count() * CC_RT_MINB, RT_THREADS, route_smem_bytes(),
               (cudaStream_t)stream>>>(*sh);
     if (const int rc = cc_check_launch("k_route")) return rc;
-    k_bin<<<sm_count() * bin_blocks_per_sm, BN_THREADS, bin_smem_bytes(),
-            (cudaStream_t)stream>>>(*sh);
+    if (sh->l1_ncnt) {
+        if (sh->l1_rb > CC_L1_NCNT_MAX_RB)
+            return cc_set_error("cc_deliver: l1_ncnt needs l1_rb <= %d", CC_L1_NCNT_MAX_RB);
+        if (!(sh->flags & CC_FLAG_NO_TAIL_DELIVERY))
+            return cc_set_error("cc_deliver: l1_ncnt needs CC_FLAG_NO_TAIL_DELIVERY (every list "
+                                "record must come through k_bin)");
+        k_bin<<<sm_count() * bin_blocks_per_sm_ncnt[sh->l1_rb], BN_THREADS,
+                bin_smem_bytes(sh->l1_rb), (cudaStream_t)stream>>>(*sh);
+    } else {
+        k_bin<<<sm_count() * bin_blocks_per_sm, BN_THREADS, bin_smem_bytes(),
+                (cudaStream_t)stream>>>(*sh);
+    }
     return cc_check_launch("k_bin");
 }
 
@@ -2097,12 +2119,17 @@ extern "C" int CC_V(cc_prepare)(void) {
     if (cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)route_smem_bytes()) != cudaSuccess ||
         cudaFuncSetAttribute(k_bin, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)bin_smem_bytes()) != cudaSuccess)
+                             (int)bin_smem_bytes(CC_L1_NCNT_MAX_RB)) != cudaSuccess)
         return cc_set_error("cc_prepare (routed delivery): %s",
                             cudaGetErrorString(cudaGetLastError()));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bin_blocks_per_sm, k_bin, BN_THREADS,
                                                   bin_smem_bytes());
     if (bin_blocks_per_sm < 1) bin_blocks_per_sm = 1;
+    for (int rb = 5; rb <= CC_L1_NCNT_MAX_RB; ++rb) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bin_blocks_per_sm_ncnt[rb], k_bin,
+                                                      BN_THREADS, bin_smem_bytes(rb));
+        if (bin_blocks_per_sm_ncnt[rb] < 1) bin_blocks_per_sm_ncnt[rb] = 1;
+    }
     // (filled here, outside any stream capture; the tail tables grow by 16 B
     // per two delay steps, so the occupancy changes at a few d_max values only)
     int per_sm[2] = {0, 0};

@@ -284,6 +284,10 @@ class Simulator:
                 l1_ref=T.empty((n_regions, l1_cap), dtype=i32, device=dev),
                 l1_w=T.empty((n_regions, l1_cap), dtype=i32, device=dev),
                 l1_tgt=T.empty((n_regions, l1_cap), dtype=T.int16, device=dev))
+            # per-neuron record counts from k_bin: the planning pass then does
+            # not read the lists' records (CC_L1_NCNT=0: it counts them itself)
+            if rb <= _lib.L1_NCNT_MAX_RB and int(os.environ.get("CC_L1_NCNT", "1")):
+                self.buf["l1_ncnt"] = T.zeros(2 * n_groups * 32, dtype=i32, device=dev)
         self.probes = None if probes is None else np.asarray(probes, np.int64)
         n_probe = 0 if self.probes is None else len(self.probes)
         if n_probe:
@@ -303,6 +307,8 @@ class Simulator:
             sh.l1_rb, sh.n_regions, sh.l1_cap = rb, n_regions, l1_cap
             for k in ("l1_cnt", "l1_ref", "l1_w", "l1_tgt"):
                 setattr(sh, k, b[k].data_ptr())
+            if "l1_ncnt" in b:
+                sh.l1_ncnt = b["l1_ncnt"].data_ptr()
             # the tail delivery's scattered deposits are what this mode avoids
             sh.flags |= _lib.FLAG_NO_TAIL_DELIVERY
         sh.spk_cap, sh.seg_stride = spk_cap, seg_stride

@@ -302,6 +302,23 @@ def test_routed_delivery_same_run(cuda, name, sublists, rb, monkeypatch):
     assert 0.9 * c.rec_events < c.del_events <= c.rec_events
 
 
+@pytest.mark.parametrize("name", ["config0_cal", "tiny_gauss_long"])
+def test_routed_delivery_planning_counts_records_itself(cuda, name, monkeypatch):
+    """Routed delivery without k_bin's per-neuron counts (CC_L1_NCNT=0: the
+    planning pass reads the lists' records as in the direct mode) - the same
+    run; with them (the default) the shard carries the count array."""
+    from paper_1803_08833_b200.engine import Simulator, run_b200
+    from paper_1803_08833_b200.network import build_b200
+    cfg, meta, arr = golden_run(name)
+    monkeypatch.setenv("CC_ROUTED", "1")
+    net = build_b200(cfg)
+    assert Simulator(cfg, net).shard.l1_ncnt
+    monkeypatch.setenv("CC_L1_NCNT", "0")
+    assert not Simulator(cfg, net).shard.l1_ncnt
+    _assert_same_run(run_b200(cfg, 1, net=net), meta, arr)
+    _assert_same_run(run_b200(cfg, 1, net=net, bin_cap=2), meta, arr)
+
+
 def test_routed_delivery_list_overflow_and_region_capacity(cuda, monkeypatch):
     """Routed delivery with 2-record input lists (k_bin's overflow path) gives
     the reference raster; a region array too small for a step's records stops
