@@ -315,7 +315,10 @@ class Simulator:
         # delivery lanes per spike: 16 on shards of >= 2 M neurons (config 3 gaussian: k_deliver
         # 448 -> 367 us, step -3.3 %), 8 below (configs 1, 2 and the config-4 GPU block: 16 lanes are ~1 % slower);
         # CC_DEL_LPS overrides for experiments (profiles/r01l_delivery_sweep.md)
-        lps = int(os.environ.get("CC_DEL_LPS", "0")) or (16 if n_local >= DEL_WIDE_NEURONS else 8)
+        # (k_route, whose tile staging is indifferent to the run structure: 16 lanes
+        # - config 2 stress point, delivery 779 -> 752 us)
+        lps = int(os.environ.get("CC_DEL_LPS", "0")) or (
+            16 if n_local >= DEL_WIDE_NEURONS or self.routed else 8)
         if lps not in (8, 16):
             raise ValueError(f"CC_DEL_LPS must be 8 or 16, got {lps}")
         sh.del_lps_log2 = lps.bit_length() - 1

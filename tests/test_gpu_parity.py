@@ -291,6 +291,9 @@ def test_routed_delivery_same_run(cuda, name, sublists, rb, monkeypatch):
     monkeypatch.setenv("CC_SUBLISTS", sublists)
     res = run_b200(cfg, 1)
     _assert_same_run(res, meta, arr)
+    monkeypatch.setenv("CC_DEL_LPS", "8")              # (routed default: 16 lanes per spike)
+    _assert_same_run(run_b200(cfg, 1), meta, arr)
+    monkeypatch.delenv("CC_DEL_LPS")
     sim = Simulator(cfg, build_b200(cfg))
     assert sim.routed and sim.shard.l1_rb == int(rb)
     assert sim.kernels_per_step() == Simulator(cfg, sim.net, routed=False).kernels_per_step() + 1
